@@ -1,0 +1,233 @@
+/*
+ * forkkv.h — C ABI of the B200-native ForkKV ResidualAttention hot path.
+ *
+ * ForkKV (arxiv 2604.06370, /root/reference/PAPER.md) serves many LoRA agents
+ * forked from a shared context by disaggregating each agent's KV cache into
+ *   bCache = xW   (K stored post-RoPE; shared zero-copy by every agent that
+ *                  holds the same tokens)                  P:269 §5.1, Eq.2
+ *   rCache = xA_i (rank r, per agent, stored without RoPE)  P:130-134 §2.2
+ * tracked by a DualRadixTree (base tree keyed by token ids, residual tree
+ * keyed by agent id + token ids, §5.2) with OS-style fork + copy-on-write
+ * (§5.2), and by ResidualAttention (Alg.1, Eq.4)
+ * which rebuilds K = K_base + RoPE(K_res B_k) and V = V_base + V_res B_v on
+ * chip so a full per-agent K/V never reaches HBM.
+ *
+ * Ownership
+ *   - Device memory (pools, RoPE table, adapters, Q, O, plan buffers,
+ *     workspace) is CALLER-owned and passed as raw pointers; the library only
+ *     borrows it. The caller keeps it alive until fkv_destroy / plan free.
+ *   - The library owns all host metadata (pools, tables, trees, plans).
+ *   - Streams are caller-supplied (cudaStream_t passed as void*; NULL = the
+ *     legacy default stream). Nothing synchronises internally except where a
+ *     function says so.
+ * Errors
+ *   Every call returns fkv_status (int32). Nothing throws or aborts across
+ *   the ABI. fkv_last_error(ctx) returns a message for the last failure on
+ *   that ctx. Mutating calls are atomic: on failure tables, refcounts and
+ *   trees are unchanged ("never silently evicts").
+ * Concurrency
+ *   One mutation gate: a ctx is not thread-safe; the caller serialises calls
+ *   on a ctx. Kernels enqueued on streams may run concurrently.
+ * Host-only mode
+ *   fkv_config.device = -1 creates a control-plane-only ctx (no CUDA calls;
+ *   kernels are skipped, data pointers may be NULL). Used by CPU tests.
+ */
+#ifndef FORKKV_H_
+#define FORKKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t fkv_status;
+enum {
+  FKV_OK = 0,
+  FKV_E_INVALID = 1,          /* dimension/shape/argument mismatch */
+  FKV_E_NEEDS_EVICTION = 2,   /* a pool is exhausted; nothing evicted */
+  FKV_E_UNKNOWN_AGENT = 3,    /* no such agent */
+  FKV_E_STALE = 4,            /* plan built against an older table generation */
+  FKV_E_READONLY = 5,         /* write to a page with more than one holder */
+  FKV_E_NO_KEYS = 6,          /* a causal query row has no keys */
+  FKV_E_UNWRITTEN = 7,        /* attention would read rows never written */
+  FKV_E_CUDA = 8              /* CUDA error; message from cudaGetErrorString */
+};
+
+enum { FKV_DTYPE_BF16 = 0, FKV_DTYPE_F32 = 1 };
+/* Residual-key RoPE (reading C-1). DEFERRED = the paper's
+ * K_lora = RoPE(K_res B_k) at the key's absolute position (Alg1.335).
+ * NONE = no rotation of the residual term, i.e. the north-star split
+ * q.(K_base + R_K B_K)^T = q K_base^T + (q B_K^T) R_K^T (exact only then). */
+enum { FKV_ROPE_NONE = 0, FKV_ROPE_DEFERRED = 1 };
+enum { FKV_KIND_BASE = 0, FKV_KIND_RES = 1 };
+
+#define FKV_FORK_SHARE_RESIDUAL 1u  /* same-agent branch: share residual pages CoW (C-12) */
+
+#define FKV_WRITE_KBASE 1u
+#define FKV_WRITE_VBASE 2u
+#define FKV_WRITE_RK 4u
+#define FKV_WRITE_RV 8u
+
+#define FKV_PLAN_CHECK_WRITTEN 1u   /* verify every key row of every layer was written */
+#define FKV_PLAN_FORCE_SIMT 2u      /* use the plain SIMT kernel (fp32 path is always SIMT) */
+
+typedef struct fkv_config {
+  int32_t n_layers;       /* L */
+  int32_t n_q_heads;      /* Hq (whole model; the shard holds heads of [kv_head_begin, kv_head_end)) */
+  int32_t n_kv_heads;     /* Hkv (whole model) */
+  int32_t head_dim;       /* d: 64 or 128 (bf16 tensor-core path needs 128; SIMT path: even, <=256) */
+  int32_t rank;           /* r: LoRA rank of the residual pool; adapters of smaller rank are zero-padded (C-8) */
+  int32_t page_size;      /* P: tokens per page, one of 16, 32, 64 (C-9) */
+  int64_t n_base_pages;   /* pages in the bCache pool */
+  int64_t n_res_pages;    /* pages in the rCache pool */
+  int32_t max_pos;        /* rows of the RoPE table */
+  int32_t dtype;          /* FKV_DTYPE_*: element type of pools, adapters, Q and O */
+  int32_t rope_mode;      /* FKV_ROPE_* */
+  int32_t device;         /* CUDA device ordinal, or -1 for a host-only control plane */
+  uint64_t alloc_order_seed; /* 0: ascending page ids; else seeded rank order (C-11) */
+  int32_t kv_head_begin;  /* KV-head shard [begin, end) held by this ctx (§8(e)); 0,0 = all */
+  int32_t kv_head_end;
+} fkv_config;
+
+/* Device pools (caller-owned), element type = config.dtype.
+ *   base_k, base_v : [L][n_base_pages][Hkv_local][P][d]   (K post-RoPE)
+ *   res_k,  res_v  : [L][n_res_pages][P][r]                (no RoPE)
+ *   rope_cos, rope_sin : fp32 [max_pos][d/2], built host-side in fp64
+ *                        (fkv_build_rope_table) — reading C-2, SURVEY H7. */
+typedef struct fkv_buffers {
+  void* base_k;
+  void* base_v;
+  void* res_k;
+  void* res_v;
+  const float* rope_cos;
+  const float* rope_sin;
+} fkv_buffers;
+
+typedef struct fkv_ctx fkv_ctx;
+typedef struct fkv_plan fkv_plan;
+
+/* One sequence of a batch: the agent's block table and length define the
+ * keys; its query rows are the LAST q_len positions (decode: q_len = 1;
+ * chunked prefill: q_len = chunk). Causal: the query at position p sees keys
+ * t <= p (C-6). */
+typedef struct fkv_seq {
+  int64_t agent;
+  int32_t q_len;
+  int32_t pad_;
+} fkv_seq;
+
+typedef struct fkv_plan_info {
+  int64_t n_seqs, n_rows, n_segments, n_items, n_ctas, n_warps, n_entries;
+  int64_t key_tiles;        /* 64-key tiles summed over CTAs (one layer) */
+  int64_t alg_bytes;        /* algorithmic HBM bytes per layer (SURVEY §8(d) formula) */
+  int64_t kernel;           /* 0 = tensor-core grouped (mma), 1 = SIMT, 2 = tcgen05 */
+  int64_t device_bytes;     /* bytes fkv_plan_upload needs */
+  int64_t workspace_bytes;  /* bytes fkv_residual_attention needs */
+} fkv_plan_info;
+
+/* ---- lifetime ------------------------------------------------------- */
+fkv_status fkv_create(const fkv_config* cfg, const fkv_buffers* buf, fkv_ctx** out);
+fkv_status fkv_destroy(fkv_ctx* ctx);
+const char* fkv_last_error(const fkv_ctx* ctx);
+const char* fkv_version(void);
+
+/* Register adapter `adapter_id` (>= 0): B_K, B_V device arrays
+ * [L][Hkv_local][r][d] (the kv-head column slices of B), LoRA alpha/r
+ * folded in (C-7). Borrowed. Re-registering an id replaces the pointers and
+ * invalidates existing plans (E_STALE). */
+fkv_status fkv_register_adapter(fkv_ctx* ctx, int32_t adapter_id, const void* B_K, const void* B_V);
+
+/* ---- control plane (R1-R9) ----------------------------------- */
+/* New agent with empty tables; its residual tree key is itself (R3). */
+fkv_status fkv_create_root(fkv_ctx* ctx, int64_t agent, int32_t adapter_id);
+/* Fork `child` from `parent`'s first prefix_len tokens: base pages
+ * [0, ceil(L/P)) are shared read-only (+1 ref each, a partial tail page is
+ * copied on first write, C-10); residual pages are fresh and exclusive
+ * (CoW footprint; the caller writes the child's residual rows), or shared CoW
+ * with FKV_FORK_SHARE_RESIDUAL (same adapter required). Atomic. */
+fkv_status fkv_fork(fkv_ctx* ctx, int64_t parent, int64_t prefix_len, int64_t child, int32_t adapter_id,
+                    uint32_t flags);
+/* Step 1 of P:300 by token ids: longest full-page prefix match in the base
+ * radix tree; matched pages are mapped (+1 each), fresh residual pages are
+ * allocated for them, seqlen = *matched. The caller appends the rest. */
+fkv_status fkv_fork_tokens(fkv_ctx* ctx, int64_t child, int32_t adapter_id, const int32_t* tokens, int64_t n,
+                           int64_t* matched);
+/* Reserve n_new[i] slots for agents[i] (token ids concatenated in
+ * token_ids). A first write into a page shared by >1 holder copies it
+ * (CoW kernel enqueued on `stream`). Pages that become full are inserted into
+ * both radix trees. Atomic over the whole call (E_NEEDS_EVICTION leaves no
+ * change). */
+fkv_status fkv_append(fkv_ctx* ctx, int32_t n, const int64_t* agents, const int32_t* n_new,
+                      const int32_t* token_ids, void* stream);
+/* Scatter rows [start[i], start[i]+count[i]) of agents[i] for `layer` into
+ * the pools. Device sources, rows concatenated over i:
+ *   k_base, v_base [sum count][Hkv_local][d];  r_k, r_v [sum count][r].
+ * which_mask selects the planes (FKV_WRITE_*). Rows must be reserved; a page
+ * with more than one holder is never written (E_READONLY). A row counts as
+ * written for a pool when one call stores both its K and V. */
+fkv_status fkv_write_kv(fkv_ctx* ctx, int32_t layer, int32_t n, const int64_t* agents, const int64_t* start,
+                        const int32_t* count, const void* k_base, const void* v_base, const void* r_k,
+                        const void* r_v, uint32_t which_mask, void* stream);
+/* Drop the agent's tables; pages reaching refcount 0 return to the free set. */
+fkv_status fkv_release(fkv_ctx* ctx, int64_t agent);
+
+/* ---- introspection (parity tests) -------------------------------------- */
+fkv_status fkv_get_table(const fkv_ctx* ctx, int64_t agent, int64_t cap, int32_t* base_pages,
+                         int32_t* res_pages, int64_t* n_pages, int64_t* seqlen);
+fkv_status fkv_get_agent(const fkv_ctx* ctx, int64_t agent, int32_t* adapter_id, int64_t* residual_owner);
+fkv_status fkv_page_refcount(const fkv_ctx* ctx, int32_t kind, int64_t page, int32_t* rc);
+fkv_status fkv_free_pages(const fkv_ctx* ctx, int32_t kind, int64_t* n_free);
+/* Deterministic text dump of agents, pools and both trees (R8). */
+fkv_status fkv_dump(const fkv_ctx* ctx, char* buf, size_t cap, size_t* needed);
+/* CoW copy log since the last call: quadruples (kind, src, dst, rows). */
+fkv_status fkv_take_copy_log(fkv_ctx* ctx, int32_t* buf, int64_t cap_quads, int64_t* n_quads);
+
+/* ---- the hot path ------------------------------------------------------- */
+/* Build a plan for one batch: groups sequences by shared base-page runs
+ * (agents forked from the same prefix read each shared base tile once),
+ * groups rows by residual owner, picks the KV split. Host only. */
+fkv_status fkv_plan_create(fkv_ctx* ctx, int32_t n, const fkv_seq* seqs, uint32_t flags, fkv_plan** out);
+fkv_status fkv_plan_get_info(const fkv_plan* plan, fkv_plan_info* info);
+/* Copy the plan's device arrays into a caller buffer (>= info.device_bytes,
+ * 256-byte aligned) on `stream`. Must precede fkv_residual_attention. */
+fkv_status fkv_plan_upload(fkv_ctx* ctx, fkv_plan* plan, void* dev, size_t bytes, void* stream);
+/* ResidualAttention for one layer (Alg.1 + Eq.4):
+ *   Q [n_rows_q][Hq_local][d], O same (rows = seqs in plan order, each its
+ *   q_len rows), workspace >= info.workspace_bytes (fp32 partials).
+ * sm_scale <= 0 selects 1/sqrt(d) (C-4). Enqueued on `stream`. */
+fkv_status fkv_residual_attention(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
+                                  float sm_scale, void* workspace, size_t ws_bytes, void* stream);
+/* Same with HOST Q/O (pinned recommended): H2D of Q into dQ, attention,
+ * D2H of dO into O_host, all on `stream`; synchronises the stream. */
+fkv_status fkv_residual_attention_host(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q_host,
+                                       void* O_host, void* dQ, void* dO, float sm_scale, void* workspace,
+                                       size_t ws_bytes, void* stream);
+fkv_status fkv_plan_free(fkv_plan* plan);
+
+/* ---- helpers -------------------------------------------------------------- */
+/* RoPE table in fp64, stored fp32: angle = p * inv_freq[i], inv_freq plain
+ * theta^(-2i/d) or Llama-3.1 scaled (llama3 != 0). Host arrays [max_pos][d/2]. */
+fkv_status fkv_build_rope_table(int32_t max_pos, int32_t d, double theta, int32_t llama3, double factor,
+                                double low_freq_factor, double high_freq_factor, double orig_max_pos,
+                                float* cos_out, float* sin_out);
+/* Device fill with the counter-based synthetic generator of workloads/synth.py
+ * (bit-identical): dst[n_pos][n_head][n_col] = value(seed, kind, owner, layer,
+ * pos0 + i, head0 + h, col) * scale, stored as dtype. */
+fkv_status fkv_synth_fill(void* dst, int32_t dtype, uint64_t seed, int32_t kind, uint64_t owner, int32_t layer,
+                          int64_t pos0, int32_t n_pos, int32_t head0, int32_t n_head, int32_t n_col, float scale,
+                          void* stream);
+/* Head x agent-batch partitioner (§8(e)): choose H kv-head shards and D
+ * agent shards with H*D = G, H | n_kv_heads, minimising per-GPU bytes
+ * base_bytes/H + res_bytes/D (+ replicated base if D > 1). */
+fkv_status fkv_partition(int32_t G, int32_t n_kv_heads, int64_t base_bytes, int64_t res_bytes, int32_t* H,
+                         int32_t* D);
+/* Shard of `rank` under (H, D): kv heads [*h0, *h1), agents [*a0, *a1) of n_agents. */
+fkv_status fkv_partition_shard(int32_t rank, int32_t H, int32_t D, int32_t n_kv_heads, int64_t n_agents,
+                               int32_t* h0, int32_t* h1, int64_t* a0, int64_t* a1);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FORKKV_H_ */

@@ -1,0 +1,342 @@
+// Control plane: page pools, per-agent block tables, fork with copy-on-write,
+// DualRadixTree.  Rules R1-R9 of DESIGN.md ("Control-plane rules"), from
+// PAPER.md §5.1 (P:269 separate bCache/rCache pools), §5.2 (P:291
+// DualRadixTree keys, P:300 two-step fork: prefix match then CoW residual
+// allocation) and P:87/P:219 (no in-place update of shared cache).
+#include <algorithm>
+#include <sstream>
+
+#include "internal.hpp"
+#include "kernels.hpp"
+
+namespace fkv {
+
+namespace {
+
+k::PoolView pool_view(const Ctx& c) {
+  k::PoolView pv{};
+  pv.base_k = c.buf.base_k; pv.base_v = c.buf.base_v; pv.res_k = c.buf.res_k; pv.res_v = c.buf.res_v;
+  pv.nb = c.cfg.n_base_pages; pv.nr = c.cfg.n_res_pages;
+  pv.hkv = c.hkv_local; pv.P = c.cfg.page_size; pv.d = c.cfg.head_dim; pv.r = c.cfg.rank;
+  pv.L = c.cfg.n_layers; pv.dtype = c.cfg.dtype;
+  return pv;
+}
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// R7: page `slot` of `ag` became full: walk/insert its chunks 0..slot in the
+// base tree and in the residual tree under ag.owner. New nodes take one ref.
+void tree_insert(Ctx& c, Agent& ag, int64_t slot) {
+  const int P = c.cfg.page_size;
+  for (int kind = 0; kind < 2; ++kind) {
+    TreeNode* node;
+    if (kind == FKV_KIND_BASE) {
+      node = &c.base_root;
+    } else {
+      auto& root = c.res_roots[ag.owner];
+      if (!root) root = std::make_unique<TreeNode>();
+      node = root.get();
+    }
+    const auto& table = kind == FKV_KIND_BASE ? ag.base : ag.res;
+    for (int64_t k = 0; k <= slot; ++k) {
+      std::vector<int32_t> chunk(ag.tokens.begin() + k * P, ag.tokens.begin() + (k + 1) * P);
+      auto it = node->children.find(chunk);
+      if (it == node->children.end()) {
+        auto nd = std::make_unique<TreeNode>();
+        nd->page = table[k];
+        c.pools[kind].retain(table[k]);
+        c.pools[kind].in_tree[table[k]] = 1;
+        TreeNode* raw = nd.get();
+        node->children.emplace(std::move(chunk), std::move(nd));
+        node = raw;
+      } else {
+        node = it->second.get();
+      }
+    }
+  }
+}
+
+}  // namespace
+
+void ctx_create(Ctx& c, const fkv_config& cfg, const fkv_buffers* buf) {
+  const int P = cfg.page_size;
+  if (cfg.n_layers < 1 || cfg.n_kv_heads < 1 || cfg.n_q_heads < cfg.n_kv_heads ||
+      cfg.n_q_heads % cfg.n_kv_heads != 0 || cfg.head_dim < 2 || (cfg.head_dim & 1) || cfg.head_dim > 256 ||
+      cfg.rank < 1 || cfg.rank > 64 || P < 1 || P > 64 || (64 % P) != 0 || cfg.n_base_pages < 1 ||
+      cfg.n_res_pages < 1 || cfg.n_base_pages > INT32_MAX || cfg.n_res_pages > INT32_MAX || cfg.max_pos < 0 ||
+      (cfg.dtype != FKV_DTYPE_BF16 && cfg.dtype != FKV_DTYPE_F32) ||
+      (cfg.rope_mode != FKV_ROPE_NONE && cfg.rope_mode != FKV_ROPE_DEFERRED))
+    throw Error(FKV_E_INVALID, "invalid fkv_config");
+  c.cfg = cfg;
+  int32_t h0 = cfg.kv_head_begin, h1 = cfg.kv_head_end;
+  if (h0 == 0 && h1 == 0) h1 = cfg.n_kv_heads;
+  if (h0 < 0 || h1 > cfg.n_kv_heads || h0 >= h1) throw Error(FKV_E_INVALID, "invalid kv head shard");
+  c.cfg.kv_head_begin = h0; c.cfg.kv_head_end = h1;
+  c.hkv_local = h1 - h0;
+  c.group = cfg.n_q_heads / cfg.n_kv_heads;
+  c.hq_local = c.hkv_local * c.group;
+  c.device = cfg.device >= 0;
+  c.elem = cfg.dtype == FKV_DTYPE_BF16 ? 2 : 4;
+  if (buf) c.buf = *buf;
+  if (c.device) {
+    if (!buf || !buf->base_k || !buf->base_v || !buf->res_k || !buf->res_v)
+      throw Error(FKV_E_INVALID, "device ctx needs pool buffers");
+    if (cfg.rope_mode == FKV_ROPE_DEFERRED && (!buf->rope_cos || !buf->rope_sin || cfg.max_pos < 1))
+      throw Error(FKV_E_INVALID, "DEFERRED rope needs rope_cos/rope_sin tables");
+    check_cuda(cudaSetDevice(cfg.device), "cudaSetDevice");
+  }
+  c.pools[0].init(cfg.n_base_pages, cfg.alloc_order_seed, cfg.n_layers);
+  c.pools[1].init(cfg.n_res_pages, cfg.alloc_order_seed, cfg.n_layers);
+}
+
+void create_root(Ctx& c, int64_t a, int32_t adapter) {
+  if (c.agents.count(a) || a < 0 || adapter < 0) throw Error(FKV_E_INVALID, "create_root: bad agent/adapter");
+  Agent ag;
+  ag.id = a; ag.adapter = adapter; ag.owner = a;
+  c.agents.emplace(a, std::move(ag));
+  ++c.generation;
+}
+
+void fork(Ctx& c, int64_t parent, int64_t L, int64_t child, int32_t adapter, uint32_t flags, void*) {
+  Agent& p = c.agent(parent);
+  if (c.agents.count(child) || child < 0 || adapter < 0 || L < 0 || L > p.seqlen)
+    throw Error(FKV_E_INVALID, "fork: bad child/adapter/prefix_len");
+  const bool share = flags & FKV_FORK_SHARE_RESIDUAL;
+  if (share && adapter != p.adapter) throw Error(FKV_E_INVALID, "fork: SHARE_RESIDUAL needs the parent's adapter");
+  const int P = c.cfg.page_size;
+  const int64_t k = (L + P - 1) / P;
+  if (!share && c.pools[FKV_KIND_RES].n_free() < k) throw Error(FKV_E_NEEDS_EVICTION, "fork: residual pool exhausted");
+  Agent ch;
+  ch.id = child; ch.adapter = adapter; ch.owner = share ? p.owner : child; ch.seqlen = L;
+  ch.base.assign(p.base.begin(), p.base.begin() + k);
+  for (int32_t pg : ch.base) c.pools[FKV_KIND_BASE].retain(pg);
+  if (share) {
+    ch.res.assign(p.res.begin(), p.res.begin() + k);
+    for (int32_t pg : ch.res) c.pools[FKV_KIND_RES].retain(pg);
+  } else {
+    for (int64_t i = 0; i < k; ++i) ch.res.push_back(c.pools[FKV_KIND_RES].alloc());
+  }
+  ch.tokens.assign(p.tokens.begin(), p.tokens.begin() + L);
+  c.agents.emplace(child, std::move(ch));
+  ++c.generation;
+}
+
+int64_t fork_tokens(Ctx& c, int64_t child, int32_t adapter, const int32_t* tokens, int64_t n) {
+  if (c.agents.count(child) || child < 0 || adapter < 0 || n < 0 || (n > 0 && !tokens))
+    throw Error(FKV_E_INVALID, "fork_tokens: bad child/adapter/tokens");
+  const int P = c.cfg.page_size;
+  std::vector<int32_t> pages;
+  const TreeNode* node = &c.base_root;
+  for (int64_t s = 0; s < n / P; ++s) {
+    std::vector<int32_t> chunk(tokens + s * P, tokens + (s + 1) * P);
+    auto it = node->children.find(chunk);
+    if (it == node->children.end()) break;
+    pages.push_back(it->second->page);
+    node = it->second.get();
+  }
+  const int64_t k = (int64_t)pages.size();
+  if (c.pools[FKV_KIND_RES].n_free() < k) throw Error(FKV_E_NEEDS_EVICTION, "fork_tokens: residual pool exhausted");
+  Agent ch;
+  ch.id = child; ch.adapter = adapter; ch.owner = child; ch.seqlen = k * P;
+  ch.base = pages;
+  for (int32_t pg : pages) c.pools[FKV_KIND_BASE].retain(pg);
+  for (int64_t i = 0; i < k; ++i) ch.res.push_back(c.pools[FKV_KIND_RES].alloc());
+  ch.tokens.assign(tokens, tokens + k * P);
+  c.agents.emplace(child, std::move(ch));
+  ++c.generation;
+  return k * P;
+}
+
+void append(Ctx& c, int32_t n, const int64_t* agents, const int32_t* n_new, const int32_t* tokens, void* stream) {
+  if (n < 0 || (n > 0 && (!agents || !n_new))) throw Error(FKV_E_INVALID, "append: bad arrays");
+  {
+    std::vector<int64_t> ids(agents, agents + n);
+    std::sort(ids.begin(), ids.end());
+    if (std::adjacent_find(ids.begin(), ids.end()) != ids.end()) throw Error(FKV_E_INVALID, "append: duplicate agent");
+  }
+  int64_t total = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    c.agent(agents[i]);
+    if (n_new[i] < 0) throw Error(FKV_E_INVALID, "append: negative count");
+    total += n_new[i];
+  }
+  if (total > 0 && !tokens) throw Error(FKV_E_INVALID, "append: token ids required");
+  const int P = c.cfg.page_size;
+  // Dry run: pages needed, simulating refcount drops of earlier CoWs (atomicity).
+  int64_t need[2] = {0, 0};
+  std::map<std::pair<int, int32_t>, int32_t> delta;
+  for (int32_t i = 0; i < n; ++i) {
+    const Agent& ag = c.agents.at(agents[i]);
+    const int64_t t0 = ag.seqlen, cnt = n_new[i];
+    if (cnt == 0) continue;
+    if (t0 % P != 0) {
+      const int64_t slot = t0 / P;
+      for (int kind = 0; kind < 2; ++kind) {
+        const int32_t pg = (kind == 0 ? ag.base : ag.res)[slot];
+        const int32_t rc = c.pools[kind].rc[pg] + delta[{kind, pg}];
+        if (rc > 1) { need[kind] += 1; delta[{kind, pg}] -= 1; }
+      }
+    }
+    const int64_t first_new = (t0 + P - 1) / P, last = t0 + cnt - 1;
+    const int64_t pages = last >= first_new * P ? last / P - first_new + 1 : 0;
+    need[0] += pages; need[1] += pages;
+  }
+  if (need[0] > c.pools[0].n_free() || need[1] > c.pools[1].n_free())
+    throw Error(FKV_E_NEEDS_EVICTION, "append: pool exhausted");
+  std::vector<k::CopyOp> copies;
+  int64_t tok = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    Agent& ag = c.agents.at(agents[i]);
+    for (int32_t j = 0; j < n_new[i]; ++j) {
+      const int64_t t = ag.seqlen + j, slot = t / P;
+      const int off = (int)(t % P);
+      if (off == 0) {
+        ag.base.push_back(c.pools[0].alloc());
+        ag.res.push_back(c.pools[1].alloc());
+      } else if (j == 0) {
+        for (int kind = 0; kind < 2; ++kind) {
+          auto& table = kind == 0 ? ag.base : ag.res;
+          const int32_t pg = table[slot];
+          if (c.pools[kind].rc[pg] > 1) {  // copy-on-write (C-10)
+            const int32_t nw = c.pools[kind].alloc();
+            copies.push_back({kind, pg, nw, off});
+            c.copy_log.insert(c.copy_log.end(), {kind, pg, nw, off});
+            const uint64_t keep = off >= 64 ? ~0ull : ((1ull << off) - 1);
+            for (int32_t l = 0; l < c.cfg.n_layers; ++l)
+              c.pools[kind].wmask(nw, l) = c.pools[kind].wmask(pg, l) & keep;
+            c.pools[kind].release(pg);
+            table[slot] = nw;
+          }
+        }
+      }
+      for (int kind = 0; kind < 2; ++kind) {
+        const int32_t pg = (kind == 0 ? ag.base : ag.res)[slot];
+        for (int32_t l = 0; l < c.cfg.n_layers; ++l) c.pools[kind].wmask(pg, l) &= ~(1ull << off);
+      }
+      ag.tokens.push_back(tokens[tok + j]);
+      if (off == P - 1) tree_insert(c, ag, slot);
+    }
+    ag.seqlen += n_new[i];
+    tok += n_new[i];
+  }
+  ++c.generation;
+  if (c.device && !copies.empty()) {
+    const auto pv = pool_view(c);
+    for (size_t o = 0; o < copies.size(); o += k::kMaxCopies) {
+      const int32_t m = (int32_t)std::min<size_t>(k::kMaxCopies, copies.size() - o);
+      check_cuda(k::launch_cow_copy(pv, copies.data() + o, m, (cudaStream_t)stream), "cow_copy");
+    }
+  }
+}
+
+void write_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int64_t* start, const int32_t* count,
+              const void* kb, const void* vb, const void* rk, const void* rv, uint32_t mask, void* stream) {
+  if (layer < 0 || layer >= c.cfg.n_layers || (mask & ~15u) || n < 0 || (n > 0 && (!agents || !start || !count)))
+    throw Error(FKV_E_INVALID, "write_kv: bad layer/mask/arrays");
+  for (int32_t i = 0; i < n; ++i) {
+    const Agent& ag = c.agent(agents[i]);
+    if (start[i] < 0 || count[i] < 0 || start[i] + count[i] > ag.seqlen)
+      throw Error(FKV_E_INVALID, "write_kv: rows not reserved");
+  }
+  const int P = c.cfg.page_size;
+  for (int32_t i = 0; i < n; ++i) {
+    const Agent& ag = c.agents.at(agents[i]);
+    if (count[i] == 0) continue;
+    for (int64_t s = start[i] / P; s <= (start[i] + count[i] - 1) / P; ++s) {
+      if ((mask & 3u) && !c.pools[0].writable(ag.base[s])) throw Error(FKV_E_READONLY, "write_kv: shared base page");
+      if ((mask & 12u) && !c.pools[1].writable(ag.res[s])) throw Error(FKV_E_READONLY, "write_kv: shared residual page");
+    }
+  }
+  if (c.device) {
+    if (((mask & FKV_WRITE_KBASE) && !kb) || ((mask & FKV_WRITE_VBASE) && !vb) || ((mask & FKV_WRITE_RK) && !rk) ||
+        ((mask & FKV_WRITE_RV) && !rv))
+      throw Error(FKV_E_INVALID, "write_kv: missing source");
+  }
+  std::vector<k::WriteRun> runs;
+  int64_t src = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const Agent& ag = c.agents.at(agents[i]);
+    int64_t t = start[i];
+    const int64_t end = start[i] + count[i];
+    while (t < end) {
+      const int64_t s = t / P;
+      const int32_t row0 = (int32_t)(t % P);
+      const int32_t m = (int32_t)std::min<int64_t>(P - row0, end - t);
+      runs.push_back({ag.base[s], ag.res[s], row0, m, (int32_t)src, {0, 0, 0}});
+      const uint64_t bits = (m >= 64 ? ~0ull : ((1ull << m) - 1)) << row0;
+      if ((mask & 3u) == 3u) c.pools[0].wmask(ag.base[s], layer) |= bits;
+      if ((mask & 12u) == 12u) c.pools[1].wmask(ag.res[s], layer) |= bits;
+      t += m; src += m;
+    }
+  }
+  if (c.device && !runs.empty()) {
+    const auto pv = pool_view(c);
+    for (size_t o = 0; o < runs.size(); o += k::kMaxRuns) {
+      const int32_t m = (int32_t)std::min<size_t>(k::kMaxRuns, runs.size() - o);
+      check_cuda(k::launch_kv_write(pv, layer, runs.data() + o, m, kb, vb, rk, rv, mask, (cudaStream_t)stream),
+                 "kv_write");
+    }
+  }
+}
+
+void release(Ctx& c, int64_t a) {
+  Agent& ag = c.agent(a);
+  for (int32_t pg : ag.base) c.pools[0].release(pg);
+  for (int32_t pg : ag.res) c.pools[1].release(pg);
+  c.agents.erase(a);
+  ++c.generation;
+}
+
+namespace {
+void join(std::ostringstream& o, const std::vector<int32_t>& v) {
+  for (size_t i = 0; i < v.size(); ++i) o << (i ? "," : "") << v[i];
+}
+void walk(std::ostringstream& o, const TreeNode& nd, int depth, const PagePool& pool) {
+  for (const auto& kv : nd.children) {
+    o << " " << depth << " page=" << kv.second->page << " rc=" << pool.rc[kv.second->page] << " tok=";
+    join(o, kv.first);
+    o << "\n";
+    walk(o, *kv.second, depth + 1, pool);
+  }
+}
+}  // namespace
+
+std::string dump(const Ctx& c) {
+  std::ostringstream o;
+  o << "P=" << c.cfg.page_size << "\n";
+  std::vector<int64_t> ids;
+  for (const auto& kv : c.agents) ids.push_back(kv.first);
+  std::sort(ids.begin(), ids.end());
+  for (int64_t a : ids) {
+    const Agent& ag = c.agents.at(a);
+    o << "agent " << ag.id << " adapter=" << ag.adapter << " owner=" << ag.owner << " seqlen=" << ag.seqlen
+      << " base=";
+    join(o, ag.base);
+    o << " res=";
+    join(o, ag.res);
+    o << "\n";
+  }
+  const char* names[2] = {"base", "res"};
+  for (int kind = 0; kind < 2; ++kind) {
+    const PagePool& p = c.pools[kind];
+    o << names[kind] << "_free " << p.free_set.size() << " order=";
+    bool first = true;
+    for (const auto& e : p.free_set) { o << (first ? "" : ",") << e.second; first = false; }
+    o << "\n" << names[kind] << "_rc ";
+    first = true;
+    for (int64_t i = 0; i < p.n; ++i)
+      if (p.rc[i] > 0) { o << (first ? "" : " ") << i << ":" << p.rc[i]; first = false; }
+    o << "\n";
+  }
+  o << "base_tree\n";
+  walk(o, c.base_root, 0, c.pools[0]);
+  for (const auto& kv : c.res_roots) {
+    o << "res_tree owner=" << kv.first << "\n";
+    walk(o, *kv.second, 0, c.pools[1]);
+  }
+  return o.str();
+}
+
+}  // namespace fkv

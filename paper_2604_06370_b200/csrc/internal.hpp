@@ -1,0 +1,179 @@
+// Internal structures of the forkkv library (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/forkkv.h"
+
+namespace fkv {
+
+struct Error : std::runtime_error {
+  fkv_status code;
+  Error(fkv_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// R1: one page pool. Free set ordered by (rank, id).
+struct PagePool {
+  int64_t n = 0;
+  uint64_t seed = 0;
+  int32_t layers = 0;
+  std::vector<int32_t> rc;
+  std::vector<uint8_t> in_tree;
+  std::set<std::pair<uint64_t, int32_t>> free_set;
+  std::vector<uint64_t> written;  // [page][layer] row bitmask (rows < 64)
+
+  void init(int64_t n_pages, uint64_t s, int32_t n_layers) {
+    n = n_pages; seed = s; layers = n_layers;
+    rc.assign(n, 0); in_tree.assign(n, 0);
+    written.assign((size_t)n * n_layers, 0);
+    free_set.clear();
+    for (int64_t i = 0; i < n; ++i) free_set.insert({rank(i), (int32_t)i});
+  }
+  uint64_t rank(int64_t id) const { return seed == 0 ? (uint64_t)id : splitmix64(seed ^ (uint64_t)id); }
+  int64_t n_free() const { return (int64_t)free_set.size(); }
+  int32_t alloc() {
+    auto it = free_set.begin();
+    int32_t id = it->second;
+    free_set.erase(it);
+    rc[id] = 1; in_tree[id] = 0;
+    for (int32_t l = 0; l < layers; ++l) written[(size_t)id * layers + l] = 0;
+    return id;
+  }
+  void retain(int32_t id) { rc[id] += 1; }
+  void release(int32_t id) {
+    rc[id] -= 1;
+    if (rc[id] == 0) { in_tree[id] = 0; free_set.insert({rank(id), id}); }
+  }
+  bool writable(int32_t id) const { return rc[id] - (in_tree[id] ? 1 : 0) == 1; }
+  uint64_t& wmask(int32_t id, int32_t layer) { return written[(size_t)id * layers + layer]; }
+};
+
+struct Agent {
+  int64_t id = 0;
+  int32_t adapter = 0;
+  int64_t owner = 0;   // residual tree key
+  int64_t seqlen = 0;
+  std::vector<int32_t> base, res;
+  std::vector<int32_t> tokens;
+};
+
+struct TreeNode {
+  int32_t page = -1;
+  std::map<std::vector<int32_t>, std::unique_ptr<TreeNode>> children;
+};
+
+struct AdapterSlot {
+  int32_t id;
+  const void* bk;
+  const void* bv;
+};
+
+struct Ctx {
+  fkv_config cfg{};
+  fkv_buffers buf{};
+  int32_t hkv_local = 0, hq_local = 0, group = 0;
+  bool device = false;
+  PagePool pools[2];
+  std::unordered_map<int64_t, Agent> agents;
+  TreeNode base_root;
+  std::map<int64_t, std::unique_ptr<TreeNode>> res_roots;
+  std::vector<int32_t> copy_log;  // quads (kind, src, dst, rows)
+  std::vector<AdapterSlot> adapters;
+  std::unordered_map<int32_t, int32_t> adapter_slot;
+  uint64_t generation = 1;
+  std::string last_error;
+  size_t elem = 2;
+
+  Agent& agent(int64_t a) {
+    auto it = agents.find(a);
+    if (it == agents.end()) throw Error(FKV_E_UNKNOWN_AGENT, "unknown agent " + std::to_string(a));
+    return it->second;
+  }
+};
+
+// ---- plan -------------------------------------------------------------------
+// Device-side plan records (uploaded as one blob).
+struct DevSeq {         // per sequence
+  int32_t q_row0;       // first query row in Q/O
+  int32_t q_len;
+  int32_t seqlen;
+  int32_t adapter_slot;
+};
+struct DevWarp {        // one warp = up to 16 rows of one residual owner
+  int32_t row_off;      // index into rows[] (16 entries, padded with -1)
+  int32_t n_rows;
+  int32_t res_off;      // offset in res_pages[] of the owner's table (slot 0)
+  int32_t adapter_slot;
+  int32_t entry_off;    // first partial entry
+  int32_t pad_[3];
+};
+struct DevItem {        // one CTA
+  int32_t kv_head;      // local kv head
+  int32_t key_begin;    // token range [key_begin, key_end)
+  int32_t key_end;
+  int32_t base_off;     // offset in base_pages[] of the leader seq's table (slot 0)
+  int32_t warp_off;
+  int32_t n_warps;
+  int32_t pad_[2];
+};
+struct DevRow {         // query row: (seq, query index, local q head)
+  int32_t seq;
+  int32_t qi;
+  int32_t qh;
+  int32_t pos;          // absolute position of the query (causal limit)
+};
+
+struct Plan {
+  uint64_t generation = 0;
+  int32_t n_seqs = 0;
+  int64_t n_rows_q = 0;  // total query rows (sum q_len)
+  int32_t kernel = 0;    // 0 mma grouped, 1 simt
+  std::vector<DevSeq> seqs;
+  std::vector<int32_t> base_pages, res_pages;
+  std::vector<DevItem> items;
+  std::vector<DevWarp> warps;
+  std::vector<DevRow> rows;        // warp rows (16 per warp)
+  std::vector<int32_t> out_ptr;    // CSR over output rows (n_rows_q * hq_local + 1)
+  std::vector<int32_t> out_entries;
+  std::vector<int64_t> adapter_ptrs;  // [slot][2] device pointers
+  std::vector<int32_t> qrow_seq;      // query row -> plan seq index
+  int64_t n_segments = 0, n_entries = 0, key_tiles = 0, alg_bytes = 0;
+  // device layout (offsets into the uploaded blob)
+  std::vector<uint8_t> blob;
+  size_t off_seqs = 0, off_base = 0, off_res = 0, off_items = 0, off_warps = 0, off_rows = 0, off_outptr = 0,
+         off_outent = 0, off_adapters = 0, off_qrow = 0;
+  void* dev = nullptr;
+  size_t ws_bytes = 0;
+};
+
+// control.cpp
+void ctx_create(Ctx& c, const fkv_config& cfg, const fkv_buffers* buf);
+void create_root(Ctx& c, int64_t a, int32_t adapter);
+void fork(Ctx& c, int64_t parent, int64_t L, int64_t child, int32_t adapter, uint32_t flags, void* stream);
+int64_t fork_tokens(Ctx& c, int64_t child, int32_t adapter, const int32_t* tokens, int64_t n);
+void append(Ctx& c, int32_t n, const int64_t* agents, const int32_t* n_new, const int32_t* tokens, void* stream);
+void write_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int64_t* start, const int32_t* count,
+              const void* kb, const void* vb, const void* rk, const void* rv, uint32_t mask, void* stream);
+void release(Ctx& c, int64_t a);
+std::string dump(const Ctx& c);
+
+// plan.cpp
+Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags);
+void upload_plan(Ctx& c, Plan& p, void* dev, size_t bytes, void* stream);
+void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O, float scale, void* ws,
+                   size_t ws_bytes, void* stream);
+
+}  // namespace fkv

@@ -1,0 +1,321 @@
+// Agent-grouping planner (§8(a) row a4) and the attention launch (a5, a6).
+//
+// Agents forked from the same prefix hold the same physical base pages
+// (§5.2 "mapping the globally shared bCache"); the planner finds these
+// shared page runs (an LCP over the batch's base block tables), so that one
+// CTA streams each shared base tile once and applies it to the query rows of
+// every agent holding it.  Inside a segment, rows are grouped by residual
+// owner (same adapter and same residual pages), 16 rows per warp: the warp
+// rebuilds its owner's K_lora = RoPE(K_res B_k) tile once (Alg1.335) and uses
+// it for all its rows.  Long segments are split along the keys (split-KV) to
+// fill the 148 SMs; partial (m, l, acc, acc_r) are merged by the combine
+// kernel, which also applies the late V fusion acc + acc_r B_v (Eq.4).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+#include "internal.hpp"
+#include "kernels.hpp"
+
+namespace fkv {
+
+namespace {
+constexpr int kRowsPerWarp = 16;
+constexpr int kWarpsPerCta = 8;
+constexpr int kTileKeys = 64;
+
+struct Seg {
+  int64_t slot0, slot1;
+  std::vector<int32_t> members;  // plan seq indices
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+template <class T>
+size_t put(std::vector<uint8_t>& blob, const std::vector<T>& v) {
+  size_t off = align256(blob.size());
+  blob.resize(off + std::max<size_t>(v.size() * sizeof(T), 16));
+  if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+  return off;
+}
+}  // namespace
+
+Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
+  if (n < 1 || !seqs) throw Error(FKV_E_INVALID, "plan: empty batch");
+  const int P = c.cfg.page_size;
+  const int g = c.group;
+  auto plan = std::make_unique<Plan>();
+  Plan& pl = *plan;
+  pl.generation = c.generation;
+  pl.n_seqs = n;
+  std::vector<int64_t> nslots(n), base_off(n), res_off(n);
+  std::vector<const Agent*> ags(n);
+  int64_t qrow = 0;
+  for (int32_t b = 0; b < n; ++b) {
+    const Agent& ag = c.agent(seqs[b].agent);
+    if (seqs[b].q_len < 1) throw Error(FKV_E_INVALID, "plan: q_len must be >= 1");
+    if (seqs[b].q_len > ag.seqlen) throw Error(FKV_E_NO_KEYS, "plan: a query row has no keys");
+    auto it = c.adapter_slot.find(ag.adapter);
+    if (it == c.adapter_slot.end()) throw Error(FKV_E_INVALID, "plan: adapter not registered");
+    ags[b] = &ag;
+    nslots[b] = (ag.seqlen + P - 1) / P;
+    base_off[b] = (int64_t)pl.base_pages.size();
+    res_off[b] = (int64_t)pl.res_pages.size();
+    pl.base_pages.insert(pl.base_pages.end(), ag.base.begin(), ag.base.begin() + nslots[b]);
+    pl.res_pages.insert(pl.res_pages.end(), ag.res.begin(), ag.res.begin() + nslots[b]);
+    pl.seqs.push_back({(int32_t)qrow, seqs[b].q_len, (int32_t)ag.seqlen, it->second});
+    for (int32_t i = 0; i < seqs[b].q_len; ++i) pl.qrow_seq.push_back(b);
+    qrow += seqs[b].q_len;
+    if (flags & FKV_PLAN_CHECK_WRITTEN) {
+      for (int64_t s = 0; s < nslots[b]; ++s) {
+        const int64_t rows = std::min<int64_t>(P, ag.seqlen - s * P);
+        const uint64_t need = rows >= 64 ? ~0ull : ((1ull << rows) - 1);
+        for (int32_t l = 0; l < c.cfg.n_layers; ++l)
+          if ((c.pools[0].wmask(ag.base[s], l) & need) != need || (c.pools[1].wmask(ag.res[s], l) & need) != need)
+            throw Error(FKV_E_UNWRITTEN, "plan: agent " + std::to_string(ag.id) + " slot " + std::to_string(s) +
+                                             " layer " + std::to_string(l) + " not written");
+      }
+    }
+  }
+  if (qrow > INT32_MAX / 64) throw Error(FKV_E_INVALID, "plan: too many query rows");
+  pl.n_rows_q = qrow;
+
+  // ---- segments: maximal slot runs over which the member set shares pages --
+  std::vector<Seg> segs;
+  {
+    std::vector<std::pair<std::vector<int32_t>, int64_t>> stack;
+    std::vector<int32_t> all(n);
+    for (int32_t b = 0; b < n; ++b) all[b] = b;
+    stack.push_back({all, 0});
+    while (!stack.empty()) {
+      auto [mem, slot] = std::move(stack.back());
+      stack.pop_back();
+      int64_t s = slot;
+      for (;;) {
+        bool ok = true;
+        for (int32_t b : mem)
+          if (nslots[b] <= s || ags[b]->base[s] != ags[mem[0]]->base[s]) { ok = false; break; }
+        if (!ok) break;
+        ++s;
+      }
+      if (s > slot) segs.push_back({slot, s, mem});
+      std::map<int32_t, std::vector<int32_t>> groups;  // page id -> members (deterministic order)
+      for (int32_t b : mem)
+        if (nslots[b] > s) groups[ags[b]->base[s]].push_back(b);
+      // push in reverse so segments come out in ascending page-id order
+      for (auto it = groups.rbegin(); it != groups.rend(); ++it) stack.push_back({it->second, s});
+    }
+  }
+  pl.n_segments = (int64_t)segs.size();
+
+  // ---- rows -> owner groups -> warps -> CTAs -> key splits ------------------
+  struct Cta {
+    int32_t kv_head;
+    int64_t k0, k1;
+    int32_t base_off;
+    std::vector<int32_t> warp_ids;
+  };
+  std::vector<Cta> ctas;
+  std::vector<std::vector<int32_t>> warp_rows;  // row indices into pl.rows per warp (before splitting)
+  std::vector<DevWarp> proto_warps;
+  std::vector<DevRow> proto_rows;
+  int64_t res_bytes = 0, base_bytes = 0;
+  const size_t el = c.elem;
+  const int32_t hkv = c.hkv_local, d = c.cfg.head_dim, r = c.cfg.rank;
+  for (const Seg& sg : segs) {
+    int64_t maxlen = 0;
+    for (int32_t b : sg.members) maxlen = std::max<int64_t>(maxlen, ags[b]->seqlen);
+    const int64_t k0 = sg.slot0 * P, k1 = std::min<int64_t>(sg.slot1 * P, maxlen);
+    if (k1 <= k0) continue;
+    base_bytes += (k1 - k0) * hkv * d * 2 * (int64_t)el;
+    // owner key: adapter slot + residual pages over the segment
+    std::map<std::pair<int32_t, std::vector<int32_t>>, std::vector<int32_t>> owners;
+    for (int32_t b : sg.members) {
+      std::vector<int32_t> rp(ags[b]->res.begin() + sg.slot0, ags[b]->res.begin() + sg.slot1);
+      owners[{pl.seqs[b].adapter_slot, std::move(rp)}].push_back(b);
+    }
+    for (const auto& ow : owners) {
+      int64_t okeys = 0;
+      for (int32_t b : ow.second) okeys = std::max<int64_t>(okeys, std::min<int64_t>(k1, ags[b]->seqlen) - k0);
+      res_bytes += okeys * r * 2 * (int64_t)el;
+    }
+    for (int32_t h = 0; h < hkv; ++h) {
+      std::vector<int32_t> cta_warps;
+      for (const auto& ow : owners) {
+        std::vector<DevRow> rows;
+        for (int32_t b : ow.second) {
+          const int32_t L = pl.seqs[b].seqlen, C = pl.seqs[b].q_len;
+          for (int32_t i = 0; i < C; ++i) {
+            const int32_t pos = L - C + i;
+            if (pos < k0) continue;  // no key of this segment is visible to the row
+            for (int32_t kk = h * g; kk < (h + 1) * g; ++kk) rows.push_back({b, i, kk, pos});
+          }
+        }
+        for (size_t o = 0; o < rows.size(); o += kRowsPerWarp) {
+          DevWarp w{};
+          w.row_off = (int32_t)proto_rows.size();
+          w.n_rows = (int32_t)std::min<size_t>(kRowsPerWarp, rows.size() - o);
+          w.res_off = (int32_t)res_off[ow.second[0]];
+          w.adapter_slot = ow.first.first;
+          for (int j = 0; j < kRowsPerWarp; ++j)
+            proto_rows.push_back(j < w.n_rows ? rows[o + j] : DevRow{-1, 0, 0, -1});
+          cta_warps.push_back((int32_t)proto_warps.size());
+          proto_warps.push_back(w);
+          if ((int)cta_warps.size() == kWarpsPerCta) {
+            ctas.push_back({h, k0, k1, (int32_t)base_off[sg.members[0]], cta_warps});
+            cta_warps.clear();
+          }
+        }
+      }
+      if (!cta_warps.empty()) ctas.push_back({h, k0, k1, (int32_t)base_off[sg.members[0]], cta_warps});
+    }
+  }
+  // key split: aim for ~2 waves over the SMs
+  int sms = 148;
+  if (c.device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, c.cfg.device) == cudaSuccess && v > 0) sms = v;
+  }
+  int64_t total_tiles = 0;
+  for (const Cta& ct : ctas) total_tiles += (ct.k1 - ct.k0 + kTileKeys - 1) / kTileKeys;
+  const int64_t target = 2LL * sms;
+  const int64_t split_tiles = std::max<int64_t>(2, (total_tiles + target - 1) / std::max<int64_t>(1, target));
+  int64_t entries = 0;
+  for (const Cta& ct : ctas) {
+    const int64_t tiles = (ct.k1 - ct.k0 + kTileKeys - 1) / kTileKeys;
+    for (int64_t t = 0; t < tiles; t += split_tiles) {
+      const int64_t kb = ct.k0 + t * kTileKeys;
+      const int64_t ke = std::min<int64_t>(ct.k1, ct.k0 + (t + split_tiles) * kTileKeys);
+      // rows that see no key of this split get no entry
+      DevItem it{};
+      it.kv_head = ct.kv_head;
+      it.key_begin = (int32_t)kb;
+      it.key_end = (int32_t)ke;
+      it.base_off = ct.base_off;
+      it.warp_off = (int32_t)pl.warps.size();
+      for (int32_t wi : ct.warp_ids) {
+        DevWarp w = proto_warps[wi];
+        w.row_off = (int32_t)pl.rows.size();
+        int32_t nr = 0;
+        DevRow keep[kRowsPerWarp];
+        for (int j = 0; j < proto_warps[wi].n_rows; ++j) {
+          const DevRow& rw = proto_rows[proto_warps[wi].row_off + j];
+          if (rw.pos >= kb) keep[nr++] = rw;
+        }
+        if (nr == 0) continue;
+        w.n_rows = nr;
+        w.entry_off = (int32_t)entries;
+        entries += kRowsPerWarp;  // entries are per warp slot (padded) for simple indexing
+        for (int j = 0; j < kRowsPerWarp; ++j) pl.rows.push_back(j < nr ? keep[j] : DevRow{-1, 0, 0, -1});
+        pl.warps.push_back(w);
+      }
+      it.n_warps = (int32_t)pl.warps.size() - it.warp_off;
+      if (it.n_warps > 0) {
+        pl.items.push_back(it);
+        pl.key_tiles += (ke - kb + kTileKeys - 1) / kTileKeys;
+      }
+    }
+  }
+  if (entries > INT32_MAX) throw Error(FKV_E_INVALID, "plan: too many partial entries");
+  pl.n_entries = entries;
+  // CSR: output row -> entries
+  const int64_t n_out = pl.n_rows_q * c.hq_local;
+  std::vector<int32_t> cnt(n_out + 1, 0);
+  for (const DevWarp& w : pl.warps)
+    for (int j = 0; j < w.n_rows; ++j) {
+      const DevRow& rw = pl.rows[w.row_off + j];
+      cnt[(int64_t)(pl.seqs[rw.seq].q_row0 + rw.qi) * c.hq_local + rw.qh + 1]++;
+    }
+  for (int64_t i = 0; i < n_out; ++i) cnt[i + 1] += cnt[i];
+  pl.out_ptr = cnt;
+  pl.out_entries.assign(cnt[n_out], 0);
+  std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
+  for (const DevWarp& w : pl.warps)
+    for (int j = 0; j < w.n_rows; ++j) {
+      const DevRow& rw = pl.rows[w.row_off + j];
+      const int64_t o = (int64_t)(pl.seqs[rw.seq].q_row0 + rw.qi) * c.hq_local + rw.qh;
+      pl.out_entries[fill[o]++] = w.entry_off + j;
+    }
+  for (int64_t o = 0; o < n_out; ++o)
+    if (pl.out_ptr[o + 1] == pl.out_ptr[o]) throw Error(FKV_E_NO_KEYS, "plan: an output row has no keys");
+  // adapters
+  pl.adapter_ptrs.resize(c.adapters.size() * 2);
+  for (size_t s = 0; s < c.adapters.size(); ++s) {
+    pl.adapter_ptrs[2 * s] = (int64_t)(intptr_t)c.adapters[s].bk;
+    pl.adapter_ptrs[2 * s + 1] = (int64_t)(intptr_t)c.adapters[s].bv;
+  }
+  // algorithmic bytes per layer: shared base once per segment,
+  // residual once per (segment, owner), adapters once, Q in + O out.
+  std::set<int32_t> used_adapters;
+  for (const DevSeq& s : pl.seqs) used_adapters.insert(s.adapter_slot);
+  pl.alg_bytes = base_bytes + res_bytes + (int64_t)used_adapters.size() * 2 * r * d * hkv * (int64_t)el +
+                 pl.n_rows_q * c.hq_local * d * 2 * (int64_t)el;
+  // kernel choice
+  const bool mma_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d == 128 && r == 16 && !(flags & FKV_PLAN_FORCE_SIMT);
+  pl.kernel = mma_ok ? 0 : 1;
+  // blob
+  pl.blob.clear();
+  pl.off_seqs = put(pl.blob, pl.seqs);
+  pl.off_base = put(pl.blob, pl.base_pages);
+  pl.off_res = put(pl.blob, pl.res_pages);
+  pl.off_items = put(pl.blob, pl.items);
+  pl.off_warps = put(pl.blob, pl.warps);
+  pl.off_rows = put(pl.blob, pl.rows);
+  pl.off_outptr = put(pl.blob, pl.out_ptr);
+  pl.off_outent = put(pl.blob, pl.out_entries);
+  pl.off_adapters = put(pl.blob, pl.adapter_ptrs);
+  pl.off_qrow = put(pl.blob, pl.qrow_seq);
+  pl.blob.resize(align256(pl.blob.size()));
+  pl.ws_bytes = align256((size_t)pl.n_entries * (size_t)(2 + d + r) * sizeof(float));
+  return plan.release();
+}
+
+void upload_plan(Ctx& c, Plan& p, void* dev, size_t bytes, void* stream) {
+  if (!c.device) throw Error(FKV_E_INVALID, "plan_upload: host-only ctx");
+  if (!dev || bytes < p.blob.size() || ((uintptr_t)dev & 255)) throw Error(FKV_E_INVALID, "plan_upload: bad buffer");
+  cudaError_t e = cudaMemcpyAsync(dev, p.blob.data(), p.blob.size(), cudaMemcpyHostToDevice, (cudaStream_t)stream);
+  if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("plan_upload: ") + cudaGetErrorString(e));
+  p.dev = dev;
+}
+
+void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O, float scale, void* ws,
+                   size_t ws_bytes, void* stream) {
+  if (!c.device) throw Error(FKV_E_INVALID, "attention: host-only ctx");
+  if (p.generation != c.generation) throw Error(FKV_E_STALE, "attention: plan is stale");
+  if (!p.dev) throw Error(FKV_E_INVALID, "attention: plan not uploaded");
+  if (layer < 0 || layer >= c.cfg.n_layers || !Q || !O) throw Error(FKV_E_INVALID, "attention: bad layer/Q/O");
+  if (!ws || ws_bytes < p.ws_bytes || ((uintptr_t)ws & 15)) throw Error(FKV_E_INVALID, "attention: workspace too small");
+  const uint8_t* base = (const uint8_t*)p.dev;
+  k::AttnParams a{};
+  a.base_k = c.buf.base_k; a.base_v = c.buf.base_v; a.res_k = c.buf.res_k; a.res_v = c.buf.res_v;
+  a.rope_cos = c.buf.rope_cos; a.rope_sin = c.buf.rope_sin;
+  a.Q = Q; a.O = O; a.ws = (float*)ws;
+  a.seqs = (const DevSeq*)(base + p.off_seqs);
+  a.base_pages = (const int32_t*)(base + p.off_base);
+  a.res_pages = (const int32_t*)(base + p.off_res);
+  a.items = (const DevItem*)(base + p.off_items);
+  a.warps = (const DevWarp*)(base + p.off_warps);
+  a.rows = (const DevRow*)(base + p.off_rows);
+  a.out_ptr = (const int32_t*)(base + p.off_outptr);
+  a.out_entries = (const int32_t*)(base + p.off_outent);
+  a.adapters = (const int64_t*)(base + p.off_adapters);
+  a.qrow_seq = (const int32_t*)(base + p.off_qrow);
+  const int64_t P = c.cfg.page_size, d = c.cfg.head_dim, r = c.cfg.rank;
+  a.base_layer_stride = c.cfg.n_base_pages * c.hkv_local * P * d;
+  a.res_layer_stride = c.cfg.n_res_pages * P * r;
+  a.adapter_layer_stride = (int64_t)c.hkv_local * r * d;
+  a.layer = layer; a.hkv = c.hkv_local; a.hq = c.hq_local; a.group = c.group; a.P = (int32_t)P;
+  a.d = (int32_t)d; a.r = (int32_t)r; a.rope_mode = c.cfg.rope_mode; a.dtype = c.cfg.dtype;
+  a.n_items = (int32_t)p.items.size();
+  a.n_out_rows = (int32_t)(p.n_rows_q * c.hq_local);
+  a.entry_stride = (int32_t)(2 + d + r);
+  if (scale <= 0.f) scale = 1.0f / std::sqrt((float)d);
+  a.scale_log2 = scale * 1.4426950408889634f;
+  cudaError_t e = p.kernel == 0 ? k::launch_attention_mma(a, (cudaStream_t)stream)
+                                : k::launch_attention_simt(a, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = k::launch_combine(a, (cudaStream_t)stream);
+  if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("attention: ") + cudaGetErrorString(e));
+}
+
+}  // namespace fkv
