@@ -199,8 +199,18 @@ fkv_status fkv_plan_upload(fkv_ctx* ctx, fkv_plan* plan, void* dev, size_t bytes
  * sm_scale <= 0 selects 1/sqrt(d) (C-4). Enqueued on `stream`. */
 fkv_status fkv_residual_attention(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
                                   float sm_scale, void* workspace, size_t ws_bytes, void* stream);
-/* Same with HOST Q/O (pinned recommended): H2D of Q into dQ, attention,
- * D2H of dO into O_host, all on `stream`; synchronises the stream. */
+/* The two kernels of fkv_residual_attention separately (for per-kernel
+ * timing): phases = FKV_PHASE_MAIN (split partials, Stages 1-2) and/or
+ * FKV_PHASE_COMBINE (merge + late V fusion, Stage 3). MAIN must precede
+ * COMBINE on the same stream with the same workspace. */
+#define FKV_PHASE_MAIN 1u
+#define FKV_PHASE_COMBINE 2u
+fkv_status fkv_residual_attention_phases(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
+                                         float sm_scale, void* workspace, size_t ws_bytes, void* stream,
+                                         uint32_t phases);
+/* Same as fkv_residual_attention with HOST Q/O (pinned for async copies):
+ * H2D of Q_host into dQ, attention into dO, D2H of dO into O_host, all
+ * enqueued on `stream`; O_host is valid once the stream has synchronised. */
 fkv_status fkv_residual_attention_host(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q_host,
                                        void* O_host, void* dQ, void* dO, float sm_scale, void* workspace,
                                        size_t ws_bytes, void* stream);

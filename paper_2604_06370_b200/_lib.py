@@ -93,7 +93,8 @@ SIGNATURES = {
     "fkv_plan_get_info": ([_vp, ctypes.POINTER(fkv_plan_info)], _i32),
     "fkv_plan_upload": ([_vp, _vp, _vp, _sz, _vp], _i32),
     "fkv_residual_attention": ([_vp, _vp, _i32, _vp, _vp, _f32, _vp, _sz, _vp], _i32),
-    "fkv_residual_attention_host": ([_vp, _vp, _i32, _vp, _vp, _vp, _vp, _f32, _vp, _sz, _vp], _i32),
+    "fkv_residual_attention_phases": ([_vp, _vp, _i32, _vp, _vp, _f32, _vp, _sz, _vp, _u32], _i32),
+    "fkv_residual_attention_host":([_vp, _vp, _i32, _vp, _vp, _vp, _vp, _f32, _vp, _sz, _vp], _i32),
     "fkv_plan_free": ([_vp], _i32),
     "fkv_build_rope_table": ([_i32, _i32, _f64, _i32, _f64, _f64, _f64, _f64, _vp, _vp], _i32),
     "fkv_synth_fill": ([_vp, _i32, _u64, _i32, _u64, _i32, _i64, _i32, _i32, _i32, _i32, _f32, _vp], _i32),

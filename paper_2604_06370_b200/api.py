@@ -275,6 +275,13 @@ class ForkKV:
                                                 _ptr(pl.ws), pl.ws.numel() * 4, _stream_handle(stream)))
         return O
 
+    def residual_attention_phases(self, pl: Plan, layer: int, Q, O, phases: int, sm_scale: float = 0.0,
+                                  stream=None):
+        self._c(self.lib.fkv_residual_attention_phases(self.ctx, pl.handle, layer, _ptr(Q), _ptr(O), sm_scale,
+                                                       _ptr(pl.ws), pl.ws.numel() * 4, _stream_handle(stream),
+                                                       phases))
+        return O
+
     def residual_attention_host(self, pl: Plan, layer: int, Q_host, O_host, dQ, dO, sm_scale: float = 0.0,
                                 stream=None):
         self._c(self.lib.fkv_residual_attention_host(self.ctx, pl.handle, layer, _ptr(Q_host), _ptr(O_host),

@@ -217,6 +217,15 @@ fkv_status fkv_residual_attention(fkv_ctx* ctx, const fkv_plan* plan, int32_t la
   return guard(ctx, [&] { fkv::run_attention(ctx->c, *plan->p, layer, Q, O, sm_scale, workspace, ws_bytes, stream); });
 }
 
+fkv_status fkv_residual_attention_phases(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
+                                         float sm_scale, void* workspace, size_t ws_bytes, void* stream,
+                                         uint32_t phases) {
+  if (!ctx || !plan) return FKV_E_INVALID;
+  return guard(ctx, [&] {
+    fkv::run_attention(ctx->c, *plan->p, layer, Q, O, sm_scale, workspace, ws_bytes, stream, phases);
+  });
+}
+
 fkv_status fkv_residual_attention_host(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q_host,
                                        void* O_host, void* dQ, void* dO, float sm_scale, void* workspace,
                                        size_t ws_bytes, void* stream) {
@@ -228,7 +237,6 @@ fkv_status fkv_residual_attention_host(fkv_ctx* ctx, const fkv_plan* plan, int32
     if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
     fkv::run_attention(ctx->c, *plan->p, layer, dQ, dO, sm_scale, workspace, ws_bytes, stream);
     e = cudaMemcpyAsync(O_host, dO, bytes, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("D2H: ") + cudaGetErrorString(e));
   });
 }

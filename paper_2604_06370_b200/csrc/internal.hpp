@@ -174,6 +174,6 @@ std::string dump(const Ctx& c);
 Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags);
 void upload_plan(Ctx& c, Plan& p, void* dev, size_t bytes, void* stream);
 void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O, float scale, void* ws,
-                   size_t ws_bytes, void* stream);
+                   size_t ws_bytes, void* stream, uint32_t phases = 3u);
 
 }  // namespace fkv

@@ -280,7 +280,8 @@ void upload_plan(Ctx& c, Plan& p, void* dev, size_t bytes, void* stream) {
 }
 
 void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O, float scale, void* ws,
-                   size_t ws_bytes, void* stream) {
+                   size_t ws_bytes, void* stream, uint32_t phases) {
+  if (phases == 0 || (phases & ~3u)) throw Error(FKV_E_INVALID, "attention: bad phases");
   if (!c.device) throw Error(FKV_E_INVALID, "attention: host-only ctx");
   if (p.generation != c.generation) throw Error(FKV_E_STALE, "attention: plan is stale");
   if (!p.dev) throw Error(FKV_E_INVALID, "attention: plan not uploaded");
@@ -312,9 +313,11 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.entry_stride = (int32_t)(2 + d + r);
   if (scale <= 0.f) scale = 1.0f / std::sqrt((float)d);
   a.scale_log2 = scale * 1.4426950408889634f;
-  cudaError_t e = p.kernel == 0 ? k::launch_attention_mma(a, (cudaStream_t)stream)
-                                : k::launch_attention_simt(a, (cudaStream_t)stream);
-  if (e == cudaSuccess) e = k::launch_combine(a, (cudaStream_t)stream);
+  cudaError_t e = cudaSuccess;
+  if (phases & FKV_PHASE_MAIN)
+    e = p.kernel == 0 ? k::launch_attention_mma(a, (cudaStream_t)stream)
+                      : k::launch_attention_simt(a, (cudaStream_t)stream);
+  if (e == cudaSuccess && (phases & FKV_PHASE_COMBINE)) e = k::launch_combine(a, (cudaStream_t)stream);
   if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("attention: ") + cudaGetErrorString(e));
 }
 
