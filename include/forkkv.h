@@ -237,6 +237,16 @@ fkv_status fkv_partition(int32_t G, int32_t n_kv_heads, int64_t base_bytes, int6
 fkv_status fkv_partition_shard(int32_t rank, int32_t H, int32_t D, int32_t n_kv_heads, int64_t n_agents,
                                int32_t* h0, int32_t* h1, int64_t* a0, int64_t* a1);
 
+/* ---- diagnostics ---------------------------------------------------------- */
+/* Self-test of the tcgen05 operand layouts used by the tensor-core kernel:
+ * D[M][N] (fp32) = A[M][K] . B[N][K]^T with A, B bf16 row-major device
+ * arrays staged into shared memory in layout `test` (0: K-major SW128 x2,
+ * 1: MN-major SW128 x2, 2: K-major SW32 A x MN-major SW128 B, 3: MN-major
+ * SW32 A x MN-major SW128 B, 4: A in TMEM x K-major SW128 B) and multiplied
+ * by tcgen05.mma; test 5 checks a TMA SW128 box load (D[0] = mismatches). */
+fkv_status fkv_selftest_umma(int32_t test, const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,
+                             void* stream);
+
 #ifdef __cplusplus
 }
 #endif
