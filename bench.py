@@ -100,7 +100,7 @@ def _scenario(name):
     if name == "c5":
         return recipes.c5(), 32, "configs[4] point: Llama-3.1-8B 32 layers, 64 independent agents over a 32K prefix, r=16"
     return recipes.c2(), 32, ("configs[1] C2: Llama-3.1-8B all 32 layers, 16 agents / 16 adapters x 4 branches = "
-                              "decode batch 64, 32K shared prefix, r=16, page 64")
+                              "decode batch 64, 32K shared prefix, r=16")
 
 
 def _cpu_baseline(scen, n_layers, mode, seed, max_seqs, budget_s=20.0):
@@ -176,7 +176,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     scen, n_layers, desc = _scenario(args.config)
-    P = 64
+    P = args.page
     batch = scen.batch()
     B = len(batch)
     nb, nr = scen.pages_needed(P)
@@ -323,7 +323,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": desc, "rope_mode": args.mode, "decode_batch_per_gpu": B,
+        "config": {"workload": desc, "rope_mode": args.mode, "decode_batch_per_gpu": B, "page_size": P,
                    "keys_per_seq": max(scen.seqlen(a) for a in batch) + args.warmup,
                    "layers": n_layers, "parallelism": f"agent-batch x{world} (partitioner H=1, D={world})",
                    "l2": "inputs larger than L2 (each step streams the whole per-layer cache, >>126 MB)",
@@ -359,6 +359,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seqs", type=int, default=8)
+    ap.add_argument("--page", type=int, default=128, help="tokens per KV page (DESIGN.md C-9)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

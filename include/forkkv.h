@@ -72,6 +72,7 @@ enum { FKV_KIND_BASE = 0, FKV_KIND_RES = 1 };
 
 #define FKV_PLAN_CHECK_WRITTEN 1u   /* verify every key row of every layer was written */
 #define FKV_PLAN_FORCE_SIMT 2u      /* use the plain SIMT kernel (fp32 path is always SIMT) */
+#define FKV_PLAN_FORCE_MMA 4u       /* use the warp-level mma.sync kernel instead of tcgen05 */
 
 typedef struct fkv_config {
   int32_t n_layers;       /* L */
@@ -246,6 +247,10 @@ fkv_status fkv_partition_shard(int32_t rank, int32_t H, int32_t D, int32_t n_kv_
  * by tcgen05.mma; test 5 checks a TMA SW128 box load (D[0] = mismatches). */
 fkv_status fkv_selftest_umma(int32_t test, const void* A, const void* B, float* D, int32_t M, int32_t N, int32_t K,
                              void* stream);
+/* Pipeline timeline of one CTA of the tcgen05 kernel: when `dbg` (device,
+ * int64 [32 events][256 tiles], zeroed by the caller) is non-NULL, CTA
+ * `block` stores clock64() stamps of its pipeline events. NULL disables. */
+fkv_status fkv_debug_timeline(fkv_ctx* ctx, void* dbg, int32_t block);
 
 #ifdef __cplusplus
 }

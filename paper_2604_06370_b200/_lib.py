@@ -34,6 +34,7 @@ WRITE_KBASE, WRITE_VBASE, WRITE_RK, WRITE_RV = 1, 2, 4, 8
 WRITE_ALL = 15
 PLAN_CHECK_WRITTEN = 1
 PLAN_FORCE_SIMT = 2
+PLAN_FORCE_MMA = 4
 
 
 class fkv_config(ctypes.Structure):
@@ -99,6 +100,7 @@ SIGNATURES = {
     "fkv_build_rope_table": ([_i32, _i32, _f64, _i32, _f64, _f64, _f64, _f64, _vp, _vp], _i32),
     "fkv_synth_fill": ([_vp, _i32, _u64, _i32, _u64, _i32, _i64, _i32, _i32, _i32, _i32, _f32, _vp], _i32),
     "fkv_selftest_umma": ([_i32, _vp, _vp, _vp, _i32, _i32, _i32, _vp], _i32),
+    "fkv_debug_timeline": ([_vp, _vp, _i32], _i32),
     "fkv_partition": ([_i32, _i32, _i64, _i64, _pi32, _pi32], _i32),
     "fkv_partition_shard": ([_i32, _i32, _i32, _i32, _i64, _pi32, _pi32, _pi64, _pi64], _i32),
 }

@@ -329,3 +329,10 @@ fkv_status fkv_partition_shard(int32_t rank, int32_t H, int32_t D, int32_t n_kv_
 }
 
 }  // extern "C"
+
+extern "C" fkv_status fkv_debug_timeline(fkv_ctx* ctx, void* dbg, int32_t block) {
+  if (!ctx || block < 0) return FKV_E_INVALID;
+  ctx->c.dbg = dbg;
+  ctx->c.dbg_block = block;
+  return FKV_OK;
+}

@@ -8,6 +8,7 @@
 
 #include "internal.hpp"
 #include "kernels.hpp"
+#include "tma_host.hpp"
 
 namespace fkv {
 
@@ -64,7 +65,7 @@ void ctx_create(Ctx& c, const fkv_config& cfg, const fkv_buffers* buf) {
   const int P = cfg.page_size;
   if (cfg.n_layers < 1 || cfg.n_kv_heads < 1 || cfg.n_q_heads < cfg.n_kv_heads ||
       cfg.n_q_heads % cfg.n_kv_heads != 0 || cfg.head_dim < 2 || (cfg.head_dim & 1) || cfg.head_dim > 256 ||
-      cfg.rank < 1 || cfg.rank > 64 || P < 1 || P > 64 || (64 % P) != 0 || cfg.n_base_pages < 1 ||
+      cfg.rank < 1 || cfg.rank > 64 || P < 1 || P > 128 || (128 % P) != 0 || cfg.n_base_pages < 1 ||
       cfg.n_res_pages < 1 || cfg.n_base_pages > INT32_MAX || cfg.n_res_pages > INT32_MAX || cfg.max_pos < 0 ||
       (cfg.dtype != FKV_DTYPE_BF16 && cfg.dtype != FKV_DTYPE_F32) ||
       (cfg.rope_mode != FKV_ROPE_NONE && cfg.rope_mode != FKV_ROPE_DEFERRED))
@@ -86,6 +87,25 @@ void ctx_create(Ctx& c, const fkv_config& cfg, const fkv_buffers* buf) {
     if (cfg.rope_mode == FKV_ROPE_DEFERRED && (!buf->rope_cos || !buf->rope_sin || cfg.max_pos < 1))
       throw Error(FKV_E_INVALID, "DEFERRED rope needs rope_cos/rope_sin tables");
     check_cuda(cudaSetDevice(cfg.device), "cudaSetDevice");
+    // TMA tensor maps over the pools for the tcgen05 kernel (2D views, one page per box)
+    if (cfg.dtype == FKV_DTYPE_BF16 && cfg.head_dim == 128 && cfg.rank == 16 && (128 % P) == 0 && P >= 8) {
+      const uint64_t brows = (uint64_t)cfg.n_layers * cfg.n_base_pages * c.hkv_local * P;
+      const uint64_t rrows = (uint64_t)cfg.n_layers * cfg.n_res_pages * P;
+      if (brows < (1ull << 31) && rrows < (1ull << 31)) {
+        CUtensorMap m[4];
+        if (P == 128) {  // one page per 128-key tile: both d-halves in one 3D box
+          m[0] = make_tmap_3d_bf16_halves(buf->base_k, brows, 128);
+          m[1] = make_tmap_3d_bf16_halves(buf->base_v, brows, 128);
+        } else {
+          m[0] = make_tmap_2d_bf16(buf->base_k, brows, 128, 256, 64, P, 128);
+          m[1] = make_tmap_2d_bf16(buf->base_v, brows, 128, 256, 64, P, 128);
+        }
+        m[2] = make_tmap_2d_bf16(buf->res_k, rrows, 16, 32, 16, P, 32);
+        m[3] = make_tmap_2d_bf16(buf->res_v, rrows, 16, 32, 16, P, 32);
+        c.tc_maps.assign((const uint8_t*)m, (const uint8_t*)m + sizeof(m));
+        c.has_tc_maps = true;
+      }
+    }
   }
   c.pools[0].init(cfg.n_base_pages, cfg.alloc_order_seed, cfg.n_layers);
   c.pools[1].init(cfg.n_res_pages, cfg.alloc_order_seed, cfg.n_layers);
@@ -203,9 +223,7 @@ void append(Ctx& c, int32_t n, const int64_t* agents, const int32_t* n_new, cons
             const int32_t nw = c.pools[kind].alloc();
             copies.push_back({kind, pg, nw, off});
             c.copy_log.insert(c.copy_log.end(), {kind, pg, nw, off});
-            const uint64_t keep = off >= 64 ? ~0ull : ((1ull << off) - 1);
-            for (int32_t l = 0; l < c.cfg.n_layers; ++l)
-              c.pools[kind].wmask(nw, l) = c.pools[kind].wmask(pg, l) & keep;
+            for (int32_t l = 0; l < c.cfg.n_layers; ++l) c.pools[kind].wcopy_prefix(nw, pg, l, off);
             c.pools[kind].release(pg);
             table[slot] = nw;
           }
@@ -213,7 +231,7 @@ void append(Ctx& c, int32_t n, const int64_t* agents, const int32_t* n_new, cons
       }
       for (int kind = 0; kind < 2; ++kind) {
         const int32_t pg = (kind == 0 ? ag.base : ag.res)[slot];
-        for (int32_t l = 0; l < c.cfg.n_layers; ++l) c.pools[kind].wmask(pg, l) &= ~(1ull << off);
+        for (int32_t l = 0; l < c.cfg.n_layers; ++l) c.pools[kind].wclear_bit(pg, l, off);
       }
       ag.tokens.push_back(tokens[tok + j]);
       if (off == P - 1) tree_insert(c, ag, slot);
@@ -265,9 +283,8 @@ void write_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int
       const int32_t row0 = (int32_t)(t % P);
       const int32_t m = (int32_t)std::min<int64_t>(P - row0, end - t);
       runs.push_back({ag.base[s], ag.res[s], row0, m, (int32_t)src, {0, 0, 0}});
-      const uint64_t bits = (m >= 64 ? ~0ull : ((1ull << m) - 1)) << row0;
-      if ((mask & 3u) == 3u) c.pools[0].wmask(ag.base[s], layer) |= bits;
-      if ((mask & 12u) == 12u) c.pools[1].wmask(ag.res[s], layer) |= bits;
+      if ((mask & 3u) == 3u) c.pools[0].wset_range(ag.base[s], layer, row0, m);
+      if ((mask & 12u) == 12u) c.pools[1].wset_range(ag.res[s], layer, row0, m);
       t += m; src += m;
     }
   }

@@ -1,6 +1,7 @@
 // Internal structures of the forkkv library (not part of the ABI).
 #pragma once
 #include <cstdint>
+#include <algorithm>
 #include <map>
 #include <memory>
 #include <set>
@@ -33,12 +34,12 @@ struct PagePool {
   std::vector<int32_t> rc;
   std::vector<uint8_t> in_tree;
   std::set<std::pair<uint64_t, int32_t>> free_set;
-  std::vector<uint64_t> written;  // [page][layer] row bitmask (rows < 64)
+  std::vector<uint64_t> written;  // [page][layer][2] row bitmask (rows < 128)
 
   void init(int64_t n_pages, uint64_t s, int32_t n_layers) {
     n = n_pages; seed = s; layers = n_layers;
     rc.assign(n, 0); in_tree.assign(n, 0);
-    written.assign((size_t)n * n_layers, 0);
+    written.assign((size_t)n * n_layers * 2, 0);
     free_set.clear();
     for (int64_t i = 0; i < n; ++i) free_set.insert({rank(i), (int32_t)i});
   }
@@ -49,7 +50,7 @@ struct PagePool {
     int32_t id = it->second;
     free_set.erase(it);
     rc[id] = 1; in_tree[id] = 0;
-    for (int32_t l = 0; l < layers; ++l) written[(size_t)id * layers + l] = 0;
+    for (int32_t l = 0; l < 2 * layers; ++l) written[(size_t)id * layers * 2 + l] = 0;
     return id;
   }
   void retain(int32_t id) { rc[id] += 1; }
@@ -58,7 +59,25 @@ struct PagePool {
     if (rc[id] == 0) { in_tree[id] = 0; free_set.insert({rank(id), id}); }
   }
   bool writable(int32_t id) const { return rc[id] - (in_tree[id] ? 1 : 0) == 1; }
-  uint64_t& wmask(int32_t id, int32_t layer) { return written[(size_t)id * layers + layer]; }
+  uint64_t* wmask(int32_t id, int32_t layer) { return &written[((size_t)id * layers + layer) * 2]; }
+  static uint64_t lowbits(int n) { return n <= 0 ? 0ull : (n >= 64 ? ~0ull : ((1ull << n) - 1)); }
+  void wclear_bit(int32_t id, int32_t layer, int off) { wmask(id, layer)[off >> 6] &= ~(1ull << (off & 63)); }
+  void wset_range(int32_t id, int32_t layer, int row0, int n) {
+    uint64_t* w = wmask(id, layer);
+    for (int k = 0; k < 2; ++k) {
+      const int lo = std::max(row0, 64 * k), hi = std::min(row0 + n, 64 * k + 64);
+      if (hi > lo) w[k] |= lowbits(hi - lo) << (lo - 64 * k);
+    }
+  }
+  void wcopy_prefix(int32_t dst, int32_t src, int32_t layer, int rows) {
+    uint64_t *d = wmask(dst, layer), *s = wmask(src, layer);
+    d[0] = s[0] & lowbits(rows);
+    d[1] = s[1] & lowbits(rows - 64);
+  }
+  bool wtest_prefix(int32_t id, int32_t layer, int rows) {
+    uint64_t* w = wmask(id, layer);
+    return (w[0] & lowbits(rows)) == lowbits(rows) && (w[1] & lowbits(rows - 64)) == lowbits(rows - 64);
+  }
 };
 
 struct Agent {
@@ -94,8 +113,12 @@ struct Ctx {
   std::vector<AdapterSlot> adapters;
   std::unordered_map<int32_t, int32_t> adapter_slot;
   uint64_t generation = 1;
+  bool has_tc_maps = false;
+  std::vector<uint8_t> tc_maps;  // 4 CUtensorMap (base K, base V, R_k, R_v) for the tcgen05 kernel
   std::string last_error;
   size_t elem = 2;
+  void* dbg = nullptr;  // diagnostics buffer (fkv_debug_timeline)
+  int32_t dbg_block = 0;
 
   Agent& agent(int64_t a) {
     auto it = agents.find(a);

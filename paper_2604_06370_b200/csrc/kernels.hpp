@@ -58,13 +58,19 @@ struct AttnParams {
   int64_t base_layer_stride;  // elements per layer of base pool
   int64_t res_layer_stride;   // elements per layer of residual pool
   int64_t adapter_layer_stride;  // elements per layer of B_K / B_V (= Hkv_local * r * d)
+  int64_t nb, nr;                // pages per pool
   int32_t layer, hkv, hq, group, P, d, r, rope_mode, dtype;
   int32_t n_items, n_out_rows, entry_stride;
   float scale_log2;  // sm_scale * log2(e)
+  long long* dbg;    // diagnostics: per-event clock64 stamps of CTA dbg_block (nullptr = off)
+  int32_t dbg_block;
+  int32_t tc_prefetch;  // tiles of L2 prefetch lookahead in the tcgen05 producer (0 = off)
 };
 
 cudaError_t launch_attention_mma(const AttnParams& p, cudaStream_t s);
 cudaError_t launch_attention_simt(const AttnParams& p, cudaStream_t s);
+cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStream_t s);
+size_t tc_maps_bytes();
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t s);
 
 cudaError_t launch_synth_fill(void* dst, int32_t dtype, uint64_t seed, int32_t kind, uint64_t owner, int32_t layer,

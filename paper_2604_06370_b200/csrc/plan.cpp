@@ -12,6 +12,7 @@
 // kernel, which also applies the late V fusion acc + acc_r B_v (Eq.4).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 
@@ -22,8 +23,6 @@ namespace fkv {
 
 namespace {
 constexpr int kRowsPerWarp = 16;
-constexpr int kWarpsPerCta = 8;
-constexpr int kTileKeys = 64;
 
 struct Seg {
   int64_t slot0, slot1;
@@ -47,6 +46,14 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   const int g = c.group;
   auto plan = std::make_unique<Plan>();
   Plan& pl = *plan;
+  // kernel choice: tcgen05 (2) > mma.sync (0) > SIMT (1)
+  const int32_t d_ = c.cfg.head_dim, r_ = c.cfg.rank;
+  const bool tc_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && c.has_tc_maps && (128 % P) == 0 &&
+                     P >= 8 && !(flags & (FKV_PLAN_FORCE_SIMT | FKV_PLAN_FORCE_MMA));
+  const bool mma_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && !(flags & FKV_PLAN_FORCE_SIMT);
+  pl.kernel = tc_ok ? 2 : (mma_ok ? 0 : 1);
+  const int kWarpsPerCta = pl.kernel == 2 ? 4 : 8;
+  const int kTileKeys = pl.kernel == 2 ? 128 : 64;
   pl.generation = c.generation;
   pl.n_seqs = n;
   std::vector<int64_t> nslots(n), base_off(n), res_off(n);
@@ -69,10 +76,9 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
     qrow += seqs[b].q_len;
     if (flags & FKV_PLAN_CHECK_WRITTEN) {
       for (int64_t s = 0; s < nslots[b]; ++s) {
-        const int64_t rows = std::min<int64_t>(P, ag.seqlen - s * P);
-        const uint64_t need = rows >= 64 ? ~0ull : ((1ull << rows) - 1);
+        const int rows = (int)std::min<int64_t>(P, ag.seqlen - s * P);
         for (int32_t l = 0; l < c.cfg.n_layers; ++l)
-          if ((c.pools[0].wmask(ag.base[s], l) & need) != need || (c.pools[1].wmask(ag.res[s], l) & need) != need)
+          if (!c.pools[0].wtest_prefix(ag.base[s], l, rows) || !c.pools[1].wtest_prefix(ag.res[s], l, rows))
             throw Error(FKV_E_UNWRITTEN, "plan: agent " + std::to_string(ag.id) + " slot " + std::to_string(s) +
                                              " layer " + std::to_string(l) + " not written");
       }
@@ -179,7 +185,9 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   }
   int64_t total_tiles = 0;
   for (const Cta& ct : ctas) total_tiles += (ct.k1 - ct.k0 + kTileKeys - 1) / kTileKeys;
-  const int64_t target = 2LL * sms;
+  const char* wenv = getenv("FKV_SPLIT_WAVES");
+  const double waves = wenv ? atof(wenv) : 2.0;
+  const int64_t target = std::max<int64_t>(1, (int64_t)(waves * sms));
   const int64_t split_tiles = std::max<int64_t>(2, (total_tiles + target - 1) / std::max<int64_t>(1, target));
   int64_t entries = 0;
   for (const Cta& ct : ctas) {
@@ -251,9 +259,6 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   for (const DevSeq& s : pl.seqs) used_adapters.insert(s.adapter_slot);
   pl.alg_bytes = base_bytes + res_bytes + (int64_t)used_adapters.size() * 2 * r * d * hkv * (int64_t)el +
                  pl.n_rows_q * c.hq_local * d * 2 * (int64_t)el;
-  // kernel choice
-  const bool mma_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d == 128 && r == 16 && !(flags & FKV_PLAN_FORCE_SIMT);
-  pl.kernel = mma_ok ? 0 : 1;
   // blob
   pl.blob.clear();
   pl.off_seqs = put(pl.blob, pl.seqs);
@@ -306,6 +311,8 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.base_layer_stride = c.cfg.n_base_pages * c.hkv_local * P * d;
   a.res_layer_stride = c.cfg.n_res_pages * P * r;
   a.adapter_layer_stride = (int64_t)c.hkv_local * r * d;
+  a.nb = c.cfg.n_base_pages;
+  a.nr = c.cfg.n_res_pages;
   a.layer = layer; a.hkv = c.hkv_local; a.hq = c.hq_local; a.group = c.group; a.P = (int32_t)P;
   a.d = (int32_t)d; a.r = (int32_t)r; a.rope_mode = c.cfg.rope_mode; a.dtype = c.cfg.dtype;
   a.n_items = (int32_t)p.items.size();
@@ -313,10 +320,14 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.entry_stride = (int32_t)(2 + d + r);
   if (scale <= 0.f) scale = 1.0f / std::sqrt((float)d);
   a.scale_log2 = scale * 1.4426950408889634f;
+  a.dbg = (long long*)c.dbg;
+  a.dbg_block = c.dbg_block;
+  { const char* e = getenv("FKV_TC_PREFETCH"); a.tc_prefetch = e ? atoi(e) : 2; }
   cudaError_t e = cudaSuccess;
   if (phases & FKV_PHASE_MAIN)
-    e = p.kernel == 0 ? k::launch_attention_mma(a, (cudaStream_t)stream)
-                      : k::launch_attention_simt(a, (cudaStream_t)stream);
+    e = p.kernel == 2   ? k::launch_attention_tc(a, c.tc_maps.data(), (cudaStream_t)stream)
+        : p.kernel == 0 ? k::launch_attention_mma(a, (cudaStream_t)stream)
+                        : k::launch_attention_simt(a, (cudaStream_t)stream);
   if (e == cudaSuccess && (phases & FKV_PHASE_COMBINE)) e = k::launch_combine(a, (cudaStream_t)stream);
   if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("attention: ") + cudaGetErrorString(e));
 }

@@ -46,6 +46,8 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(SelfTest t, const
     case 3:  // A MN-major SW32 (R_v^T, owner blocks of 16 at LBO), B MN-major SW128 (P^T)
       a_mn = true; aW = 2; a_lbo = K * 32; a_sbo = 256; a_kstep = 512; b_mn = true; b_lbo = K * 128;
       b_kstep = 2048; break;
+    case 6:  // A K-major SW32 (R_k, K=16), B MN-major SW64 (permuted B_k quarter blocks, N = 32 per atom)
+      aW = 2; a_sbo = 256; b_mn = true; bW = 4; b_lbo = K * 64; b_sbo = 512; b_kstep = 1024; break;
     case 4:  // A in TMEM (bf16 packed), B K-major SW128 (S_res = K_lora Q_o^T)
       b_kblk = N * 128; break;
     default: break;
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(SelfTest t, const
       else aoff = (s * 16 / (8 * aW)) * a_kblk + (s * 16 % (8 * aW)) * 2;
       if (b_mn) boff = s * b_kstep;
       else boff = (s * 16 / (8 * bW)) * b_kblk + (s * 16 % (8 * bW)) * 2;
-      const uint64_t bd = make_desc(b0 + boff, b_lbo, b_sbo, bW == 8 ? SWZ_128 : SWZ_32);
+      const uint64_t bd = make_desc(b0 + boff, b_lbo, b_sbo, bW == 8 ? SWZ_128 : (bW == 4 ? SWZ_64 : SWZ_32));
       if (t.test == 4) {
         mma_ts(d_tmem, a_tmem + 8 * s, bd, idesc, s > 0);
       } else {
@@ -160,7 +162,7 @@ extern "C" fkv_status fkv_selftest_umma(int32_t test, const void* A, const void*
     }
     return cudaGetLastError() == cudaSuccess ? FKV_OK : FKV_E_CUDA;
   }
-  if (test < 0 || test > 4 || M != 128 || N < 16 || N > 256 || N % 16 || K < 16 || K > 128 || K % 16)
+  if (test < 0 || test > 6 || test == 5 || M != 128 || N < 16 || N > 256 || N % 16 || K < 16 || K > 128 || K % 16)
     return FKV_E_INVALID;
   const int smem = 128 * 1024;
   static bool attr = false;

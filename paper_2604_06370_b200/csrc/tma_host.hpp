@@ -45,4 +45,20 @@ inline CUtensorMap make_tmap_2d_bf16(const void* base, uint64_t rows, uint64_t c
   return m;
 }
 
+// 3D view of a bf16 [rows][128] array as (64 d-in-half, rows, 2 halves) with
+// strides (256 B, 128 B): one box {64, box_rows, 2} lands in shared memory as
+// [half][box_rows][128 B] (SW128), i.e. both d-halves of a page in one TMA op.
+inline CUtensorMap make_tmap_3d_bf16_halves(const void* base, uint64_t rows, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {64, rows, 2};
+  cuuint64_t strides[2] = {256, 128};
+  cuuint32_t box[3] = {64, box_rows, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (3D) failed: " + std::to_string((int)r));
+  return m;
+}
+
 }  // namespace fkv

@@ -66,16 +66,40 @@ def test_device_synth_matches_host_generator():
 
 
 @pytest.mark.parametrize("mode", ["deferred", "none"])
-@pytest.mark.parametrize("kernel", ["mma", "simt"])
+@pytest.mark.parametrize("kernel", ["tc", "mma", "simt"])
 def test_c1_parity(mode, kernel):
     """configs[0] (C1): 1 layer Llama-3.1-8B shape, r=16, 4 agents forked from a
     2K-token prefix + 128 private + 1 decode token; llama3 RoPE, theta 5e5."""
     scen = recipes.c1()
     fkv = _ctx(scen, 1, 32, 8, 128, 16, 64, "bf16", mode, theta=500000.0, llama3=True)
     driver.build(fkv, scen, seed=0)
-    err, pl = _run_and_check(fkv, scen, 0, 0, "bf16", mode, flags=L.PLAN_CHECK_WRITTEN | (
-        L.PLAN_FORCE_SIMT if kernel == "simt" else 0), theta=500000.0, llama3=True)
-    assert pl.info.kernel == (0 if kernel == "mma" else 1)
+    force = {"tc": 0, "mma": L.PLAN_FORCE_MMA, "simt": L.PLAN_FORCE_SIMT}[kernel]
+    err, pl = _run_and_check(fkv, scen, 0, 0, "bf16", mode, flags=L.PLAN_CHECK_WRITTEN | force, theta=500000.0,
+                             llama3=True)
+    assert pl.info.kernel == {"tc": 2, "mma": 0, "simt": 1}[kernel]
+    assert err <= TOL["bf16"], err
+
+
+@pytest.mark.parametrize("mode", ["deferred", "none"])
+@pytest.mark.parametrize("P", [16, 32, 64, 128])
+def test_tc_kernel_page_sizes_and_groups(mode, P):
+    """tcgen05 kernel: page sizes 16/32/64 (TMA box = one page), owner groups
+    with several slots (same-agent branches: 4 branches x g=4 rows = one slot;
+    a chunked-prefill owner spanning several slots), key ranges ending inside
+    a page, and multi-tile split items."""
+    ag = [recipes.AgentSpec(100, 100, None, 0, False, 700, decode=False)]
+    for i in range(3):
+        ag.append(recipes.AgentSpec(1000 + i, i, 100, 700, False, 0, decode=False))
+        for b in range(4):
+            ag.append(recipes.AgentSpec(10 * i + b, i, 1000 + i, 700, True, 30 + 7 * b))
+    scen = recipes.Scenario("tcgroups", ag, q_len=1)
+    fkv = _ctx(scen, 1, 32, 8, 128, 16, P, "bf16", mode)
+    driver.build(fkv, scen, seed=11)
+    err, pl = _run_and_check(fkv, scen, 11, 0, "bf16", mode)
+    assert pl.info.kernel == 2
+    assert err <= TOL["bf16"], err
+    scen.q_len = 9   # multi-row chunk per sequence: slots of one owner span several warps
+    err, pl = _run_and_check(fkv, scen, 11, 0, "bf16", mode)
     assert err <= TOL["bf16"], err
 
 
@@ -102,7 +126,7 @@ def test_random_suite(seed):
     branches sharing residual pages, chunked-prefill query rows), both RoPE
     modes, bf16 tensor-core path and fp32 SIMT path, page sizes 16/64."""
     rnd = random.Random(seed)
-    P = rnd.choice([16, 64])
+    P = rnd.choice([16, 64, 128])
     mode = rnd.choice(["deferred", "none"])
     dtype = "f32" if seed % 4 == 0 else "bf16"
     d = 64 if (dtype == "f32" and seed % 8 == 0) else 128

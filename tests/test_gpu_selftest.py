@@ -18,7 +18,8 @@ def _need_gpu():
 
 
 @pytest.mark.parametrize("test,N,K", [(0, 64, 128), (0, 128, 64), (0, 256, 128), (1, 64, 128), (1, 128, 64),
-                                      (2, 128, 16), (3, 64, 128), (4, 16, 128), (4, 64, 128)])
+                                      (2, 128, 16), (3, 64, 128), (4, 16, 128), (4, 64, 128), (6, 32, 16),
+                                      (6, 128, 16)])
 def test_umma_layouts(test, N, K):
     g = torch.Generator(device="cpu").manual_seed(test * 1000 + N + K)
     A = torch.randn(128, K, generator=g).to(torch.bfloat16).cuda()
