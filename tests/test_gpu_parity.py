@@ -190,3 +190,15 @@ def test_prefill_chunk_parity():
         driver.build(fkv, scen, seed=5)
         err, pl = _run_and_check(fkv, scen, 5, 0, "bf16", mode)
         assert err <= TOL["bf16"], err
+
+
+@pytest.mark.parametrize("mode", ["deferred", "none"])
+def test_kv_head_shard_parity(mode):
+    """§8(e) head sharding: a ctx holding kv heads [4, 8) only (pools, adapters
+    and Q/O restricted to its heads) matches the oracle for those heads."""
+    scen = recipes.c1(prefix=300, private=40)
+    fkv = _ctx(scen, 1, 32, 8, 128, 16, 128, "bf16", mode, kv_heads=(4, 8))
+    driver.build(fkv, scen, seed=21, h0=4)
+    err, pl = _run_and_check(fkv, scen, 21, 0, "bf16", mode, h0=4)
+    assert pl.info.kernel == 2
+    assert err <= TOL["bf16"], err

@@ -9,7 +9,8 @@ import numpy as np
 from . import synth
 from .recipes import Scenario
 
-_CHUNK = 8192
+_CHUNK = 65536       # rows per staged write (base rows: 65536 x Hkv x d x 2 B = 128 MiB at 8 heads)
+_CHUNK_RES = 1 << 20  # residual-only writes are r-wide: stage up to 1M rows
 
 
 def make_adapter(fkv, seed: int, adapter_id: int, h0: int):
@@ -36,18 +37,22 @@ def write_rows(fkv, seed: int, agent: int, writer: int, pos0: int, n: int, mask:
         return
     tdt = torch.bfloat16 if fkv.dtype_name == "bf16" else torch.float32
     dev = torch.device("cuda", fkv.device)
-    m = min(n, _CHUNK)
+    chunk = _CHUNK if mask & 3 else _CHUNK_RES
+    m = min(n, chunk)
     if stage is None:
         stage = {}
-    if stage.get("n", 0) < m:
-        stage.update(n=m, kb=torch.empty(m, fkv.hkv, fkv.d, dtype=tdt, device=dev),
-                     vb=torch.empty(m, fkv.hkv, fkv.d, dtype=tdt, device=dev),
-                     rk=torch.empty(m, fkv.r, dtype=tdt, device=dev),
+    if (mask & 3) and stage.get("nb", 0) < m:
+        stage.update(nb=m, kb=torch.empty(m, fkv.hkv, fkv.d, dtype=tdt, device=dev),
+                     vb=torch.empty(m, fkv.hkv, fkv.d, dtype=tdt, device=dev))
+    if stage.get("nr", 0) < m:
+        stage.update(nr=m, rk=torch.empty(m, fkv.r, dtype=tdt, device=dev),
                      rv=torch.empty(m, fkv.r, dtype=tdt, device=dev))
     for layer in (range(fkv.L) if layers is None else layers):
-        for o in range(0, n, _CHUNK):
-            c = min(_CHUNK, n - o)
-            kb, vb, rk, rv = stage["kb"][:c], stage["vb"][:c], stage["rk"][:c], stage["rv"][:c]
+        for o in range(0, n, chunk):
+            c = min(chunk, n - o)
+            kb = stage["kb"][:c] if mask & 3 else None
+            vb = stage["vb"][:c] if mask & 3 else None
+            rk, rv = stage["rk"][:c], stage["rv"][:c]
             if mask & 3:
                 synth_fill(kb, seed, synth.KIND_KBASE, writer, layer, pos0 + o, head0=h0)
                 synth_fill(vb, seed, synth.KIND_VBASE, writer, layer, pos0 + o, head0=h0)
