@@ -20,6 +20,7 @@ k::PoolView pool_view(const Ctx& c) {
   pv.nb = c.cfg.n_base_pages; pv.nr = c.cfg.n_res_pages;
   pv.hkv = c.hkv_local; pv.P = c.cfg.page_size; pv.d = c.cfg.head_dim; pv.r = c.cfg.rank;
   pv.L = c.cfg.n_layers; pv.dtype = c.cfg.dtype;
+  pv.res_swz = c.cfg.dtype == FKV_DTYPE_BF16 && c.cfg.rank == 16;
   return pv;
 }
 
@@ -92,16 +93,16 @@ void ctx_create(Ctx& c, const fkv_config& cfg, const fkv_buffers* buf) {
       const uint64_t brows = (uint64_t)cfg.n_layers * cfg.n_base_pages * c.hkv_local * P;
       const uint64_t rrows = (uint64_t)cfg.n_layers * cfg.n_res_pages * P;
       if (brows < (1ull << 31) && rrows < (1ull << 31)) {
+        // see TcMaps in ra_tc.cu: K_base whole tiles (3D, both d-halves) when P = 128, V_base 64-key halves,
+        // residual pages as 128-byte rows (the page format is already the SW32 operand layout, res_col)
+        const uint32_t Pm = P < 64 ? (uint32_t)P : 64u;
         CUtensorMap m[4];
-        if (P == 128) {  // one page per 128-key tile: both d-halves in one 3D box
-          m[0] = make_tmap_3d_bf16_halves(buf->base_k, brows, 128);
-          m[1] = make_tmap_3d_bf16_halves(buf->base_v, brows, 128);
-        } else {
-          m[0] = make_tmap_2d_bf16(buf->base_k, brows, 128, 256, 64, P, 128);
-          m[1] = make_tmap_2d_bf16(buf->base_v, brows, 128, 256, 64, P, 128);
-        }
-        m[2] = make_tmap_2d_bf16(buf->res_k, rrows, 16, 32, 16, P, 32);
-        m[3] = make_tmap_2d_bf16(buf->res_v, rrows, 16, 32, 16, P, 32);
+        m[0] = P == 128 ? make_tmap_3d_bf16_halves(buf->base_k, brows, 128)
+                        : make_tmap_2d_bf16(buf->base_k, brows, 128, 256, 64, P, 128);
+        m[1] = P >= 64 ? make_tmap_3d_bf16_halves(buf->base_v, brows, 64)
+                       : make_tmap_2d_bf16(buf->base_v, brows, 128, 256, 64, P, 128);
+        m[2] = make_tmap_2d_bf16(buf->res_k, rrows / 4, 64, 128, 64, P / 4, 0);
+        m[3] = make_tmap_2d_bf16(buf->res_v, rrows / 4, 64, 128, 64, Pm / 4, 0);
         c.tc_maps.assign((const uint8_t*)m, (const uint8_t*)m + sizeof(m));
         c.has_tc_maps = true;
       }

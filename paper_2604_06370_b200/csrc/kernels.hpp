@@ -16,6 +16,7 @@ struct PoolView {
   void* res_v;
   int64_t nb, nr;  // pages per pool
   int32_t hkv, P, d, r, L, dtype;
+  int32_t res_swz;  // residual rows stored in SW32 order (see res_col)
 };
 
 // A contiguous run of rows written into one (base page, residual page) slot.
@@ -34,6 +35,15 @@ cudaError_t launch_kv_write(const PoolView& pv, int32_t layer, const WriteRun* r
                             const void* kb, const void* vb, const void* rk, const void* rv, uint32_t mask,
                             cudaStream_t s);
 cudaError_t launch_cow_copy(const PoolView& pv, const CopyOp* ops, int32_t n_ops, cudaStream_t s);
+
+// Per-item header of the persistent tcgen05 kernel, staged into shared memory with the item's Q rows (176 B).
+struct ItemRec {
+  int32_t k0, k1, n_tiles, meta;  // meta = n_slots | n_groups << 4 | group-first slot mask << 8 | kv head << 16
+  int32_t n_rows[4];              // query rows of each slot
+  int32_t entry_off[4];           // first partial entry of each slot
+  uint16_t pos1[64];              // per query column: position - k0 + 1 (key t visible iff t - k0 < pos1), 0 = none
+};
+static_assert(sizeof(ItemRec) == 176, "ItemRec");
 
 struct AttnParams {
   const void* base_k;
@@ -64,12 +74,33 @@ struct AttnParams {
   float scale_log2;  // sm_scale * log2(e)
   long long* dbg;    // diagnostics: per-event clock64 stamps of CTA dbg_block (nullptr = off)
   int32_t dbg_block;
-  int32_t tc_prefetch;  // tiles of L2 prefetch lookahead in the tcgen05 producer (0 = off)
+  // persistent tcgen05 kernel: CTA c runs items sched_items[sched_ptr[c] .. sched_ptr[c+1])
+  const int32_t* sched_ptr;
+  const int32_t* sched_items;
+  int32_t n_ctas;
+  // per-CTA tile records, CTA c owns records [tile_ptr[c], tile_ptr[c+1]) in its processing order:
+  // {t0, k1, meta = n_slots | n_groups << 4 | group-first slot mask << 8, res page of slots 0..3, base page}
+  // (pages only meaningful when P == 128: one page per tile)
+  const int32_t* tile_ptr;
+  const int4* tile_recs;
+  const ItemRec* item_recs;  // per plan item
+  int32_t max_pos;
+  int32_t tc_prefetch;  // L2 prefetch distance in tiles (tcgen05 producer; 0 = off)
+  uint8_t* stage;  // per-warp-slot staged operand images (ws region, kStageBytes each)
+  int32_t res_swz;  // residual rows stored in SW32 order (see res_col)
 };
+constexpr int kStageBytes = 8192;
+
+// Residual page format (bf16, r = 16): row i of a page holds R[i][j] at column j ^ (8 * ((i >> 2) & 1)), i.e.
+// the two 16-byte halves of rows 4..7 of every 8-row group are swapped. This is exactly the 32-byte-swizzled
+// K-major operand layout of tcgen05 (SW32), so a residual page streams into shared memory with one plain
+// 128-byte-row TMA box and is an MMA operand as is (tcgen05 kernel, ra_tc.cu).
+__host__ __device__ __forceinline__ int res_col(int row, int j, int swz) { return swz ? (j ^ (((row >> 2) & 1) << 3)) : j; }  // per warp slot: Q image 4 KB + (q~ 512 B | packed B_k 4 KB)
 
 cudaError_t launch_attention_mma(const AttnParams& p, cudaStream_t s);
 cudaError_t launch_attention_simt(const AttnParams& p, cudaStream_t s);
 cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStream_t s);
+cudaError_t launch_stage(const AttnParams& p, int32_t n_warps, cudaStream_t s);
 size_t tc_maps_bytes();
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t s);
 

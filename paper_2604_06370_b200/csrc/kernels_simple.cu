@@ -61,10 +61,22 @@ __global__ void kv_write_kernel(PoolView pv, int32_t layer, Runs<kMaxRuns> runs,
                    threadIdx.x, blockDim.x);
     }
     const int64_t rdst = (((int64_t)layer * pv.nr + w.res_page) * pv.P + (w.row0 + j)) * (int64_t)pv.r;
-    if (mask & FKV_WRITE_RK)
-      copy_elems((uint8_t*)pv.res_k + rdst * es, rk + src * pv.r * es, pv.r, es, threadIdx.x, blockDim.x);
-    if (mask & FKV_WRITE_RV)
-      copy_elems((uint8_t*)pv.res_v + rdst * es, rv + src * pv.r * es, pv.r, es, threadIdx.x, blockDim.x);
+    if (pv.res_swz && ((w.row0 + j) >> 2) & 1) {  // swizzled row: swap the two 8-element halves
+      const int hr = pv.r / 2;
+      for (int hh = 0; hh < 2; ++hh) {
+        if (mask & FKV_WRITE_RK)
+          copy_elems((uint8_t*)pv.res_k + (rdst + hh * hr) * es, rk + (src * pv.r + (1 - hh) * hr) * es, hr, es,
+                     threadIdx.x, blockDim.x);
+        if (mask & FKV_WRITE_RV)
+          copy_elems((uint8_t*)pv.res_v + (rdst + hh * hr) * es, rv + (src * pv.r + (1 - hh) * hr) * es, hr, es,
+                     threadIdx.x, blockDim.x);
+      }
+    } else {
+      if (mask & FKV_WRITE_RK)
+        copy_elems((uint8_t*)pv.res_k + rdst * es, rk + src * pv.r * es, pv.r, es, threadIdx.x, blockDim.x);
+      if (mask & FKV_WRITE_RV)
+        copy_elems((uint8_t*)pv.res_v + rdst * es, rv + src * pv.r * es, pv.r, es, threadIdx.x, blockDim.x);
+    }
   }
 }
 
@@ -243,7 +255,7 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnParams p) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) u[c] = 0.f;
     for (int j = 0; j < r; ++j) {
-      const float rk = ldf<T>(Rk, roff + j);
+      const float rk = ldf<T>(Rk, roff + res_col(row, j, p.res_swz));
 #pragma unroll
       for (int c = 0; c < NC; ++c) u[c] += rk * ldf<T>(Bk, (int64_t)j * D + lane + 32 * c);
     }
@@ -302,8 +314,8 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnParams p) {
     float vf[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) vf[c] = ldf<T>(Vb, boff + lane + 32 * c);
-    const float rv0 = lane < r ? ldf<T>(Rv, roff + lane) : 0.f;
-    const float rv1 = lane + 32 < r ? ldf<T>(Rv, roff + lane + 32) : 0.f;
+    const float rv0 = lane < r ? ldf<T>(Rv, roff + res_col(row, lane, p.res_swz)) : 0.f;
+    const float rv1 = lane + 32 < r ? ldf<T>(Rv, roff + res_col(row, lane + 32, p.res_swz)) : 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const float a = __shfl_sync(0xffffffffu, alpha, i);

@@ -14,7 +14,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <map>
+#include <set>
 
 #include "internal.hpp"
 #include "kernels.hpp"
@@ -177,7 +179,8 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
       if (!cta_warps.empty()) ctas.push_back({h, k0, k1, (int32_t)base_off[sg.members[0]], cta_warps});
     }
   }
-  // key split: aim for ~2 waves over the SMs
+  // key split. mma.sync / SIMT: ~2 waves of CTAs over the SMs. tcgen05 (persistent, one CTA per SM):
+  // pieces of about half the average per-CTA load, so the greedy schedule below balances.
   int sms = 148;
   if (c.device) {
     int v = 0;
@@ -185,16 +188,28 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   }
   int64_t total_tiles = 0;
   for (const Cta& ct : ctas) total_tiles += (ct.k1 - ct.k0 + kTileKeys - 1) / kTileKeys;
-  const char* wenv = getenv("FKV_SPLIT_WAVES");
-  const double waves = wenv ? atof(wenv) : 2.0;
-  const int64_t target = std::max<int64_t>(1, (int64_t)(waves * sms));
-  const int64_t split_tiles = std::max<int64_t>(2, (total_tiles + target - 1) / std::max<int64_t>(1, target));
+  int64_t split_tiles;
+  if (pl.kernel == 2) {
+    const char* penv = getenv("FKV_PIECE_TILES");
+    split_tiles = penv ? std::max<int64_t>(1, atoll(penv)) : std::max<int64_t>(4, total_tiles / (2 * sms));
+    split_tiles = std::min<int64_t>(split_tiles, 511);  // ItemRec::pos1 is 16-bit relative to the item start
+  } else {
+    const char* wenv = getenv("FKV_SPLIT_WAVES");
+    const double waves = wenv ? atof(wenv) : 2.0;
+    const int64_t target = std::max<int64_t>(1, (int64_t)(waves * sms));
+    split_tiles = std::max<int64_t>(2, (total_tiles + target - 1) / std::max<int64_t>(1, target));
+  }
   int64_t entries = 0;
-  for (const Cta& ct : ctas) {
+  std::vector<std::array<int64_t, 3>> order_key;  // (segment start, piece, cta) per item
+  std::vector<int64_t> item_cost;
+  for (size_t ci = 0; ci < ctas.size(); ++ci) {
+    const Cta& ct = ctas[ci];
     const int64_t tiles = (ct.k1 - ct.k0 + kTileKeys - 1) / kTileKeys;
-    for (int64_t t = 0; t < tiles; t += split_tiles) {
+    const int64_t n_pieces = (tiles + split_tiles - 1) / split_tiles;
+    const int64_t piece = (tiles + n_pieces - 1) / n_pieces;
+    for (int64_t t = 0, pi = 0; t < tiles; t += piece, ++pi) {
       const int64_t kb = ct.k0 + t * kTileKeys;
-      const int64_t ke = std::min<int64_t>(ct.k1, ct.k0 + (t + split_tiles) * kTileKeys);
+      const int64_t ke = std::min<int64_t>(ct.k1, ct.k0 + (t + piece) * kTileKeys);
       // rows that see no key of this split get no entry
       DevItem it{};
       it.kv_head = ct.kv_head;
@@ -221,8 +236,83 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
       it.n_warps = (int32_t)pl.warps.size() - it.warp_off;
       if (it.n_warps > 0) {
         pl.items.push_back(it);
-        pl.key_tiles += (ke - kb + kTileKeys - 1) / kTileKeys;
+        const int64_t nt = (ke - kb + kTileKeys - 1) / kTileKeys;
+        pl.key_tiles += nt;
+        order_key.push_back({ct.k0, pi, (int64_t)ci});
+        // cost in KB of shared-memory ingest: base K + V tiles, R_k + R_v per slot, + per-item overhead
+        // per-item overhead (header staging, first-tile softmax setup, epilogue) measured at ~4 tiles
+        item_cost.push_back((nt + 4) * (64 + 8 * it.n_warps));
       }
+    }
+  }
+  if (pl.kernel == 2) {
+    // persistent schedule: items in (segment, piece, row block) order, each to the least-loaded CTA, so the
+    // row blocks and kv heads that stream the same base / residual pages run at the same time (L2 reuse)
+    const int32_t n_items = (int32_t)pl.items.size();
+    std::vector<int32_t> idx(n_items);
+    for (int32_t i = 0; i < n_items; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return order_key[a] < order_key[b]; });
+    pl.n_ctas = std::max<int32_t>(1, std::min<int32_t>(sms, n_items));
+    std::vector<std::vector<int32_t>> per(pl.n_ctas);
+    std::set<std::pair<int64_t, int32_t>> load;
+    for (int32_t cc = 0; cc < pl.n_ctas; ++cc) load.insert({0, cc});
+    for (int32_t i : idx) {
+      auto lo = *load.begin();
+      load.erase(load.begin());
+      per[lo.second].push_back(i);
+      load.insert({lo.first + item_cost[i], lo.second});
+    }
+    pl.sched_ptr.assign(1, 0);
+    for (auto& v : per) {
+      pl.sched_items.insert(pl.sched_items.end(), v.begin(), v.end());
+      pl.sched_ptr.push_back((int32_t)pl.sched_items.size());
+    }
+    // item records (k::ItemRec)
+    pl.item_recs.assign(pl.items.size() * sizeof(k::ItemRec), 0);
+    for (size_t i = 0; i < pl.items.size(); ++i) {
+      const DevItem& it = pl.items[i];
+      k::ItemRec r{};
+      r.k0 = it.key_begin;
+      r.k1 = it.key_end;
+      r.n_tiles = (it.key_end - it.key_begin + kTileKeys - 1) / kTileKeys;
+      int32_t ng = 0, gmask = 0;
+      for (int o = 0; o < it.n_warps; ++o) {
+        const DevWarp& w = pl.warps[it.warp_off + o];
+        const bool first = o == 0 || w.res_off != pl.warps[it.warp_off + o - 1].res_off ||
+                           w.adapter_slot != pl.warps[it.warp_off + o - 1].adapter_slot;
+        if (first) { ++ng; gmask |= 1 << o; }
+        r.n_rows[o] = w.n_rows;
+        r.entry_off[o] = w.entry_off;
+        for (int j = 0; j < w.n_rows; ++j) {
+          const int64_t v = (int64_t)pl.rows[w.row_off + j].pos - it.key_begin + 1;
+          r.pos1[16 * o + j] = (uint16_t)std::min<int64_t>(65535, std::max<int64_t>(0, v));
+        }
+      }
+      r.meta = it.n_warps | (ng << 4) | (gmask << 8) | (it.kv_head << 16);
+      std::memcpy(pl.item_recs.data() + i * sizeof(k::ItemRec), &r, sizeof(r));
+    }
+    // tile records (the residual loader and the TMA producer stream them instead of chasing page tables)
+    pl.tile_ptr.assign(1, 0);
+    pl.tile_recs.clear();
+    for (auto& v : per) {
+      for (int32_t i : v) {
+        const DevItem& it = pl.items[i];
+        int32_t meta = it.n_warps, ng = 0, gmask = 0;
+        for (int o = 0; o < it.n_warps; ++o) {
+          const DevWarp& w = pl.warps[it.warp_off + o];
+          const bool first = o == 0 || w.res_off != pl.warps[it.warp_off + o - 1].res_off ||
+                             w.adapter_slot != pl.warps[it.warp_off + o - 1].adapter_slot;
+          if (first) { ++ng; gmask |= 1 << o; }
+        }
+        meta |= (ng << 4) | (gmask << 8) | (it.kv_head << 16);
+        for (int32_t t0 = it.key_begin; t0 < it.key_end; t0 += kTileKeys) {
+          const int32_t sl = t0 / P;
+          int32_t rec[8] = {t0, it.key_end, meta, -1, -1, -1, -1, pl.base_pages[it.base_off + sl]};
+          for (int o = 0; o < it.n_warps; ++o) rec[3 + o] = pl.res_pages[pl.warps[it.warp_off + o].res_off + sl];
+          pl.tile_recs.insert(pl.tile_recs.end(), rec, rec + 8);
+        }
+      }
+      pl.tile_ptr.push_back((int32_t)(pl.tile_recs.size() / 8));
     }
   }
   if (entries > INT32_MAX) throw Error(FKV_E_INVALID, "plan: too many partial entries");
@@ -271,8 +361,17 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   pl.off_outent = put(pl.blob, pl.out_entries);
   pl.off_adapters = put(pl.blob, pl.adapter_ptrs);
   pl.off_qrow = put(pl.blob, pl.qrow_seq);
+  pl.off_sptr = put(pl.blob, pl.sched_ptr);
+  pl.off_sitems = put(pl.blob, pl.sched_items);
+  pl.off_tptr = put(pl.blob, pl.tile_ptr);
+  pl.off_trecs = put(pl.blob, pl.tile_recs);
+  pl.off_irecs = put(pl.blob, pl.item_recs);
   pl.blob.resize(align256(pl.blob.size()));
   pl.ws_bytes = align256((size_t)pl.n_entries * (size_t)(2 + d + r) * sizeof(float));
+  if (pl.kernel == 2) {
+    pl.stage_off = pl.ws_bytes;
+    pl.ws_bytes += align256(pl.warps.size() * (size_t)k::kStageBytes);
+  }
   return plan.release();
 }
 
@@ -322,9 +421,19 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.scale_log2 = scale * 1.4426950408889634f;
   a.dbg = (long long*)c.dbg;
   a.dbg_block = c.dbg_block;
-  { const char* e = getenv("FKV_TC_PREFETCH"); a.tc_prefetch = e ? atoi(e) : 2; }
+  a.max_pos = c.cfg.max_pos;
+  { const char* e = getenv("FKV_TC_PREFETCH"); a.tc_prefetch = e ? atoi(e) : 3; }
+  a.res_swz = c.cfg.dtype == FKV_DTYPE_BF16 && c.cfg.rank == 16;
+  a.sched_ptr = (const int32_t*)(base + p.off_sptr);
+  a.sched_items = (const int32_t*)(base + p.off_sitems);
+  a.tile_ptr = (const int32_t*)(base + p.off_tptr);
+  a.tile_recs = (const int4*)(base + p.off_trecs);
+  a.item_recs = (const k::ItemRec*)(base + p.off_irecs);
+  a.n_ctas = p.n_ctas;
+  a.stage = p.kernel == 2 ? (uint8_t*)ws + p.stage_off : nullptr;
   cudaError_t e = cudaSuccess;
-  if (phases & FKV_PHASE_MAIN)
+  if ((phases & FKV_PHASE_MAIN) && p.kernel == 2) e = k::launch_stage(a, (int32_t)p.warps.size(), (cudaStream_t)stream);
+  if (e == cudaSuccess && (phases & FKV_PHASE_MAIN))
     e = p.kernel == 2   ? k::launch_attention_tc(a, c.tc_maps.data(), (cudaStream_t)stream)
         : p.kernel == 0 ? k::launch_attention_mma(a, (cudaStream_t)stream)
                         : k::launch_attention_simt(a, (cudaStream_t)stream);

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1) ra_mma_kernel(AttnParams p) {
         const bool valid = t < it.key_end;
         const int tt = valid ? t : it.key_begin;
         const int pg = p.res_pages[w.res_off + tt / P];
-        const int64_t off = ((int64_t)pg * P + (tt % P)) * kR + ch * 8;
+        const int64_t off = ((int64_t)pg * P + (tt % P)) * kR + res_col(tt % P, ch * 8, p.res_swz);
         cp_async16(smem_u32(rk_s + r_off(row, ch)), Rk + off, valid);
         cp_async16(smem_u32(rv_s + r_off(row, ch)), Rv + off, valid);
       }

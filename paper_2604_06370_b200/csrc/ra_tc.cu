@@ -1,35 +1,39 @@
 // Grouped ResidualAttention on 5th-generation tensor cores (tcgen05 + TMEM +
 // TMA), bf16 in / fp32 accumulate, d = 128, r = 16: the hot loop of §8(a)
-// row a5 for items whose rows share a base-page segment.
+// rows a5 (decode) and a7 (chunked prefill) for plan items whose query rows
+// share a base-page segment.
 //
-// One CTA = one plan item: kv head h, key range [k0, k1) of a base-page
-// segment shared by all its query rows, up to 4 "slots" of 16 rows; a slot
-// belongs to one residual owner (adapter + residual pages), consecutive slots
-// of one owner form a group. The key tile (128 keys) sits on the TMEM lanes
-// (M = keys), the CTA's 64 query rows on N, so per-owner residual terms are
-// plain N-slices of the same accumulator:
+// Persistent kernel: one CTA per SM walks its list of plan items (kv head h,
+// key range [k0, k1) of a shared segment, up to 4 "slots" of 16 query rows; a
+// slot belongs to one residual owner = adapter + residual pages; consecutive
+// slots of one owner form a group).  Keys sit on the TMEM lanes (M = 128 keys
+// per tile), the item's 64 query rows on N, so every per-owner residual term
+// is an N-slice of the same accumulator:
 //
-//   Stage 1 (Alg1.332-336)   S^T  = K_base Q^T                    [tcgen05 SS]
-//     DEFERRED (paper):      KL   = R_k,g B_k,g for one half of d; B_k's
-//                            columns are permuted so a half holds the RoPE
-//                            pairs (i, i+64)                       [tcgen05 SS]
-//                            key warps: KL <- RoPE_t(KL) in fp32x2, bf16
-//                            written back in place in TMEM       [tcgen05.ld/st]
-//                            S^T[:, rows of g] += KL Q_g^T       [tcgen05 TS]
-//     NONE (north-star split): S^T[:, rows of g] += R_k,g (Q_g B_k,g^T)^T [SS]
-//   Stage 2 (Alg1.338-346)   key warps: one online softmax per query row
-//                            (a column of S^T), lazily rescaled; P^T -> smem
-//                            O^T  += V_base^T P^T                [tcgen05 SS]
-//                            A^T  += [R_v,0..3 ; 1]^T P^T        [tcgen05 SS]
-//                            (the all-ones slot accumulates the row sums l)
-//   Stage 3 (Alg1.348-350)   in the combine kernel (late V fusion, Eq.4).
+//   Stage 1 (Alg1.332-336)  S^T  = K_base Q^T                          [SS]
+//     NONE (north-star split, Eq.4 applied to K):
+//                           S^T[:, rows of g] += R_k,g (Q_g B_k,g^T)^T  [SS]
+//     DEFERRED (paper, Alg1.335): KL = R_k,g B_k,g per 32-column quarter
+//                           block of d (RoPE pairs (i, i+64) side by side)
+//                           [SS] -> key warps rotate KL at the key's
+//                           absolute position in fp32 and write bf16 back in
+//                           place -> S^T[:, rows of g] += KL Q_g^T       [TS]
+//   Stage 2 (Alg1.338-346)  key warps: online softmax per query row (one
+//                           column of S^T), lazily rescaled; P^T -> smem
+//                           O^T += V_base^T P^T                         [SS]
+//                           A^T += [R_v,0..3 ; 1]^T P^T (the all-ones slot
+//                           accumulates the row sums l)                 [SS]
+//   Stage 3 (Alg1.348-350)  combine kernel (late V fusion, Eq.4).
 //
-// 12 warps: warpgroup 2 = control (warp 8 TMA producer, 9/10 S-side MMA issuers (10 also allocates
-// TMEM), 11 PV-side MMA issuer; setmaxnreg.dec; high warp ids win the issue arbiter), warpgroups 0, 1
-// = key warps (thread = TMEM lane = key of the tile; WG1 owns d-half 0 of the
-// K_lora rebuild and query columns 0..31, WG2 d-half 1 and columns 32..63;
-// setmaxnreg.inc).  Buffers: K_base x1 (released right after S^T), R_k x2,
-// V_base x2, R_v x2.
+// 12 warps: warp 8 = TMA producer (K-side ring of 16 KB slabs: K_base d-half
+// 0/1 and R_k of the item's groups; V-side ring of 64-key halves: V_base +
+// R_v + ones; per-item Q / q~ / packed-B_k images), warp 9 = S-side MMA
+// issuer, warp 10 = PV-side MMA issuer, warp 11 = TMEM allocator (the
+// control warps have the high warp ids, which win the issue arbiter), warps
+// 0..7 = key warps (thread = TMEM lane = key of the tile; key warpgroup w owns query
+// columns [32w, 32w+32) and, in DEFERRED, the d-half w of the rotation).
+// S^T is double-buffered in TMEM so S(j+1) overlaps softmax(j); P^T is
+// double-buffered in smem so PV(j) overlaps softmax(j+1).
 #include <cuda_bf16.h>
 
 #include <cstddef>
@@ -44,42 +48,123 @@ namespace {
 using namespace sm100;
 
 constexpr int kD = 128, kR = 16, kTile = 128, kRows = 64, kSlots = 4;
-// shared memory map (bytes from the 1024-aligned dynamic smem base)
-constexpr uint32_t OFF_KB = 0;                       // K_base [2 d-halves][128 keys][128 B]  32 KB
-constexpr uint32_t OFF_RK = 32768;                   // R_k x2 stages x 4 slots x 4 KB       32 KB
-constexpr uint32_t OFF_V = 65536;                    // V_base x2 stages                      64 KB
-constexpr uint32_t OFF_RV = 131072;                  // R_v x2 stages x 5 slots (slot 4 = 1)  40 KB
-constexpr uint32_t kRvStage = 5 * 4096;
-constexpr uint32_t OFF_Q = OFF_RV + 2 * kRvStage;    // Q rows, K-major SW128               16 KB
-constexpr uint32_t OFF_BK = OFF_Q + 16384;           // B_k slots (DEFERRED) | q~ (NONE)     16 KB
-constexpr uint32_t OFF_P = OFF_BK + 16384;           // P^T [128 keys][64 rows]             16 KB
-constexpr uint32_t OFF_MISC = OFF_P + 16384;
-constexpr uint32_t kSmemBytes = OFF_MISC + 3072;
-// TMEM columns
-// S^T is split in two accumulators: S0 = K_base Q^T + the d-half-0 residual terms (key warpgroup 0),
-// S1 = the d-half-1 residual terms (key warpgroup 1); the softmax adds them.
-constexpr uint32_t T_S = 0, T_S1 = 64, T_O = 128, T_A = 192, T_KL = 256;  // KL: [wg][4 bufs] x 32 columns
 constexpr int kKlBufs = 4;
+// TMEM columns: S^T x2 | O^T | A^T | KL [wg][4 bufs] x 32 (DEFERRED)
+constexpr uint32_t T_S = 0, T_O = 128, T_A = 192, T_KL = 256;
+
+template <bool kDef>
+struct Cfg {
+  // R_k (small) is single-buffered with its pages L2-prefetched two tiles ahead; V_base / R_v wait for softmax(T):
+  // a deeper ring; P^T double-buffered so softmax(T+1) overlaps PV(T)
+  static constexpr int KS = 2;                   // K_base ring (32 KB: one 128-key tile, both d-halves)
+  static constexpr int RS = 1;                   // R_k ring (16 KB: 4 slots x 128 keys x 32 B), L2-prefetched
+  static constexpr int VS = 3;                   // V-side ring (26 KB: 64-key half of V_base | R_v 4 slots | ones)
+  static constexpr int NP = 2;                   // P^T buffers (16 KB)
+  static constexpr int NQ = kDef ? 1 : 2;        // per-item Q / X buffers
+  static constexpr int AB = kDef ? 1 : 2;        // O^T / A^T accumulator sets in TMEM (NONE: the KL columns are free)
+  static constexpr uint32_t XB = kDef ? 4096 : 512;  // per-slot X image: packed B_k | q~
+  static constexpr uint32_t VE = 26624;
+  static constexpr uint32_t OFF_V = 0;
+  static constexpr uint32_t OFF_K = OFF_V + VS * VE;
+  static constexpr uint32_t OFF_R = OFF_K + KS * 32768;
+  static constexpr uint32_t OFF_Q = OFF_R + RS * 16384;  // [NQ][2 d-halves][64 rows][128 B]
+  static constexpr uint32_t OFF_P = OFF_Q + NQ * 16384;  // [NP][128 keys / 8][8][64 cols x 2 B]
+  static constexpr uint32_t OFF_X = OFF_P + NP * 16384;  // [NQ][4 slots][XB]
+  static constexpr uint32_t OFF_MISC = OFF_X + NQ * kSlots * XB;
+  static constexpr uint32_t SMEM = OFF_MISC + 1024;
+  static_assert(SMEM <= 232448, "shared memory");
+};
 
 struct Misc {
-  uint64_t kbfull, kbempty, rkfull[2], rkempty[2], vfull[2], vempty[2], sfull[2], sfree, klfull[2][kKlBufs], klready[2][kKlBufs],
-      pfull, pvdone;
+  uint64_t kfull[2], kempty[2], rfull[1], rempty[1], vfull[3], vempty[3], rvfull[3], qfull[2], qempty[2], sfull[2], sfree[2], pfull[2], pfree[2],
+      accfree[2], klfull[2][kKlBufs], klready[2][kKlBufs];
   alignas(16) float m_run[kRows];
-  alignas(16) float alpha[kRows];
-  float red[2][4][32];
-  alignas(16) int32_t pos[kRows];
-  int32_t g_first[kSlots], g_cnt[kSlots];
-  int32_t slot_res[kSlots], slot_ad[kSlots];
-  int32_t n_groups, n_slots, causal;
+  alignas(16) ItemRec rec[2];  // per-item header (staged with the item's Q rows; NQ buffers)
   uint32_t tmem_base;
 };
-static_assert(sizeof(Misc) <= 3072, "misc");
-constexpr int kNumBars = 31;
-static_assert(offsetof(Misc, m_run) >= kNumBars * 8 && offsetof(Misc, m_run) % 16 == 0, "barriers");
+static_assert(sizeof(Misc) <= 1024, "misc");
 
 struct TcMaps {
+  // kb: P == 128: 3D {64, 128, 2} (a whole tile, both d-halves), else 2D {64, P}; vb: P >= 64: 3D {64, 64, 2},
+  // else 2D {64, P}; rk / rv: the residual pool viewed as 128-byte rows, {64, P / 4} / {64, min(P, 64) / 4}
   CUtensorMap kb, vb, rk, rv;
 };
+
+struct ItemInfo {
+  int h, k0, k1, base_off, warp_off, n_slots, n_groups, n_tiles;
+  int g_first[kSlots], g_cnt[kSlots], slot_res[kSlots];
+};
+
+__device__ __forceinline__ void load_item(const AttnParams& p, int idx, ItemInfo& I) {
+  const DevItem it = p.items[idx];
+  I.h = it.kv_head;
+  I.k0 = it.key_begin;
+  I.k1 = it.key_end;
+  I.base_off = it.base_off;
+  I.warp_off = it.warp_off;
+  I.n_slots = it.n_warps;
+  I.n_tiles = (it.key_end - it.key_begin + kTile - 1) / kTile;
+  int ng = 0, prev_res = -1, prev_ad = -1;
+  for (int o = 0; o < kSlots; ++o) {
+    if (o < it.n_warps) {
+      const DevWarp w = p.warps[it.warp_off + o];
+      I.slot_res[o] = w.res_off;
+      if (o > 0 && w.res_off == prev_res && w.adapter_slot == prev_ad) {
+        I.g_cnt[ng - 1]++;
+      } else {
+        I.g_first[ng] = o;
+        I.g_cnt[ng] = 1;
+        ++ng;
+      }
+      prev_res = w.res_off;
+      prev_ad = w.adapter_slot;
+    }
+  }
+  I.n_groups = ng;
+}
+
+// group structure from a staged item header
+__device__ __forceinline__ void item_from_rec(const ItemRec& r, ItemInfo& I) {
+  I.k0 = r.k0;
+  I.k1 = r.k1;
+  I.n_tiles = r.n_tiles;
+  I.n_slots = r.meta & 15;
+  int ng = 0;
+  for (int o = 0; o < I.n_slots; ++o) {
+    if ((r.meta >> (8 + o)) & 1) {
+      I.g_first[ng] = o;
+      I.g_cnt[ng] = 1;
+      ++ng;
+    } else {
+      I.g_cnt[ng - 1]++;
+    }
+  }
+  I.n_groups = ng;
+}
+
+// the fields the key warps need (no per-slot arrays: keeps them in registers)
+struct ItemLite {
+  int k0, k1, warp_off, n_slots, n_groups, n_tiles;
+};
+__device__ __forceinline__ void load_item_lite(const AttnParams& p, int idx, ItemLite& I) {
+  const DevItem it = p.items[idx];
+  I.k0 = it.key_begin;
+  I.k1 = it.key_end;
+  I.warp_off = it.warp_off;
+  I.n_slots = it.n_warps;
+  I.n_tiles = (it.key_end - it.key_begin + kTile - 1) / kTile;
+  int ng = 0, prev_res = -1, prev_ad = -1;
+#pragma unroll
+  for (int o = 0; o < kSlots; ++o) {
+    if (o < it.n_warps) {
+      const DevWarp w = p.warps[it.warp_off + o];
+      if (!(o > 0 && w.res_off == prev_res && w.adapter_slot == prev_ad)) ++ng;
+      prev_res = w.res_off;
+      prev_ad = w.adapter_slot;
+    }
+  }
+  I.n_groups = ng;
+}
 
 __device__ __forceinline__ bool bar_or(uint32_t id, uint32_t n, bool pred) {
   uint32_t r;
@@ -125,9 +210,56 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void unpack_h2(uint32_t v, float& lo, float& hi) {
+  asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}\n"
+      : "=f"(lo), "=f"(hi)
+      : "r"(v));
+}
+__device__ __forceinline__ void atomic_max_f(float* a, float v) {
+  if (v >= 0.f)
+    atomicMax((int*)a, __float_as_int(v));
+  else
+    atomicMin((unsigned int*)a, __float_as_uint(v));
+}
+// tcgen05 issue from a whole warp: one elected lane issues (uniform operands keep ptxas on the uniform datapath)
+__device__ __forceinline__ void mma_ss_e(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_e(uint32_t mbar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(mbar)
+      : "memory");
+}
 
-// diagnostics: clock64 stamp of pipeline event e for tile j of CTA dbg_block
-__device__ __forceinline__ void ev(const AttnParams& p, int e, int j) {
+// arrive on `bar` when all of this thread's prior cp.async copies have landed (no count increment)
+__device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// diagnostics: clock64 stamp of pipeline event e for index j (< 256) of CTA dbg_block (fkv_debug_timeline)
+__device__ __forceinline__ void ev(const AttnParams& p, int e, uint32_t j) {
   if (p.dbg && (int)blockIdx.x == p.dbg_block && j < 256) p.dbg[e * 256 + j] = clock64();
 }
 
@@ -138,594 +270,948 @@ __device__ __forceinline__ int perm_d(int n) {
   return 32 * (b >> 1) + 16 * (b & 1) + (c < 16 ? c : 64 + c - 16);
 }
 
+// ---------------------------------------------------------------------------
+// Stage kernel: per warp slot (16 query rows of one owner), the exact shared-
+// memory images the main kernel bulk-copies: Q rows (K-major SW128, both
+// d-halves, 2 KB each) and q~ = Q B_k^T (NONE, K-major SW32, 512 B) or B_k^h
+// with permuted columns (DEFERRED, MN-major SW64 quarter blocks, 4 KB).
+__global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_warps) {
+  const int wi = blockIdx.x;
+  if (wi >= n_warps) return;
+  __shared__ __align__(16) float qs[16][kD];
+  const DevWarp w = p.warps[wi];
+  uint8_t* img = p.stage + (int64_t)wi * kStageBytes;
+  const int tid = threadIdx.x;
+  const DevItem* dummy = nullptr;
+  (void)dummy;
+  // kv head of this slot: any row's q head / group (padding rows have seq < 0)
+  int h = 0;
+  {
+    const DevRow r0 = p.rows[w.row_off];
+    h = r0.qh / p.group;
+  }
+  for (int c = tid; c < 16 * 16; c += 128) {
+    const int row = c >> 4, ch = c & 15;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < w.n_rows) {
+      const DevRow rw = p.rows[w.row_off + row];
+      v = __ldg((const uint4*)((const __nv_bfloat16*)p.Q + ((int64_t)(p.seqs[rw.seq].q_row0 + rw.qi) * p.hq + rw.qh) * kD) +
+                ch);
+    }
+    *(uint4*)(img + (ch >> 3) * 2048 + kmajor_off(row, (ch & 7) * 8, 8, 1024, 0)) = v;
+    const __nv_bfloat162* b2 = (const __nv_bfloat162*)&v;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(b2[e]);
+      qs[row][ch * 8 + 2 * e] = f.x;
+      qs[row][ch * 8 + 2 * e + 1] = f.y;
+    }
+  }
+  __syncthreads();
+  const __nv_bfloat16* Bk = (const __nv_bfloat16*)p.adapters[2 * w.adapter_slot] +
+                            (int64_t)p.layer * p.adapter_layer_stride + (int64_t)h * kR * kD;
+  if (p.rope_mode == FKV_ROPE_DEFERRED) {
+    for (int c = tid; c < kR * (kD / 8); c += 128) {
+      const int jj = c >> 4, n8 = (c & 15) * 8;
+      const uint4 v = __ldg((const uint4*)(Bk + jj * kD + perm_d(n8)));
+      *(uint4*)(img + 4096 + mnmajor_off(n8, jj, 4, 1024, 512)) = v;
+    }
+  } else {
+    for (int c = tid; c < 16 * kR; c += 128) {
+      const int row = c >> 4, jj = c & 15;
+      float acc = 0.f;
+      for (int d8 = 0; d8 < kD; d8 += 8) {
+        const uint4 bv = __ldg((const uint4*)(Bk + jj * kD + d8));
+        const __nv_bfloat162* b2 = (const __nv_bfloat162*)&bv;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 b = __bfloat1622float2(b2[e]);
+          acc += qs[row][d8 + 2 * e] * b.x + qs[row][d8 + 2 * e + 1] * b.y;
+        }
+      }
+      *(__nv_bfloat16*)(img + 4096 + kmajor_off(row, jj, 2, 256, 0)) = __float2bfloat16_rn(row < w.n_rows ? acc : 0.f);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <bool kDef>
 __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ TcMaps maps, AttnParams p) {
+  using C = Cfg<kDef>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
-  Misc& ms = *reinterpret_cast<Misc*>(smem + OFF_MISC);
+  Misc& ms = *reinterpret_cast<Misc*>(smem + C::OFF_MISC);
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (sbase & 1023) __trap();
-  if (tid == 0) ev(p, 20, 0);
-  const DevItem it = p.items[blockIdx.x];
-  const int h = it.kv_head;
-  const int k0 = it.key_begin, k1 = it.key_end;
-  const int n_tiles = (k1 - k0 + kTile - 1) / kTile;
+  const long long t_start = clock64();
+  const int cta = blockIdx.x;
+  const int it_begin = p.sched_ptr[cta], it_end = p.sched_ptr[cta + 1];
+  const int n_my = it_end - it_begin;
   const int P = p.P;
-  const bool deferred = p.rope_mode == FKV_ROPE_DEFERRED;
 
   // ---------------- setup ----------------
   if (tid == 0) {
-    ms.n_slots = it.n_warps;
-    int ng = 0, causal = 0;
-    for (int o = 0; o < it.n_warps; ++o) {
-      const DevWarp w = p.warps[it.warp_off + o];
-      ms.slot_res[o] = w.res_off;
-      ms.slot_ad[o] = w.adapter_slot;
-      if (o > 0 && w.res_off == ms.slot_res[o - 1] && w.adapter_slot == ms.slot_ad[o - 1]) {
-        ms.g_cnt[ng - 1]++;
-      } else {
-        ms.g_first[ng] = o; ms.g_cnt[ng] = 1; ++ng;
-      }
-      for (int i = 0; i < w.n_rows; ++i)
-        if (p.rows[w.row_off + i].pos < k1 - 1) causal = 1;
+    for (int i = 0; i < C::KS; ++i) { mbar_init(smem_u32(&ms.kfull[i]), 1); mbar_init(smem_u32(&ms.kempty[i]), 1); }
+    // rfull / rvfull: one cp.async.mbarrier.arrive.noinc per lane of the copying warp
+    for (int i = 0; i < C::RS; ++i) { mbar_init(smem_u32(&ms.rfull[i]), 32); mbar_init(smem_u32(&ms.rempty[i]), 1); }
+    for (int i = 0; i < C::VS; ++i) {
+      mbar_init(smem_u32(&ms.vfull[i]), 1);
+      mbar_init(smem_u32(&ms.vempty[i]), 1);
+      mbar_init(smem_u32(&ms.rvfull[i]), 32);
     }
-    ms.n_groups = ng;
-    ms.causal = causal;
-    uint64_t* bars = &ms.kbfull;
-    for (int i = 0; i < kNumBars; ++i) mbar_init(smem_u32(bars + i), 1);
-    mbar_init(smem_u32(&ms.sfree), 256);
-    if (p.rope_mode == FKV_ROPE_DEFERRED) {  // both S-side issuers release R_k
-      mbar_init(smem_u32(&ms.rkempty[0]), 2);
-      mbar_init(smem_u32(&ms.rkempty[1]), 2);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&ms.qfull[i]), 1);
+      mbar_init(smem_u32(&ms.qempty[i]), 3);  // S-side commit + one arrive per key warpgroup
+      mbar_init(smem_u32(&ms.sfull[i]), 1);
+      mbar_init(smem_u32(&ms.sfree[i]), 256);
+      mbar_init(smem_u32(&ms.pfull[i]), 256);
+      mbar_init(smem_u32(&ms.pfree[i]), 1);
     }
-    mbar_init(smem_u32(&ms.pfull), 256);
+    mbar_init(smem_u32(&ms.accfree[0]), 256);
+    mbar_init(smem_u32(&ms.accfree[1]), 256);
     for (int w = 0; w < 2; ++w)
-      for (int b = 0; b < kKlBufs; ++b) mbar_init(smem_u32(&ms.klready[w][b]), 128);
+      for (int b = 0; b < kKlBufs; ++b) {
+        mbar_init(smem_u32(&ms.klfull[w][b]), 1);
+        mbar_init(smem_u32(&ms.klready[w][b]), 128);
+      }
     fence_mbar_init();
   }
-  if (wid == 10) tmem_alloc(smem_u32(&ms.tmem_base), 512);
-  if (tid < kRows) {
-    ms.m_run[tid] = -INFINITY;
-    const int o = tid >> 4, i = tid & 15;
-    int pos = -1;
-    if (o < it.n_warps) {
-      const DevWarp w = p.warps[it.warp_off + o];
-      if (i < w.n_rows) pos = p.rows[w.row_off + i].pos;
-    }
-    ms.pos[tid] = pos;
-  }
-  // Q rows -> K-major SW128 (B operand of S^T = K Q^T); zero rows for padding
-  for (int c = tid; c < kRows * 16; c += 384) {
-    const int row = c >> 4, ch = c & 15;
-    const int o = row >> 4, i = row & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (o < it.n_warps) {
-      const DevWarp w = p.warps[it.warp_off + o];
-      if (i < w.n_rows) {
-        const DevRow rw = p.rows[w.row_off + i];
-        v = __ldg((const uint4*)((const __nv_bfloat16*)p.Q +
-                                 ((int64_t)(p.seqs[rw.seq].q_row0 + rw.qi) * p.hq + rw.qh) * kD) + ch);
-      }
-    }
-    *(uint4*)(smem + OFF_Q + kmajor_off(row, ch * 8, 8, 1024, 8192)) = v;
-  }
-  // all-ones R_v slot 4 of both stages: A^T lanes 64..79 accumulate the row sums l
-  for (int c = tid; c < 2 * 256; c += 384)
-    *(uint4*)(smem + OFF_RV + (c >> 8) * kRvStage + 4 * 4096 + (c & 255) * 16) =
+  if (wid == 11) tmem_alloc(smem_u32(&ms.tmem_base), 512);
+  // the all-ones R_v slot (index 4) of every V-side entry: A^T lanes 64..79 accumulate the row sums l
+  for (int c = tid; c < C::VS * 128; c += 384)
+    *(uint4*)(smem + C::OFF_V + (c >> 7) * C::VE + 16384 + 4 * 2048 + (c & 127) * 16) =
         make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
-  __syncthreads();
-  const int n_groups = ms.n_groups, n_slots = ms.n_slots;
-  if (deferred) {
-    // B_k^h of each slot, columns permuted, MN-major SW64 [quarter block][16 r][32]
-    for (int c = tid; c < n_slots * kR * (kD / 8); c += 384) {
-      const int o = c / (kR * 16), e = c % (kR * 16), jj = e >> 4, n8 = (e & 15) * 8;
-      const __nv_bfloat16* Bk = (const __nv_bfloat16*)p.adapters[2 * ms.slot_ad[o]] +
-                                (int64_t)p.layer * p.adapter_layer_stride + (int64_t)h * kR * kD + jj * kD;
-      // 8 consecutive permuted columns n8..n8+7 map to 8 consecutive d
-      const uint4 v = __ldg((const uint4*)(Bk + perm_d(n8)));
-      *(uint4*)(smem + OFF_BK + o * 4096 + mnmajor_off(n8, jj, 4, 1024, 512)) = v;
-    }
-  } else {
-    // q~ = Q B_k^T per row (the north-star split), bf16, K-major SW32
-    for (int c = tid; c < kRows * kR; c += 384) {
-      const int row = c >> 4, jj = c & 15, o = row >> 4;
-      float acc = 0.f;
-      if (o < n_slots) {
-        const __nv_bfloat16* Bk = (const __nv_bfloat16*)p.adapters[2 * ms.slot_ad[o]] +
-                                  (int64_t)p.layer * p.adapter_layer_stride + (int64_t)h * kR * kD + jj * kD;
-        for (int d8 = 0; d8 < kD; d8 += 8) {
-          const uint4 qv = *(const uint4*)(smem + OFF_Q + kmajor_off(row, d8, 8, 1024, 8192));
-          const uint4 bv = __ldg((const uint4*)(Bk + d8));
-          const __nv_bfloat162* q2 = (const __nv_bfloat162*)&qv;
-          const __nv_bfloat162* b2 = (const __nv_bfloat162*)&bv;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 a = __bfloat1622float2(q2[e]), b = __bfloat1622float2(b2[e]);
-            acc += a.x * b.x + a.y * b.y;
-          }
-        }
-      }
-      *(__nv_bfloat16*)(smem + OFF_BK + kmajor_off(row, jj, 2, 256, 0)) = __float2bfloat16_rn(acc);
-    }
-  }
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = ms.tmem_base;
-  if (tid == 0) ev(p, 21, 0);
 
   if (wid >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
-    if (wid == 8 && lane == 0) {
-      // ================= TMA producer =================
+    if (wid == 8 && P == kTile) {
+      // ================= producer, fast path (P = 128: one page per tile), whole warp =================
+      // TMA (lane 0): K_base tiles, V_base halves, per-item Q / X images; cp.async (all lanes): R_k tiles.
+      // Page ids come from the tile records, each stream's next record preloaded (no page-table chasing).
+      tma_prefetch_desc(&maps.kb); tma_prefetch_desc(&maps.vb);
+      const __nv_bfloat16* rkl = (const __nv_bfloat16*)p.res_k + (int64_t)p.layer * p.res_layer_stride;
+      const int64_t brow_l = (int64_t)p.layer * p.nb;
+      const int r0 = p.tile_ptr[cta], nrec = p.tile_ptr[cta + 1] - r0;
+      auto ldrec = [&](int T, int4& a, int4& b) {
+        if (T < nrec) {
+          a = __ldg(&p.tile_recs[2 * (r0 + T)]);
+          b = __ldg(&p.tile_recs[2 * (r0 + T) + 1]);
+        }
+      };
+      auto base_row = [&](const int4& a, const int4& b) {  // 2D-view row of the tile's base page
+        return (int)(((brow_l + b.w) * p.hkv + (a.z >> 16)) * kTile);
+      };
+      int4 kA = make_int4(0, 0, 0, 0), kB = kA, vA = kA, vB = kA, rA = kA, rB = kA, fA = kA, fB = kA;
+      ldrec(0, kA, kB);
+      vA = kA; vB = kB; rA = kA; rB = kB;
+      constexpr int kPf = 2;  // L2 prefetch distance (tiles) of K_base and R_k
+      ldrec(kPf, fA, fB);
+      uint32_t nk = 0, nv = 0, nr = 0;
+      int iq = 0;
+      for (;;) {
+        bool busy = false, progress = false;
+        if (nk < (uint32_t)nrec) {  // K_base tile (32 KB, one 3D box)
+          busy = true;
+          const int slot = nk % C::KS;
+          if (nk < (uint32_t)C::KS || mbar_test(smem_u32(&ms.kempty[slot]), ((nk / C::KS) - 1) & 1)) {
+            if (lane == 0) {
+              ev(p, 0, nk);
+              const uint32_t bar = smem_u32(&ms.kfull[slot]);
+              mbar_expect_tx(bar, 32768);
+              tma_load_3d(sbase + C::OFF_K + slot * 32768, &maps.kb, 0, base_row(kA, kB), 0, bar);
+              if (nk + kPf < (uint32_t)nrec) tma_prefetch_l2_3d(&maps.kb, 0, base_row(fA, fB), 0);
+            }
+            if (nk + kPf < (uint32_t)nrec) {  // R_k pages of tile nk + kPf -> L2 (one 128-byte line per lane)
+              const int pgs[4] = {fA.w, fB.x, fB.y, fB.z};
+#pragma unroll
+              for (int o = 0; o < kSlots; ++o)
+                if ((fA.z >> (8 + o)) & 1)
+                  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(rkl + (int64_t)pgs[o] * kTile * kR + lane * 64));
+            }
+            ++nk;
+            ldrec(nk, kA, kB);
+            ldrec(nk + kPf, fA, fB);
+            progress = true;
+          }
+        }
+        if (nr < (uint32_t)nrec) {  // R_k of the tile's groups (cp.async, 4 KB per group)
+          busy = true;
+          const int slot = nr % C::RS;
+          if (nr < (uint32_t)C::RS || mbar_test(smem_u32(&ms.rempty[slot]), ((nr / C::RS) - 1) & 1)) {
+            const uint32_t dst = sbase + C::OFF_R + slot * 16384;
+            const int pgs[4] = {rA.w, rB.x, rB.y, rB.z};
+#pragma unroll
+            for (int o = 0; o < kSlots; ++o) {
+              if ((rA.z >> (8 + o)) & 1) {
+                const __nv_bfloat16* src = rkl + (int64_t)pgs[o] * kTile * kR;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  const int c = lane + 32 * u;
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + o * 4096 + c * 16),
+                               "l"(src + c * 8)
+                               : "memory");
+                }
+              }
+            }
+            cp_async_arrive(smem_u32(&ms.rfull[slot]));
+            ++nr;
+            ldrec(nr, rA, rB);
+            progress = true;
+          }
+        }
+        if (nv < 2u * nrec) {  // V_base 64-key half (16 KB, one 3D box)
+          busy = true;
+          const int slot = nv % C::VS;
+          if (nv < (uint32_t)C::VS || mbar_test(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1)) {
+            if (lane == 0) {
+              ev(p, 7, nv);
+              const uint32_t bar = smem_u32(&ms.vfull[slot]);
+              mbar_expect_tx(bar, 16384);
+              tma_load_3d(sbase + C::OFF_V + slot * C::VE, &maps.vb, 0, base_row(vA, vB) + 64 * (nv & 1), 0, bar);
+            }
+            ++nv;
+            if ((nv & 1) == 0) ldrec(nv >> 1, vA, vB);
+            progress = true;
+          }
+        }
+        if (iq < n_my) {  // per-item Q rows and q~ / packed B_k (staged images)
+          busy = true;
+          const int qb = iq % C::NQ;
+          if (iq < C::NQ || mbar_test(smem_u32(&ms.qempty[qb]), ((iq / C::NQ) - 1) & 1)) {
+            if (lane == 0) {
+              const DevItem it = p.items[p.sched_items[it_begin + iq]];
+              ev(p, 9, iq);
+              const uint32_t bar = smem_u32(&ms.qfull[qb]);
+              mbar_expect_tx(bar, it.n_warps * (4096 + C::XB) + (uint32_t)sizeof(ItemRec));
+              bulk_g2s(smem_u32(&ms.rec[qb]), p.item_recs + p.sched_items[it_begin + iq], sizeof(ItemRec), bar);
+              for (int o = 0; o < it.n_warps; ++o) {
+                const uint8_t* src = p.stage + (int64_t)(it.warp_off + o) * kStageBytes;
+                bulk_g2s(sbase + C::OFF_Q + qb * 16384 + o * 2048, src, 2048, bar);
+                bulk_g2s(sbase + C::OFF_Q + qb * 16384 + 8192 + o * 2048, src + 2048, 2048, bar);
+                bulk_g2s(sbase + C::OFF_X + qb * kSlots * C::XB + o * C::XB, src + 4096, C::XB, bar);
+              }
+            }
+            ++iq;
+            progress = true;
+          }
+        }
+        if (!busy) break;
+        if (!progress) __nanosleep(20);
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    } else if (wid == 8 && lane == 0) {
+      // ================= TMA producer (generic page size) =================
       tma_prefetch_desc(&maps.kb); tma_prefetch_desc(&maps.vb);
       tma_prefetch_desc(&maps.rk); tma_prefetch_desc(&maps.rv);
-      const int64_t brow_l = (int64_t)p.layer * p.nb;  // 2D views: row = ((layer*NB + page)*Hkv + h)*P
-      const int64_t rrow_l = (int64_t)p.layer * p.nr;  //                 (layer*NR + page)*P
-      const int pages = kTile / P;
-      auto row_of = [&](int t, bool base) -> int {  // 2D-view row of the page holding key t (clamped)
-        const int slot = (t < k1 ? t : k0) / P;
-        if (base) return (int)(((brow_l + p.base_pages[it.base_off + slot]) * p.hkv + h) * P);
-        return slot;
+      const int64_t brow_l = (int64_t)p.layer * p.nb;  // 2D views: row = ((layer*NB + page)*Hkv + h)*P + key
+      const int Pm = P < 64 ? P : 64;
+      const int pf = p.tc_prefetch;
+      ItemInfo Ik, Iv;
+      int ik = 0, jk = 0, iv = 0, jv = 0, eh = 0, iq = 0;
+      uint32_t nk = 0, nv = 0;
+      if (n_my > 0) { load_item(p, p.sched_items[it_begin], Ik); Iv = Ik; }
+      auto brow = [&](const ItemInfo& I, int sl) {
+        return (int)(((brow_l + p.base_pages[I.base_off + sl]) * p.hkv + I.h) * P);
       };
-      auto prefetch = [&](int j) {  // L2 prefetch of every box of tile j (hides DRAM latency)
-        if (j >= n_tiles) return;
-        const int t0 = k0 + j * kTile;
-        for (int q = 0; q < pages; ++q) {
-          const int t = t0 + q * P;
-          if (t >= k1) break;
-          const int row = row_of(t, true), slot = row_of(t, false);
-          if (P == 128) {  // base K/V only: the single-buffered K_base is the latency-critical stream
-            tma_prefetch_l2_3d(&maps.kb, 0, row, 0);
-            tma_prefetch_l2_3d(&maps.vb, 0, row, 0);
-          } else {
-            tma_prefetch_l2(&maps.kb, 0, row); tma_prefetch_l2(&maps.kb, 64, row);
-            tma_prefetch_l2(&maps.vb, 0, row); tma_prefetch_l2(&maps.vb, 64, row);
-          }
-          (void)slot;
+      auto next = [&](int& i, int& j, ItemInfo& I) {
+        if (++j == I.n_tiles) {
+          j = 0;
+          if (++i < n_my) load_item(p, p.sched_items[it_begin + i], I);
         }
       };
-      auto issue_rk = [&](int j) {
-        const int st = j & 1, t0 = k0 + j * kTile;
-        ev(p, 0, j);
-        const uint32_t bar = smem_u32(&ms.rkfull[st]);
-        mbar_expect_tx(bar, n_groups * kTile * kR * 2);
-        for (int q = 0; q < pages; ++q) {
-          const int slot = row_of(t0 + q * P, false);
-          for (int g = 0; g < n_groups; ++g) {
-            const int o = ms.g_first[g];
-            const int rp = p.res_pages[ms.slot_res[o] + slot];
-            tma_load_2d(sbase + OFF_RK + st * 16384 + o * 4096 + q * P * 32, &maps.rk, 0, (int)((rrow_l + rp) * P),
-                        bar);
+      for (;;) {
+        bool busy = false, progress = false;
+        // K_base tile (32 KB)
+        if (ik < n_my) {
+          busy = true;
+          const int slot = nk % C::KS;
+          if (nk < (uint32_t)C::KS || mbar_test(smem_u32(&ms.kempty[slot]), ((nk / C::KS) - 1) & 1)) {
+            const uint32_t dst = sbase + C::OFF_K + slot * 32768, bar = smem_u32(&ms.kfull[slot]);
+            ev(p, 0, nk);
+            const int t0 = Ik.k0 + jk * kTile;
+            if (pf > 0 && P == kTile) {
+              // L2 prefetch of the K_base / V_base tiles pf tiles ahead (L2 is the deep buffer, smem the short one)
+              int pi = ik, pj = jk + pf;
+              while (pi < n_my && pj >= (pi == ik ? Ik.n_tiles : 1 << 30)) { pj -= Ik.n_tiles; ++pi; break; }
+              if (pi == ik && pj < Ik.n_tiles) {
+                const int tp = Ik.k0 + pj * kTile;
+                const int row = brow(Ik, tp / P);
+                tma_prefetch_l2_3d(&maps.kb, 0, row, 0);
+                tma_prefetch_l2_3d(&maps.vb, 0, row, 0);
+                tma_prefetch_l2_3d(&maps.vb, 0, row + 64, 0);
+              }
+            }
+            mbar_expect_tx(bar, 32768);
+            if (P == kTile) {
+              tma_load_3d(dst, &maps.kb, 0, brow(Ik, (t0 < Ik.k1 ? t0 : Ik.k0) / P), 0, bar);
+            } else {
+              for (int q = 0; q < kTile / P; ++q) {
+                const int t = t0 + q * P;
+                const int row = brow(Ik, (t < Ik.k1 ? t : Ik.k0) / P);
+                tma_load_2d(dst + q * P * 128, &maps.kb, 0, row, bar);
+                tma_load_2d(dst + 16384 + q * P * 128, &maps.kb, 64, row, bar);
+              }
+            }
+            ++nk;
+            progress = true;
+            next(ik, jk, Ik);
           }
         }
-      };
-      auto issue_kb = [&](int j) {
-        const int t0 = k0 + j * kTile;
-        ev(p, 1, j);
-        const uint32_t bar = smem_u32(&ms.kbfull);
-        mbar_expect_tx(bar, kTile * kD * 2);
-        if (P == 128) {
-          tma_load_3d(sbase + OFF_KB, &maps.kb, 0, row_of(t0, true), 0, bar);
-        } else {
-          for (int q = 0; q < pages; ++q) {
-            const int row = row_of(t0 + q * P, true);
-            tma_load_2d(sbase + OFF_KB + q * P * 128, &maps.kb, 0, row, bar);
-            tma_load_2d(sbase + OFF_KB + 16384 + q * P * 128, &maps.kb, 64, row, bar);
+        // V-side: 64-key half of V_base (16 KB); the residual loader warp adds R_v of every slot
+        if (iv < n_my) {
+          busy = true;
+          const int slot = nv % C::VS;
+          if (nv < (uint32_t)C::VS || mbar_test(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1)) {
+            const uint32_t dst = sbase + C::OFF_V + slot * C::VE, bar = smem_u32(&ms.vfull[slot]);
+            ev(p, 7, nv);
+            mbar_expect_tx(bar, 16384);
+            for (int q = 0; q < 64 / Pm; ++q) {
+              const int t = Iv.k0 + jv * kTile + 64 * eh + q * Pm;
+              const int tt = t < Iv.k1 ? t : Iv.k0;
+              const int sl = tt / P, off = tt % P;
+              const int row = brow(Iv, sl) + off;
+              if (P >= 64) {
+                tma_load_3d(dst, &maps.vb, 0, row, 0, bar);
+              } else {
+                tma_load_2d(dst + q * Pm * 128, &maps.vb, 0, row, bar);
+                tma_load_2d(dst + 8192 + q * Pm * 128, &maps.vb, 64, row, bar);
+              }
+            }
+            ++nv;
+            progress = true;
+            if (++eh == 2) {
+              eh = 0;
+              next(iv, jv, Iv);
+            }
           }
         }
-      };
-      auto issue_v = [&](int j) {
-        const int st = j & 1, t0 = k0 + j * kTile;
-        ev(p, 2, j);
-        const uint32_t bar = smem_u32(&ms.vfull[st]);
-        mbar_expect_tx(bar, kTile * kD * 2 + n_slots * kTile * kR * 2);
-        for (int q = 0; q < pages; ++q) {
-          const int t = t0 + q * P;
-          const int row = row_of(t, true), slot = row_of(t, false);
-          if (P == 128) {
-            tma_load_3d(sbase + OFF_V + st * 32768, &maps.vb, 0, row, 0, bar);
-          } else {
-            tma_load_2d(sbase + OFF_V + st * 32768 + q * P * 128, &maps.vb, 0, row, bar);
-            tma_load_2d(sbase + OFF_V + st * 32768 + 16384 + q * P * 128, &maps.vb, 64, row, bar);
+        // per-item Q rows and q~ / packed B_k (staged images)
+        if (iq < n_my) {
+          busy = true;
+          const int qb = iq % C::NQ;
+          if (iq < C::NQ || mbar_test(smem_u32(&ms.qempty[qb]), ((iq / C::NQ) - 1) & 1)) {
+            const DevItem it = p.items[p.sched_items[it_begin + iq]];
+            ev(p, 9, iq);
+            const uint32_t bar = smem_u32(&ms.qfull[qb]);
+            mbar_expect_tx(bar, it.n_warps * (4096 + C::XB) + (uint32_t)sizeof(ItemRec));
+            bulk_g2s(smem_u32(&ms.rec[qb]), p.item_recs + p.sched_items[it_begin + iq], sizeof(ItemRec), bar);
+            for (int o = 0; o < it.n_warps; ++o) {
+              const uint8_t* src = p.stage + (int64_t)(it.warp_off + o) * kStageBytes;
+              bulk_g2s(sbase + C::OFF_Q + qb * 16384 + o * 2048, src, 2048, bar);
+              bulk_g2s(sbase + C::OFF_Q + qb * 16384 + 8192 + o * 2048, src + 2048, 2048, bar);
+              bulk_g2s(sbase + C::OFF_X + qb * kSlots * C::XB + o * C::XB, src + 4096, C::XB, bar);
+            }
+            ++iq;
+            progress = true;
           }
-          for (int o = 0; o < n_slots; ++o) {
-            const int rp = p.res_pages[ms.slot_res[o] + slot];
-            tma_load_2d(sbase + OFF_RV + st * kRvStage + o * 4096 + q * P * 32, &maps.rv, 0,
-                        (int)((rrow_l + rp) * P), bar);
-          }
         }
-      };
-      // three independent streams, each issued as soon as its buffer is free
-      const int kPrefetch = p.tc_prefetch;
-      for (int j = 0; j < kPrefetch; ++j) prefetch(j);
-
-      int nrk = 0, nkb = 0, nv = 0;
-      while (nrk < n_tiles || nkb < n_tiles || nv < n_tiles) {
-        bool progress = false;
-        if (nrk < n_tiles && (nrk < 2 || mbar_test(smem_u32(&ms.rkempty[nrk & 1]), ((nrk >> 1) - 1) & 1))) {
-          issue_rk(nrk);
-          if (kPrefetch) prefetch(nrk + kPrefetch);
-          ++nrk;
-          progress = true;
-        }
-        if (nkb < nrk && (nkb < 1 || mbar_test(smem_u32(&ms.kbempty), (nkb - 1) & 1))) {
-          issue_kb(nkb);
-          ++nkb;
-          progress = true;
-        }
-        if (nv < nrk && (nv < 2 || mbar_test(smem_u32(&ms.vempty[nv & 1]), ((nv >> 1) - 1) & 1))) {
-          issue_v(nv);
-          ++nv;
-          progress = true;
-        }
-        if (!progress) __nanosleep(64);  // yield issue slots to the key warps
+        if (!busy) break;
+        if (!progress) __nanosleep(20);
       }
-    } else if ((wid == 9 || (wid == 10 && deferred)) && lane == 0) {
-      // ================= S-side MMA issuers =================
-      // warp 1: S0 = K_base Q^T (+ NONE residual, or the d-half-0 DEFERRED units of key warpgroup 0)
-      // warp 2: S1 = the d-half-1 DEFERRED units of key warpgroup 1
-      const int w = wid - 9;
-      const uint32_t sacc = tm + (w ? T_S1 : T_S);
+    } else if (wid == 9) {
+      // ================= S-side MMA issuer (whole warp: uniform operands, one elected lane issues) =================
       const uint32_t id_s = idesc_bf16(128, kRows, false, false);
       const uint32_t id_rb = idesc_bf16(128, 32, false, true);
-      int Uw = 0;  // this warpgroup's K_lora unit counter (buffer = U % kKlBufs)
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        const uint32_t rk = sbase + OFF_RK + st * 16384;
-        mbar_wait_sleep(smem_u32(&ms.rkfull[st]), (j >> 1) & 1);
+      uint32_t T = 0, U = 0;
+      for (int ii = 0; ii < n_my; ++ii) {
+        const int qb = ii % C::NQ;
+        const uint32_t qs = sbase + C::OFF_Q + qb * 16384;
+        const uint32_t xs = sbase + C::OFF_X + qb * kSlots * C::XB;
+        mbar_wait(smem_u32(&ms.qfull[qb]), (ii / C::NQ) & 1);
+        ev(p, 10, ii);
         tc_fence_after();
-        if (w == 0) ev(p, 3, j);
-        const int n_units = deferred ? 2 * n_groups : 0;  // unit k = q * n_groups + g (quarter-major)
-        auto rb = [&](int k) {  // KL[w][b] (fp32, 32 cols) = R_k,g B_k,g[:, quarter block 2w + q]
-          const int q = k / n_groups, g = k % n_groups, o = ms.g_first[g];
-          const int b = (Uw + k) % kKlBufs;
-          const uint64_t ad = make_desc(rk + o * 4096, 16, 256, SWZ_32);
-          const uint64_t bd = make_desc(sbase + OFF_BK + o * 4096 + (2 * w + q) * 1024, 1024, 512, SWZ_64);
-          mma_ss(tm + T_KL + 128 * w + 32 * b, ad, bd, id_rb, 0);
-          mma_commit(smem_u32(&ms.klfull[w][b]));
-        };
-        auto ts = [&](int k) {  // S_w^T[:, rows of g] += RoPE(KL)[bf16, in place] Q_g^T over the unit's 32 d
-          const int q = k / n_groups, g = k % n_groups, o = ms.g_first[g], cnt = ms.g_cnt[g];
-          const int U = Uw + k, b = U % kKlBufs;
-          mbar_wait_sleep(smem_u32(&ms.klready[w][b]), (U / kKlBufs) & 1);
-          tc_fence_after();
-          const uint32_t id = idesc_bf16(128, 16 * cnt, false, false);
+        // group table of the item, packed 8 bits per group: first slot, slot count
+        const int meta = ms.rec[qb].meta, n_tiles = ms.rec[qb].n_tiles;
+        const int n_slots = meta & 15;
+        uint32_t gf = 0, gc = 0;
+        int ng = 0;
 #pragma unroll
-          for (int s2 = 0; s2 < 2; ++s2) {
-            const int d = 64 * s2 + 32 * w + 16 * q;
-            const uint64_t bd =
-                make_desc(sbase + OFF_Q + (d >> 6) * 8192 + 2048 * o + (d & 63) * 2, 16, 1024, SWZ_128);
-            // S1 has no base term: the first K-step of each group's first unit initialises it
-            mma_ts(sacc + 16 * o, tm + T_KL + 128 * w + 32 * b + 8 * s2, bd, id, (w == 0 || q > 0 || s2 > 0));
-          }
-        };
-        for (int k = 0; k < n_units && k < kKlBufs; ++k) rb(k);
-        if (w == 0) mbar_wait_sleep(smem_u32(&ms.kbfull), j & 1);
-        if (j > 0) mbar_wait_sleep(smem_u32(&ms.sfree), (j - 1) & 1);
-        tc_fence_after();
-        if (w == 0) {
-          ev(p, 4, j);
-#pragma unroll
-          for (int s = 0; s < 8; ++s) {
-            const uint64_t ad = make_desc(sbase + OFF_KB + (s >> 2) * 16384 + (s & 3) * 32, 16, 1024, SWZ_128);
-            const uint64_t bd = make_desc(sbase + OFF_Q + (s >> 2) * 8192 + (s & 3) * 32, 16, 1024, SWZ_128);
-            mma_ss(tm + T_S, ad, bd, id_s, s > 0);
-          }
-          mma_commit(smem_u32(&ms.kbempty));
-        }
-        if (deferred) {
-          for (int k = 0; k < n_units; ++k) {
-            ts(k);
-            if (k + kKlBufs < n_units) rb(k + kKlBufs);
-          }
-          Uw += n_units;
-        } else {
-          for (int g = 0; g < n_groups; ++g) {
-            const int o = ms.g_first[g], cnt = ms.g_cnt[g];
-            const uint64_t ad = make_desc(rk + o * 4096, 16, 256, SWZ_32);
-            const uint64_t bd = make_desc(sbase + OFF_BK + o * 512, 16, 256, SWZ_32);
-            mma_ss(tm + T_S + 16 * o, ad, bd, idesc_bf16(128, 16 * cnt, false, false), 1);
+        for (int o = 0; o < kSlots; ++o) {
+          if (o < n_slots) {
+            if ((meta >> (8 + o)) & 1) {
+              gf |= (uint32_t)o << (8 * ng);
+              gc |= 1u << (8 * ng);
+              ++ng;
+            } else {
+              gc += 1u << (8 * (ng - 1));
+            }
           }
         }
-        if (w == 0) ev(p, 5, j);
-        mma_commit(smem_u32(&ms.sfull[w]));
-        mma_commit(smem_u32(&ms.rkempty[st]));
+        const uint64_t dq = make_desc(qs, 16, 1024, SWZ_128);
+        for (int j = 0; j < n_tiles; ++j, ++T) {
+          const int sb = T & 1;
+          const uint32_t sacc = tm + T_S + 64 * sb;
+          const uint64_t dk = make_desc(sbase + C::OFF_K + (T % C::KS) * 32768, 16, 1024, SWZ_128);
+          const uint32_t rk = sbase + C::OFF_R + (T % C::RS) * 16384;
+          auto base_s = [&]() {  // S^T = K_base Q^T over both d-halves (descriptor + (byte offset >> 4))
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              mma_ss_e(sacc, dk + (uint64_t)(((c >> 2) * 16384 + (c & 3) * 32) >> 4),
+                       dq + (uint64_t)(((c >> 2) * 8192 + (c & 3) * 32) >> 4), id_s, c != 0);
+            mma_commit_e(smem_u32(&ms.kempty[T % C::KS]));
+          };
+          if constexpr (!kDef) {
+            if (T >= 2) mbar_wait(smem_u32(&ms.sfree[sb]), ((T >> 1) - 1) & 1);
+            ev(p, 8, T);
+            mbar_wait(smem_u32(&ms.kfull[T % C::KS]), (T / C::KS) & 1);
+            ev(p, 1, T);
+            tc_fence_after();
+            base_s();
+            mbar_wait(smem_u32(&ms.rfull[T % C::RS]), (T / C::RS) & 1);
+            tc_fence_after();
+            const uint64_t dr = make_desc(rk, 16, 256, SWZ_32), dx = make_desc(xs, 16, 256, SWZ_32);
+#pragma unroll
+            for (int g = 0; g < kSlots; ++g) {
+              if (g < ng) {
+                const uint32_t o = (gf >> (8 * g)) & 0xff, cnt = (gc >> (8 * g)) & 0xff;
+                mma_ss_e(sacc + 16 * o, dr + (uint64_t)(o * 256), dx + (uint64_t)(o * 32),
+                         idesc_bf16(128, 16 * cnt, false, false), 1);
+              }
+            }
+            mma_commit_e(smem_u32(&ms.rempty[T % C::RS]));
+          } else {
+            // R_k first: the K_lora rebuild units start before the base tile lands
+            mbar_wait(smem_u32(&ms.rfull[T % C::RS]), (T / C::RS) & 1);
+            tc_fence_after();
+            const int n_units = 2 * ng;  // unit k = q * ng + g (quarter-major)
+            const uint64_t dr = make_desc(rk, 16, 256, SWZ_32), dx = make_desc(xs, 1024, 512, SWZ_64);
+            auto rb = [&](int w, int k) {  // KL[w][b] (fp32, 32 cols) = R_k,g B_k,g[:, quarter block 2w + q]
+              const int q = k >= ng, g = k - q * ng;
+              const uint32_t o = (gf >> (8 * g)) & 0xff;
+              const uint32_t b = (U + k) % kKlBufs;
+              mma_ss_e(tm + T_KL + 128 * w + 32 * b, dr + (uint64_t)(o * 256),
+                       dx + (uint64_t)((o * 4096 + (2 * w + q) * 1024) >> 4), id_rb, 0);
+              mma_commit_e(smem_u32(&ms.klfull[w][b]));
+              if (T == 4) ev(p, 15, 32 * w + k);
+            };
+            auto ts = [&](int w, int k) {  // S^T[:, rows of g] += RoPE(KL)[bf16, in place] Q_g^T over the unit's 32 d
+              const int q = k >= ng, g = k - q * ng;
+              const uint32_t o = (gf >> (8 * g)) & 0xff, cnt = (gc >> (8 * g)) & 0xff;
+              const uint32_t Uk = U + k, b = Uk % kKlBufs;
+              if (T == 4) ev(p, 11, 32 * w + k);
+              mbar_wait(smem_u32(&ms.klready[w][b]), (Uk / kKlBufs) & 1);
+              if (T == 4) ev(p, 12, 32 * w + k);
+              tc_fence_after();
+              const uint32_t id = idesc_bf16(128, 16 * cnt, false, false);
+#pragma unroll
+              for (int s2 = 0; s2 < 2; ++s2) {
+                const uint32_t d = 64 * s2 + 32 * w + 16 * q;
+                mma_ts_e(sacc + 16 * o, tm + T_KL + 128 * w + 32 * b + 8 * s2,
+                         dq + (uint64_t)(((d >> 6) * 8192 + 2048 * o + (d & 63) * 2) >> 4), id, 1);
+              }
+            };
+            for (int k = 0; k < n_units && k < kKlBufs; ++k) { rb(0, k); rb(1, k); }
+            if (T >= 2) mbar_wait(smem_u32(&ms.sfree[sb]), ((T >> 1) - 1) & 1);
+            ev(p, 8, T);
+            mbar_wait(smem_u32(&ms.kfull[T % C::KS]), (T / C::KS) & 1);
+            ev(p, 1, T);
+            tc_fence_after();
+            base_s();
+            for (int k = 0; k < n_units; ++k) {
+              ts(0, k);
+              ts(1, k);
+              if (k + kKlBufs < n_units) { rb(0, k + kKlBufs); rb(1, k + kKlBufs); }
+            }
+            mma_commit_e(smem_u32(&ms.rempty[T % C::RS]));
+            U += n_units;
+          }
+          mma_commit_e(smem_u32(&ms.sfull[sb]));
+          ev(p, 2, T);
+        }
+        mma_commit_e(smem_u32(&ms.qempty[qb]));
       }
-    } else if (wid == 11 && lane == 0) {
-      // ================= PV-side MMA issuer =================
+    } else if (wid == 10) {
+      // ================= PV-side MMA issuer (whole warp, one elected lane issues) =================
       const uint32_t id_pv = idesc_bf16(128, kRows, true, true);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        mbar_wait_sleep(smem_u32(&ms.pfull), j & 1);
-        mbar_wait_sleep(smem_u32(&ms.vfull[st]), (j >> 1) & 1);
-        tc_fence_after();
-        ev(p, 6, j);
+      uint32_t nv = 0, T = 0;
+      for (int ii = 0; ii < n_my; ++ii) {
+        const int qb = ii % C::NQ;
+        mbar_wait(smem_u32(&ms.qfull[qb]), (ii / C::NQ) & 1);
+        const int n_tiles = ms.rec[qb].n_tiles;
+        for (int j = 0; j < n_tiles; ++j, ++T) {
+          const int pb = T % C::NP;
+          mbar_wait(smem_u32(&ms.pfull[pb]), (T / C::NP) & 1);
+          ev(p, 5, T);
+          const int ab = ii % C::AB;
+          if (j == 0 && ii >= C::AB) mbar_wait(smem_u32(&ms.accfree[ab]), ((ii / C::AB) - 1) & 1);
+          const uint64_t dp = make_desc(sbase + C::OFF_P + pb * 16384, 16384, 1024, SWZ_128);
+          for (int kh = 0; kh < 2; ++kh, ++nv) {
+            mbar_wait(smem_u32(&ms.vfull[nv % C::VS]), (nv / C::VS) & 1);
+            mbar_wait(smem_u32(&ms.rvfull[nv % C::VS]), (nv / C::VS) & 1);
+            ev(p, 6, nv);
+            tc_fence_after();
+            const uint32_t ve = sbase + C::OFF_V + (nv % C::VS) * C::VE;
+            const uint64_t dv = make_desc(ve, 8192, 1024, SWZ_128), da = make_desc(ve + 16384, 2048, 256, SWZ_32);
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const uint64_t bd = make_desc(sbase + OFF_P + s * 2048, 16384, 1024, SWZ_128);
-          const uint64_t ad = make_desc(sbase + OFF_V + st * 32768 + s * 2048, 16384, 1024, SWZ_128);
-          mma_ss(tm + T_O, ad, bd, id_pv, (j > 0 || s > 0));
+            for (int s = 0; s < 4; ++s) {
+              const uint64_t bd = dp + (uint64_t)(((4 * kh + s) * 2048) >> 4);
+              const uint32_t acc = (j > 0 || kh > 0 || s > 0);
+              mma_ss_e(tm + T_O + 128 * ab, dv + (uint64_t)((s * 2048) >> 4), bd, id_pv, acc);
+              mma_ss_e(tm + T_A + 128 * ab, da + (uint64_t)((s * 512) >> 4), bd, id_pv, acc);
+            }
+            mma_commit_e(smem_u32(&ms.vempty[nv % C::VS]));
+          }
+          mma_commit_e(smem_u32(&ms.pfree[pb]));
         }
-#pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const uint64_t bd = make_desc(sbase + OFF_P + s * 2048, 16384, 1024, SWZ_128);
-          const uint64_t ad = make_desc(sbase + OFF_RV + st * kRvStage + s * 512, 4096, 256, SWZ_32);
-          mma_ss(tm + T_A, ad, bd, id_pv, (j > 0 || s > 0));
-        }
-        mma_commit(smem_u32(&ms.pvdone));
-        mma_commit(smem_u32(&ms.vempty[st]));
       }
+    } else if (wid == 11) {
+      // ================= residual loader (cp.async, whole warp) =================
+      // R_k tiles (per group) and R_v halves (per slot) are many small contiguous pieces (4 KB per page and
+      // owner): 16-byte cp.async by 32 lanes keeps them off the TMA engine, whose per-operation cost would
+      // otherwise dominate. The page format is the SW32 operand layout already, so copies are verbatim.
+      const __nv_bfloat16* rkl = (const __nv_bfloat16*)p.res_k + (int64_t)p.layer * p.res_layer_stride;
+      const __nv_bfloat16* rvl = (const __nv_bfloat16*)p.res_v + (int64_t)p.layer * p.res_layer_stride;
+      const int Pm = P < 64 ? P : 64;
+      auto wait_free = [&](uint32_t bar, uint32_t parity) {
+        while (!mbar_test(bar, parity)) __nanosleep(20);
+      };
+      auto commit = [&](uint32_t full_bar) { cp_async_arrive(full_bar); };
+      if (P == kTile) {
+        // fast path: one page per tile; R_v halves only (R_k is streamed by the producer warp); page ids from
+        // the tile records (32 per lane batch, the next batch prefetched)
+        const int r0 = p.tile_ptr[cta], nrec = p.tile_ptr[cta + 1] - r0;
+        int4 ca = make_int4(0, 0, 0, 0), cbv = ca, na = ca, nb = ca;
+        auto load_batch = [&](int base) {
+          const int r = base + lane;
+          if (r < nrec) {
+            na = __ldg(&p.tile_recs[2 * (r0 + r)]);
+            nb = __ldg(&p.tile_recs[2 * (r0 + r) + 1]);
+          }
+        };
+        load_batch(0);
+        for (int T = 0; T < nrec; ++T) {
+          if ((T & 31) == 0) {
+            ca = na;
+            cbv = nb;
+            load_batch(T + 32);
+          }
+          const int L = T & 31;
+          const int ns = __shfl_sync(0xffffffffu, ca.z, L) & 15;
+          const int g0 = __shfl_sync(0xffffffffu, ca.w, L), g1 = __shfl_sync(0xffffffffu, cbv.x, L);
+          const int g2 = __shfl_sync(0xffffffffu, cbv.y, L), g3 = __shfl_sync(0xffffffffu, cbv.z, L);
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t nv = 2 * T + h, slot = nv % C::VS;
+            if (nv >= (uint32_t)C::VS) wait_free(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1);
+            const uint32_t dst = sbase + C::OFF_V + slot * C::VE + 16384;
+#pragma unroll
+            for (int o = 0; o < kSlots; ++o) {
+              if (o < ns) {
+                const int pg = o == 0 ? g0 : (o == 1 ? g1 : (o == 2 ? g2 : g3));
+                const __nv_bfloat16* src = rvl + ((int64_t)pg * kTile + 64 * h) * kR;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int c = lane + 32 * u;
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + o * 2048 + c * 16),
+                               "l"(src + c * 8)
+                               : "memory");
+                }
+              }
+            }
+            commit(smem_u32(&ms.rvfull[slot]));
+          }
+        }
+      } else {
+      uint32_t T = 0;
+      for (int ii = 0; ii < n_my; ++ii) {
+        ItemInfo I;
+        load_item(p, p.sched_items[it_begin + ii], I);
+        for (int j = 0; j < I.n_tiles; ++j, ++T) {
+          const int t0 = I.k0 + j * kTile;
+          {  // R_k of the item's groups: 4 KB per group at the group's first slot
+            const int slot = T % C::RS;
+            if (T >= (uint32_t)C::RS) wait_free(smem_u32(&ms.rempty[slot]), ((T / C::RS) - 1) & 1);
+            const uint32_t dst = sbase + C::OFF_R + slot * 16384;
+            for (int g = 0; g < I.n_groups; ++g) {
+              const int o = I.g_first[g];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {  // 256 chunks of 16 B = 128 keys x 32 B
+                const int c = lane + 32 * u, key = c >> 1;
+                const int t = t0 + key;
+                const int tt = t < I.k1 ? t : I.k0;
+                const int rp = p.res_pages[I.slot_res[o] + tt / P];
+                const __nv_bfloat16* src = rkl + ((int64_t)rp * P + tt % P) * kR + (c & 1) * 8;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + o * 4096 + c * 16), "l"(src)
+                             : "memory");
+              }
+            }
+            commit(smem_u32(&ms.rfull[slot]));
+          }
+          for (int h = 0; h < 2; ++h) {  // R_v halves into the V-side entries: 2 KB per slot
+            const uint32_t nv = 2 * T + h, slot = nv % C::VS;
+            if (nv >= (uint32_t)C::VS) wait_free(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1);
+            const uint32_t dst = sbase + C::OFF_V + slot * C::VE + 16384;
+            for (int o = 0; o < I.n_slots; ++o) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {  // 128 chunks = 64 keys x 32 B
+                const int c = lane + 32 * u, key = c >> 1;
+                const int t = t0 + 64 * h + key;
+                const int tt = t < I.k1 ? t : I.k0;
+                const int rp = p.res_pages[I.slot_res[o] + tt / P];
+                const __nv_bfloat16* src = rvl + ((int64_t)rp * P + tt % P) * kR + (c & 1) * 8;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + o * 2048 + c * 16), "l"(src)
+                             : "memory");
+              }
+            }
+            commit(smem_u32(&ms.rvfull[slot]));
+          }
+        }
+      }
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      (void)Pm;
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
     // ================= key warps =================
-    const int w = wid >> 2;                        // key warpgroup 0/1
-    const int kl = tid - 128 * w;                  // key within the tile == TMEM lane
+    const int w = wid >> 2;                         // key warpgroup 0/1
+    const int kl = tid - 128 * w;                   // key within the tile == TMEM lane
     const uint32_t lb = (uint32_t)(32 * (wid & 3)) << 16;
-    const int cb = 32 * w;                         // this group's query columns [cb, cb + 32)
-    const uint32_t bar_id = 1 + w;                 // named barrier of this warpgroup
-    const bool causal = ms.causal != 0;
+    const int cb = 32 * w;                          // this group's query columns [cb, cb + 32)
+    const uint32_t bar_id = 1 + w;                  // named barrier of this warpgroup
     const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
-    int U = 0;
-    // RoPE rows of this key for the next tile, frequencies [32w, 32w + 32), prefetched one tile ahead
-    float4 rc[8], rs[8];
-    auto load_rope = [&](int jj) {
-      const int tt = min(k0 + jj * kTile + kl, k1 - 1);
-      const float4* cp = (const float4*)(p.rope_cos + (int64_t)tt * (kD / 2) + 32 * w);
-      const float4* sp = (const float4*)(p.rope_sin + (int64_t)tt * (kD / 2) + 32 * w);
+    const float scl = p.scale_log2;
+    uint32_t T = 0, U = 0;
+    // RoPE angle addition: cos/sin(theta_i * kl) of this thread's key offset for frequencies [32w, 32w + 32),
+    // packed as fp16 pairs (cos, sin) (|error| <= 2^-12, below the bf16 rounding of K_lora itself)
+    uint32_t cst[32];
+    if constexpr (kDef) {
+      const int row = kl < p.max_pos ? kl : p.max_pos - 1;
+      const float4* cp = (const float4*)(p.rope_cos + (int64_t)row * (kD / 2) + 32 * w);
+      const float4* sp = (const float4*)(p.rope_sin + (int64_t)row * (kD / 2) + 32 * w);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) { rc[q] = __ldg(cp + q); rs[q] = __ldg(sp + q); }
+      for (int q = 0; q < 8; ++q) {
+        const float4 a = __ldg(cp + q), b = __ldg(sp + q);
+        cst[4 * q] = pack_h2(a.x, b.x); cst[4 * q + 1] = pack_h2(a.y, b.y);
+        cst[4 * q + 2] = pack_h2(a.z, b.z); cst[4 * q + 3] = pack_h2(a.w, b.w);
+      }
+    }
+    // partial entries [m, l, acc[128], acc_r[16]] of item ii, columns [cb, cb+32): l, acc, acc_r (m is written
+    // at the item's end), once PV of its last tile Tl completed; then the accumulators and the header are free
+    auto epilogue = [&](int ie, uint32_t Tl, int qbe) {
+      const ItemRec& Re = ms.rec[qbe];
+      const int ab = ie % C::AB, ns = Re.meta & 15;
+      mbar_wait(smem_u32(&ms.pfree[Tl % C::NP]), (Tl / C::NP) & 1);
+      tc_fence_after();
+      uint32_t o_[32], a_[32];
+      FKV_TMEM_LD32(tm + T_O + 128 * ab + cb + lb, o_);
+      FKV_TMEM_LD32(tm + T_A + 128 * ab + cb + lb, a_);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(smem_u32(&ms.accfree[ab]));
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int c = cb + i, o = c >> 4, r = c & 15;
+        if (o < ns && r < Re.n_rows[o]) {
+          float* ent = p.ws + (int64_t)(Re.entry_off[o] + r) * p.entry_stride;
+          ent[2 + kl] = __uint_as_float(o_[i]);                                  // acc[d = kl]
+          if ((kl >> 4) == o) ent[2 + kD + (kl & 15)] = __uint_as_float(a_[i]);  // acc_r[j] of this row's owner
+          if (kl == 64) ent[1] = __uint_as_float(a_[i]);                         // l (all-ones slot)
+        }
+      }
+      // this warpgroup is done with the item header
+      named_bar_sync(bar_id, 128);
+      if (kl == 0) mbar_arrive(smem_u32(&ms.qempty[qbe]));
     };
-    if (deferred) load_rope(0);
-    for (int j = 0; j < n_tiles; ++j) {
-      const int t = k0 + j * kTile + kl;
-      const bool tvalid = t < k1;
-      if (kl == 0) ev(p, 7 + 6 * w, j);
-      if (deferred) {
-        for (int q = 0; q < 2; ++q) {
-          // quarter q: frequencies 32w + 16q + [0, 16)
-          uint64_t C[8], S[8], NS[8];
+    int pend_ii = -1, pend_qb = 0;
+    uint32_t pend_Tl = 0;
+    for (int ii = 0; ii < n_my; ++ii) {
+      const int qb = ii % C::NQ;
+      mbar_wait(smem_u32(&ms.qfull[qb]), (ii / C::NQ) & 1);
+      const ItemRec& R = ms.rec[qb];
+      ItemLite I;
+      I.k0 = R.k0;
+      I.k1 = R.k1;
+      I.n_tiles = R.n_tiles;
+      I.n_slots = R.meta & 15;
+      I.n_groups = (R.meta >> 4) & 15;
+      const uint16_t* P1 = R.pos1 + cb;  // this group's columns: key t visible iff t - k0 < P1[c]
+      // per-item column state (this warpgroup's 32 columns); the previous item's epilogue is done with m_run
+      named_bar_sync(bar_id, 128);
+      if (kl < 32) ms.m_run[cb + kl] = -INFINITY;
+      named_bar_sync(bar_id, 128);
+      bool causal = false;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float4 a = rc[4 * q + e], bq = rs[4 * q + e];
-            C[2 * e] = f2(a.x, a.y); C[2 * e + 1] = f2(a.z, a.w);
-            S[2 * e] = f2(bq.x, bq.y); S[2 * e + 1] = f2(bq.z, bq.w);
-            NS[2 * e] = f2(-bq.x, -bq.y); NS[2 * e + 1] = f2(-bq.z, -bq.w);
+      for (int c = 0; c < 32; ++c) causal |= (int)P1[c] < I.k1 - I.k0;
+      for (int j = 0; j < I.n_tiles; ++j, ++T) {
+        const int t0 = I.k0 + j * kTile;
+        const int t = t0 + kl;
+        const bool tvalid = t < I.k1;
+        if constexpr (kDef) {
+          const int prow = t0 < p.max_pos ? t0 : p.max_pos - 1;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            // frequencies 32w + 16q + [0, 16): angle addition cos/sin((t0 + kl) theta)
+            uint64_t Cs[8], Ss[8], NS[8];
+            const float4* cp = (const float4*)(p.rope_cos + (int64_t)prow * (kD / 2) + 32 * w + 16 * q);
+            const float4* sp = (const float4*)(p.rope_sin + (int64_t)prow * (kD / 2) + 32 * w + 16 * q);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float4 c0 = __ldg(cp + e), s0 = __ldg(sp + e);
+              const float c0v[4] = {c0.x, c0.y, c0.z, c0.w}, s0v[4] = {s0.x, s0.y, s0.z, s0.w};
+              float cc[4], ss[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                float a, b;
+                unpack_h2(cst[16 * q + 4 * e + u], a, b);
+                cc[u] = fmaf(c0v[u], a, -s0v[u] * b);
+                ss[u] = fmaf(s0v[u], a, c0v[u] * b);
+              }
+              Cs[2 * e] = f2(cc[0], cc[1]); Cs[2 * e + 1] = f2(cc[2], cc[3]);
+              Ss[2 * e] = f2(ss[0], ss[1]); Ss[2 * e + 1] = f2(ss[2], ss[3]);
+              NS[2 * e] = f2(-ss[0], -ss[1]); NS[2 * e + 1] = f2(-ss[2], -ss[3]);
+            }
+            // two units per step: one TMEM load/store round trip and one barrier wait for both
+            for (int g = 0; g < I.n_groups; g += 2) {
+              const int nu = (g + 1 < I.n_groups) ? 2 : 1;
+              uint32_t x[2][16], y[2][16], lh[2][16];
+#pragma unroll
+              for (int u = 0; u < 2; ++u)
+                if (u < nu) mbar_wait(smem_u32(&ms.klfull[w][(U + u) % kKlBufs]), ((U + u) / kKlBufs) & 1);
+              if (T == 4 && kl == 0) ev(p, 13, 32 * w + q * I.n_groups + g);
+              tc_fence_after();
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                if (u < nu) {
+                  const uint32_t kt = tm + T_KL + 128 * w + 32 * ((U + u) % kKlBufs) + lb;
+                  FKV_TMEM_LD16(kt, x[u]);
+                  FKV_TMEM_LD16(kt + 16, y[u]);
+                }
+              }
+              tmem_ld_wait();
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const uint64_t X = f2(__uint_as_float(x[u][2 * e]), __uint_as_float(x[u][2 * e + 1]));
+                  const uint64_t Y = f2(__uint_as_float(y[u][2 * e]), __uint_as_float(y[u][2 * e + 1]));
+                  lh[u][e] = pack2(fma2(Y, NS[e], mul2(X, Cs[e])));      // x cos - y sin  (d)
+                  lh[u][8 + e] = pack2(fma2(X, Ss[e], mul2(Y, Cs[e])));  // x sin + y cos  (d + 64)
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                if (u < nu) {
+                  const uint32_t kt = tm + T_KL + 128 * w + 32 * ((U + u) % kKlBufs) + lb;
+                  FKV_TMEM_ST16(kt, lh[u]);
+                }
+              }
+              tmem_st_wait();
+              tc_fence_before();
+#pragma unroll
+              for (int u = 0; u < 2; ++u)
+                if (u < nu) mbar_arrive(smem_u32(&ms.klready[w][(U + u) % kKlBufs]));
+              if (T == 4 && kl == 0) ev(p, 14, 32 * w + q * I.n_groups + g);
+              U += nu;
+            }
           }
-          // two units per step: one TMEM load/store round trip and one barrier wait for both
-          for (int g = 0; g < n_groups; g += 2) {
-            const int nu = (g + 1 < n_groups) ? 2 : 1;
-            uint32_t x[2][16], y[2][16], lh[2][16];
+        }
+        // ---- online softmax over this group's 32 query columns (Alg1.339-341) ----
+        const int sb = T & 1;
+        mbar_wait(smem_u32(&ms.sfull[sb]), (T >> 1) & 1);
+        if (tid == 0) ev(p, 3, T);
+        tc_fence_after();
+        uint32_t sr[32];
+        FKV_TMEM_LD32(tm + T_S + 64 * sb + cb + lb, sr);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(smem_u32(&ms.sfree[sb]));
+        uint64_t x2[16];
+        float mx = -INFINITY;
+        {
+          const float4* mp = (const float4*)&ms.m_run[cb];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              if (u < nu) {
-                const int b = (U + u) % kKlBufs;
-                mbar_wait_sleep(smem_u32(&ms.klfull[w][b]), ((U + u) / kKlBufs) & 1);
-              }
+          for (int q = 0; q < 8; ++q) {
+            const float4 m4 = mp[q];
+            const uint64_t s01 = f2(__uint_as_float(sr[4 * q]), __uint_as_float(sr[4 * q + 1]));
+            const uint64_t s23 = f2(__uint_as_float(sr[4 * q + 2]), __uint_as_float(sr[4 * q + 3]));
+            x2[2 * q] = fma2(s01, sc2, f2(-m4.x, -m4.y));
+            x2[2 * q + 1] = fma2(s23, sc2, f2(-m4.z, -m4.w));
+          }
+          if (causal || !tvalid) {
+            const int tr = t - I.k0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint2 pv = *(const uint2*)(P1 + 4 * q);
+              float a, b2, c, d;
+              uf2(x2[2 * q], a, b2);
+              uf2(x2[2 * q + 1], c, d);
+              if (!tvalid || tr >= (int)(pv.x & 0xffffu)) a = -INFINITY;
+              if (!tvalid || tr >= (int)(pv.x >> 16)) b2 = -INFINITY;
+              if (!tvalid || tr >= (int)(pv.y & 0xffffu)) c = -INFINITY;
+              if (!tvalid || tr >= (int)(pv.y >> 16)) d = -INFINITY;
+              x2[2 * q] = f2(a, b2);
+              x2[2 * q + 1] = f2(c, d);
             }
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float a, b2;
+            uf2(x2[q], a, b2);
+            mx = max3(mx, a, b2);
+          }
+        }
+        // lazy rescaling: only when some score exceeds the running max by > 2^8
+        if (bar_or(bar_id, 128, mx > 8.0f)) {
+          float mo[32];
+          {
+            const float4* mp = (const float4*)&ms.m_run[cb];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 m4 = mp[q];
+              mo[4 * q] = m4.x; mo[4 * q + 1] = m4.y; mo[4 * q + 2] = m4.z; mo[4 * q + 3] = m4.w;
+            }
+          }
+          float v[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const bool ok = tvalid && (!causal || t - I.k0 < (int)P1[c]);
+            v[c] = ok ? __uint_as_float(sr[c]) * scl : -INFINITY;
+          }
+#pragma unroll
+          for (int step = 0; step < 5; ++step) {
+            const int off = 16 >> step, half = 16 >> step;
+            const bool up = lane & off;
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+              const float send = up ? v[i] : v[i + half];
+              const float keep = up ? v[i + half] : v[i];
+              v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, off));
+            }
+          }
+          // lane l holds the warp's max for column cb + l
+          named_bar_sync(bar_id, 128);
+          if (v[0] > -INFINITY) atomic_max_f(&ms.m_run[cb + lane], v[0]);
+          named_bar_sync(bar_id, 128);
+          float mn[32];
+          bool resc = false;
+          {
+            const float4* mp = (const float4*)&ms.m_run[cb];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 m4 = mp[q];
+              mn[4 * q] = m4.x; mn[4 * q + 1] = m4.y; mn[4 * q + 2] = m4.z; mn[4 * q + 3] = m4.w;
+            }
+          }
+          float al[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            al[c] = 1.f;
+            if (mn[c] != mo[c]) {
+              al[c] = mo[c] == -INFINITY ? 0.f : ex2(mo[c] - mn[c]);
+              resc |= mo[c] != -INFINITY;
+            }
+          }
+          if (resc && j > 0) {
+            // rescale this group's columns of O^T and A^T by alpha (all PV up to tile T-1 complete)
+            mbar_wait(smem_u32(&ms.pfree[(T - 1) % C::NP]), ((T - 1) / C::NP) & 1);
             tc_fence_after();
-            if (kl == 0 && g == 0 && q == 0) ev(p, 8 + 6 * w, j);
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              if (u < nu) {
-                const uint32_t kt = tm + T_KL + 128 * w + 32 * ((U + u) % kKlBufs) + lb;
-                FKV_TMEM_LD16(kt, x[u]);
-                FKV_TMEM_LD16(kt + 16, y[u]);
-              }
-            }
-            tmem_ld_wait();
+            for (int part = 0; part < 2; ++part) {
+              const uint32_t base = tm + (part ? T_A : T_O) + 128 * (ii % C::AB) + cb + lb;
+              uint32_t r[32];
+              FKV_TMEM_LD32(base, r);
+              tmem_ld_wait();
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const uint64_t X = f2(__uint_as_float(x[u][2 * e]), __uint_as_float(x[u][2 * e + 1]));
-                const uint64_t Y = f2(__uint_as_float(y[u][2 * e]), __uint_as_float(y[u][2 * e + 1]));
-                lh[u][e] = pack2(fma2(Y, NS[e], mul2(X, C[e])));       // x cos - y sin  (d)
-                lh[u][8 + e] = pack2(fma2(X, S[e], mul2(Y, C[e])));    // x sin + y cos  (d + 64)
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              if (u < nu) {
-                const uint32_t kt = tm + T_KL + 128 * w + 32 * ((U + u) % kKlBufs) + lb;
-                FKV_TMEM_ST16(kt, lh[u]);
-              }
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * al[i]);
+              FKV_TMEM_ST16(base, r);
+              FKV_TMEM_ST16(base + 16, (r + 16));
             }
             tmem_st_wait();
             tc_fence_before();
+          }
+          // recompute with the updated running max (a column with no visible key keeps -inf -> p = 0)
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
-              if (u < nu) mbar_arrive(smem_u32(&ms.klready[w][(U + u) % kKlBufs]));
-            U += nu;
+          for (int q = 0; q < 16; ++q) {
+            const float m0 = mn[2 * q], m1 = mn[2 * q + 1];
+            const bool ok0 = tvalid && (!causal || t - I.k0 < (int)P1[2 * q]);
+            const bool ok1 = tvalid && (!causal || t - I.k0 < (int)P1[2 * q + 1]);
+            const float x0 = ok0 ? __uint_as_float(sr[2 * q]) * scl - (m0 == -INFINITY ? 0.f : m0) : -INFINITY;
+            const float x1 = ok1 ? __uint_as_float(sr[2 * q + 1]) * scl - (m1 == -INFINITY ? 0.f : m1) : -INFINITY;
+            x2[q] = f2(x0, x1);
           }
         }
-        if (j + 1 < n_tiles) load_rope(j + 1);
-      }
-      // ---- online softmax over this group's 32 query columns (Alg1.339-341) ----
-      if (kl == 0) ev(p, 9 + 6 * w, j);
-      mbar_wait_sleep(smem_u32(&ms.sfull[0]), j & 1);
-      if (deferred) mbar_wait_sleep(smem_u32(&ms.sfull[1]), j & 1);
-      tc_fence_after();
-      if (kl == 0) ev(p, 10 + 6 * w, j);
-      uint32_t sr[32];
-      FKV_TMEM_LD32(tm + T_S + cb + lb, sr);
-      if (deferred) {
-        uint32_t s1[32];
-        FKV_TMEM_LD32(tm + T_S1 + cb + lb, s1);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 32; ++c) sr[c] = __float_as_uint(__uint_as_float(sr[c]) + __uint_as_float(s1[c]));
-      }
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(smem_u32(&ms.sfree));
-      uint64_t x2[16];
-      float mx = -INFINITY;
-      {
-        const float4* mp = (const float4*)&ms.m_run[cb];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 m4 = mp[q];
-          const uint64_t s01 = f2(__uint_as_float(sr[4 * q]), __uint_as_float(sr[4 * q + 1]));
-          const uint64_t s23 = f2(__uint_as_float(sr[4 * q + 2]), __uint_as_float(sr[4 * q + 3]));
-          x2[2 * q] = fma2(s01, sc2, f2(-m4.x, -m4.y));
-          x2[2 * q + 1] = fma2(s23, sc2, f2(-m4.z, -m4.w));
-        }
-        if (causal || !tvalid) {
-          const int4* pp = (const int4*)&ms.pos[cb];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int4 p4 = pp[q];
-            float a, b2, c, d;
-            uf2(x2[2 * q], a, b2);
-            uf2(x2[2 * q + 1], c, d);
-            if (!tvalid || t > p4.x) a = -INFINITY;
-            if (!tvalid || t > p4.y) b2 = -INFINITY;
-            if (!tvalid || t > p4.z) c = -INFINITY;
-            if (!tvalid || t > p4.w) d = -INFINITY;
-            x2[2 * q] = f2(a, b2);
-            x2[2 * q + 1] = f2(c, d);
-          }
-        }
+        // P^T row of this key (bf16, MN-major SW128), columns [cb, cb + 32)
+        uint32_t pk[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           float a, b2;
           uf2(x2[q], a, b2);
-          mx = max3(mx, a, b2);
+          pk[q] = pack_bf16x2(ex2(a), ex2(b2));
+        }
+        const int pb = T % C::NP;
+        if (T >= (uint32_t)C::NP) mbar_wait(smem_u32(&ms.pfree[pb]), ((T / C::NP) - 1) & 1);
+        uint8_t* pbuf = smem + C::OFF_P + pb * 16384;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch)
+          *(uint4*)(pbuf + mnmajor_off(cb + ch * 8, kl, 8, 16384, 1024)) =
+              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+        fence_async_smem();
+        mbar_arrive(smem_u32(&ms.pfull[pb]));
+        if (tid == 0) ev(p, 4, T);
+        if (C::AB > 1 && j == 0 && pend_ii >= 0) {
+          epilogue(pend_ii, pend_Tl, pend_qb);
+          pend_ii = -1;
         }
       }
-      // lazy rescaling: only when some score exceeds the running max by > 2^8
-      if (bar_or(bar_id, 128, mx > 8.0f)) {
-        if (kl == 0) ev(p, 19, j + 128 * w);
-        float v[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const bool ok = tvalid && (!causal || t <= ms.pos[cb + c]);
-          v[c] = ok ? __uint_as_float(sr[c]) * p.scale_log2 : -INFINITY;
-        }
-#pragma unroll
-        for (int step = 0; step < 5; ++step) {
-          const int off = 16 >> step, half = 16 >> step;
-          const bool up = lane & off;
-#pragma unroll
-          for (int i = 0; i < half; ++i) {
-            const float send = up ? v[i] : v[i + half];
-            const float keep = up ? v[i + half] : v[i];
-            v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, off));
-          }
-        }
-        if (kl == 0) ev(p, 23 + w, j);
-        ms.red[w][wid & 3][lane] = v[0];  // lane l holds column cb + l
-        named_bar_sync(bar_id, 128);
-        if (kl == 0) ev(p, 29 + w, j);
-        bool resc = false;
-        if (kl < 32) {
-          const int c = cb + kl;
-          const float cm = fmaxf(fmaxf(ms.red[w][0][kl], ms.red[w][1][kl]), fmaxf(ms.red[w][2][kl], ms.red[w][3][kl]));
-          const float mo = ms.m_run[c];
-          const float mn = fmaxf(mo, cm);
-          float al = 1.f;
-          if (mn != mo) {
-            al = mo == -INFINITY ? 0.f : ex2(mo - mn);
-            resc = mo != -INFINITY;
-          }
-          ms.alpha[c] = al;
-          ms.m_run[c] = mn;
-        }
-        if (kl == 0) ev(p, 27 + w, j);
-        if (bar_or(bar_id, 128, resc) && j > 0) {
-          // rescale this group's columns of O^T and A^T by alpha
-          mbar_wait_sleep(smem_u32(&ms.pvdone), (j - 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int part = 0; part < 2; ++part) {
-            const uint32_t base = tm + (part ? T_A : T_O) + cb + lb;
-            uint32_t r[32];
-            FKV_TMEM_LD32(base, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * ms.alpha[cb + i]);
-            FKV_TMEM_ST16(base, r);
-            FKV_TMEM_ST16(base + 16, (r + 16));
-          }
-          tmem_st_wait();
-          tc_fence_before();
-        }
-        if (kl == 0) ev(p, 25 + w, j);
-        // recompute with the updated running max (a column with no visible key keeps -inf -> p = 0)
-        const float* mr = &ms.m_run[cb];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float m0 = mr[2 * q], m1 = mr[2 * q + 1];
-          const bool ok0 = tvalid && (!causal || t <= ms.pos[cb + 2 * q]);
-          const bool ok1 = tvalid && (!causal || t <= ms.pos[cb + 2 * q + 1]);
-          const float x0 = ok0 ? __uint_as_float(sr[2 * q]) * p.scale_log2 - (m0 == -INFINITY ? 0.f : m0) : -INFINITY;
-          const float x1 = ok1 ? __uint_as_float(sr[2 * q + 1]) * p.scale_log2 - (m1 == -INFINITY ? 0.f : m1)
-                               : -INFINITY;
-          x2[q] = f2(x0, x1);
+      // ---- item end: the running max is final -> m of every partial entry now; the accumulators once the
+      // last PV completes (NONE: deferred past the next item's first tile, the PV pipe runs on meanwhile) ----
+      if (kl == 64) {
+#pragma unroll 1
+        for (int i = 0; i < 32; ++i) {
+          const int c = cb + i, o = c >> 4, r = c & 15;
+          if (o < I.n_slots && r < R.n_rows[o]) p.ws[(int64_t)(R.entry_off[o] + r) * p.entry_stride] = ms.m_run[c];
         }
       }
-      // P^T row of this key (bf16, MN-major SW128), columns [cb, cb + 32)
-      uint32_t pk[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        float a, b2;
-        uf2(x2[q], a, b2);
-        pk[q] = pack_bf16x2(ex2(a), ex2(b2));
-      }
-      if (kl == 0) ev(p, 11 + 6 * w, j);
-      if (j > 0) mbar_wait_sleep(smem_u32(&ms.pvdone), (j - 1) & 1);
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch)
-        *(uint4*)(smem + OFF_P + mnmajor_off(cb + ch * 8, kl, 8, 16384, 1024)) =
-            make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-      fence_async_smem();
-      mbar_arrive(smem_u32(&ms.pfull));
-      if (kl == 0) ev(p, 12 + 6 * w, j);
-    }
-    // ---- epilogue: partial entries [m, l, acc[128], acc_r[16]] for columns [cb, cb+32) ----
-    mbar_wait_sleep(smem_u32(&ms.pvdone), (n_tiles - 1) & 1);
-    tc_fence_after();
-    uint32_t o_[32], a_[32];
-    FKV_TMEM_LD32(tm + T_O + cb + lb, o_);
-    FKV_TMEM_LD32(tm + T_A + cb + lb, a_);
-    tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int c = cb + i, o = c >> 4, r = c & 15;
-      if (o < n_slots) {
-        const DevWarp wd = p.warps[it.warp_off + o];
-        if (r < wd.n_rows) {
-          float* ent = p.ws + (int64_t)(wd.entry_off + r) * p.entry_stride;
-          ent[2 + kl] = __uint_as_float(o_[i]);                    // acc[d = kl]
-          if ((kl >> 4) == o) ent[2 + kD + (kl & 15)] = __uint_as_float(a_[i]);  // acc_r[j] of this row's owner
-          if (kl == 64) {
-            ent[0] = ms.m_run[c];
-            ent[1] = __uint_as_float(a_[i]);                      // l (all-ones slot)
-          }
-        }
+      if (C::AB == 1) {
+        epilogue(ii, T - 1, qb);
+      } else {
+        pend_ii = ii;
+        pend_Tl = T - 1;
+        pend_qb = qb;
       }
     }
+    if (pend_ii >= 0) epilogue(pend_ii, pend_Tl, pend_qb);
   }
   tc_fence_before();
   __syncthreads();
-  if (tid == 0) ev(p, 22, 0);
-  if (wid == 10) tmem_dealloc(tm, 512);
+  if (wid == 11) tmem_dealloc(tm, 512);
+  if (tid == 0 && p.dbg && cta < 256) {  // diagnostics: per-CTA duration (cycles) and tile count
+    p.dbg[30 * 256 + cta] = clock64() - t_start;
+    p.dbg[31 * 256 + cta] = p.tile_ptr[cta + 1] - p.tile_ptr[cta];
+  }
 }
 
 }  // namespace
 
 cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStream_t s) {
   if (p.n_items == 0) return cudaSuccess;
-  if (p.d != kD || p.r != kR || p.dtype != FKV_DTYPE_BF16 || (kTile % p.P) || p.P < 8) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ra_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  if (p.d != kD || p.r != kR || p.dtype != FKV_DTYPE_BF16 || (kTile % p.P) || p.P < 8 || p.n_ctas < 1 || !p.stage)
+    return cudaErrorInvalidValue;
+  const bool def = p.rope_mode == FKV_ROPE_DEFERRED;
+  static bool attr[2] = {false, false};
+  if (!attr[def]) {
+    cudaError_t e = def ? cudaFuncSetAttribute(ra_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               Cfg<true>::SMEM)
+                        : cudaFuncSetAttribute(ra_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               Cfg<false>::SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[def] = true;
   }
-  ra_tc_kernel<<<p.n_items, 384, kSmemBytes, s>>>(*(const TcMaps*)maps, p);
+  if (def)
+    ra_tc_kernel<true><<<p.n_ctas, 384, Cfg<true>::SMEM, s>>>(*(const TcMaps*)maps, p);
+  else
+    ra_tc_kernel<false><<<p.n_ctas, 384, Cfg<false>::SMEM, s>>>(*(const TcMaps*)maps, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage(const AttnParams& p, int32_t n_warps, cudaStream_t s) {
+  if (n_warps <= 0) return cudaSuccess;
+  ra_stage_kernel<<<n_warps, 128, 0, s>>>(p, n_warps);
   return cudaGetLastError();
 }
 

@@ -13,9 +13,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-EV = {0: "prod:RK", 1: "prod:KB", 2: "prod:V", 3: "S:rkfull", 4: "S:base", 5: "S:done", 6: "PV:go",
-      7: "W0:tile", 8: "W0:kl0", 9: "W0:rope_end", 10: "W0:sfull", 11: "W0:Pready", 12: "W0:pfull",
-      13: "W1:tile", 14: "W1:kl0", 15: "W1:rope_end", 16: "W1:sfull", 17: "W1:Pready", 18: "W1:pfull"}
+EV = {0: "P:kslab", 1: "S:kfull", 8: "S:sfree", 2: "S:commit", 3: "W:sfull", 4: "W:pfull", 5: "PV:pfull",
+      7: "P:vent", 6: "PV:vfull", 9: "P:Qitem", 10: "S:Qfull"}
 
 
 def main():
@@ -27,6 +26,7 @@ def main():
     ap.add_argument("--page", type=int, default=64)
     a = ap.parse_args()
     import torch
+    import numpy as np
 
     from paper_2604_06370_b200 import _lib as L
     from paper_2604_06370_b200.api import ForkKV
@@ -58,16 +58,33 @@ def main():
     torch.cuda.synchronize()
     lib.fkv_debug_timeline(fkv.ctx, None, 0)
     d = dbg.view(32, 256).cpu().numpy()
-    t0 = d[20, 0]
-    print(f"block {a.block}: setup {d[21, 0] - t0} cyc, total {d[22, 0] - t0} cyc")
-    names = [EV[e] for e in sorted(EV)]
-    print("tile " + " ".join(f"{n:>11s}" for n in names))
-    for w in range(2):
-        print(f"slow path W{w} tile0: enter {d[19, 128 * w] - t0} butterfly_done {d[23 + w, 0] - t0} "
-              f"bar_done {d[29 + w, 0] - t0} resc_bar {d[27 + w, 0] - t0} recompute {d[25 + w, 0] - t0}")
+    t0 = d[d > 0].min()
+    print("per tile T (S/W/PV events) and per ring entry (K slab 3/tile, V entry 2/tile), cycles from first event")
+    cols = [8, 2, 3, 4, 5]
+    print("   T " + " ".join(f"{EV[e]:>9s}" for e in cols) + " |  n " + " ".join(f"{EV[e]:>9s}" for e in (0, 1, 7, 6)))
     for j in range(a.tiles):
-        row = [d[e, j] - t0 if d[e, j] else -1 for e in sorted(EV)]
-        print(f"{j:4d} " + " ".join(f"{x:11d}" for x in row))
+        row = [d[e, j] - t0 if d[e, j] else -1 for e in cols]
+        row2 = [d[e, j] - t0 if d[e, j] else -1 for e in (0, 1, 7, 6)]
+        print(f"{j:4d} " + " ".join(f"{x:9d}" for x in row) + f" | {j:3d} " + " ".join(f"{x:9d}" for x in row2))
+    print("items: P:Qitem / S:Qfull", [(d[9, i] - t0, d[10, i] - t0) for i in range(16) if d[9, i]])
+    if d[11].any():
+        b0 = min(x for x in d[11] if x > 0)
+        print("DEFERRED unit pipeline, tile 4 (cycles from first S-side ts wait): w, k: S rb-commit, S wait->ok | key pair wait-ok, pair done")
+        for w in range(2):
+            for k in range(8):
+                i = 32 * w + k
+                f = lambda e: (d[e, i] - b0) if d[e, i] else -1
+                print(f"  w{w} k{k}: rb {f(15):7d}  ts-wait {f(11):7d} ok {f(12):7d} | keys ok {f(13):7d} done {f(14):7d}")
+    dur, nt = d[30, :148], d[31, :148]
+    if dur.any():
+        o = np.argsort(dur)
+        print(f"CTA cycles: min {dur.min()} median {int(np.median(dur))} max {dur.max()}; "
+              f"sum/148 {dur.sum() / 148:.0f}; tiles min {nt.min()} max {nt.max()}")
+        print("slowest CTAs (cta, cycles, tiles):", [(int(i), int(dur[i]), int(nt[i])) for i in o[-6:]])
+        print("fastest CTAs:", [(int(i), int(dur[i]), int(nt[i])) for i in o[:4]])
+    last = max(j for j in range(256) if d[2, j]) if d[2].any() else 0
+    print(f"tiles {last + 1}; last S:commit {d[2, last] - t0}, last W:pfull {d[4, last] - t0}, "
+          f"cycles/tile overall {(d[4, last] - t0) / (last + 1):.0f}")
 
 
 if __name__ == "__main__":
