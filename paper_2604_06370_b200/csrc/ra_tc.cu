@@ -248,6 +248,9 @@ __device__ __forceinline__ void mma_commit_e(uint32_t mbar) {
       : "memory");
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
 // arrive on `bar` when all of this thread's prior cp.async copies have landed (no count increment)
 __device__ __forceinline__ void cp_async_arrive(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       mbar_init(smem_u32(&ms.rvfull[i]), 32);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&ms.qfull[i]), 1);
+      mbar_init(smem_u32(&ms.qfull[i]), p.P == kTile ? 32 : 1);  // fast path: one cp.async arrive per lane
       mbar_init(smem_u32(&ms.qempty[i]), 3);  // S-side commit + one arrive per key warpgroup
       mbar_init(smem_u32(&ms.sfull[i]), 1);
       mbar_init(smem_u32(&ms.sfree[i]), 256);
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (wid == 8 && P == kTile) {
       // ================= producer, fast path (P = 128: one page per tile), whole warp =================
-      // TMA (lane 0): K_base tiles, V_base halves, per-item Q / X images; cp.async (all lanes): R_k tiles.
+      // TMA (lane 0): K_base tiles; cp.async (all lanes): R_k tiles and the per-item header / Q / X images.
       // Page ids come from the tile records, each stream's next record preloaded (no page-table chasing).
       tma_prefetch_desc(&maps.kb); tma_prefetch_desc(&maps.vb);
       const __nv_bfloat16* rkl = (const __nv_bfloat16*)p.res_k + (int64_t)p.layer * p.res_layer_stride;
@@ -406,13 +409,15 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       auto base_row = [&](const int4& a, const int4& b) {  // 2D-view row of the tile's base page
         return (int)(((brow_l + b.w) * p.hkv + (a.z >> 16)) * kTile);
       };
-      int4 kA = make_int4(0, 0, 0, 0), kB = kA, vA = kA, vB = kA, rA = kA, rB = kA, fA = kA, fB = kA;
+      int4 kA = make_int4(0, 0, 0, 0), kB = kA, rA = kA, rB = kA, fA = kA, fB = kA;
       ldrec(0, kA, kB);
-      vA = kA; vB = kB; rA = kA; rB = kB;
+      rA = kA; rB = kB;
       constexpr int kPf = 2;  // L2 prefetch distance (tiles) of K_base and R_k
       ldrec(kPf, fA, fB);
-      uint32_t nk = 0, nv = 0, nr = 0;
+      uint32_t nk = 0, nr = 0;
       int iq = 0;
+      int qitem = n_my > 0 ? p.sched_items[it_begin] : 0;
+      DevItem qit = p.items[qitem];
       for (;;) {
         bool busy = false, progress = false;
         if (nk < (uint32_t)nrec) {  // K_base tile (32 KB, one 3D box)
@@ -424,7 +429,6 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               const uint32_t bar = smem_u32(&ms.kfull[slot]);
               mbar_expect_tx(bar, 32768);
               tma_load_3d(sbase + C::OFF_K + slot * 32768, &maps.kb, 0, base_row(kA, kB), 0, bar);
-              if (nk + kPf < (uint32_t)nrec) tma_prefetch_l2_3d(&maps.kb, 0, base_row(fA, fB), 0);
             }
             if (nk + kPf < (uint32_t)nrec) {  // R_k pages of tile nk + kPf -> L2 (one 128-byte line per lane)
               const int pgs[4] = {fA.w, fB.x, fB.y, fB.z};
@@ -464,39 +468,29 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             progress = true;
           }
         }
-        if (nv < 2u * nrec) {  // V_base 64-key half (16 KB, one 3D box)
-          busy = true;
-          const int slot = nv % C::VS;
-          if (nv < (uint32_t)C::VS || mbar_test(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1)) {
-            if (lane == 0) {
-              ev(p, 7, nv);
-              const uint32_t bar = smem_u32(&ms.vfull[slot]);
-              mbar_expect_tx(bar, 16384);
-              tma_load_3d(sbase + C::OFF_V + slot * C::VE, &maps.vb, 0, base_row(vA, vB) + 64 * (nv & 1), 0, bar);
-            }
-            ++nv;
-            if ((nv & 1) == 0) ldrec(nv >> 1, vA, vB);
-            progress = true;
-          }
-        }
-        if (iq < n_my) {  // per-item Q rows and q~ / packed B_k (staged images)
+        if (iq < n_my) {  // per-item header, Q rows and q~ / packed B_k (staged images): cp.async by all lanes
           busy = true;
           const int qb = iq % C::NQ;
           if (iq < C::NQ || mbar_test(smem_u32(&ms.qempty[qb]), ((iq / C::NQ) - 1) & 1)) {
-            if (lane == 0) {
-              const DevItem it = p.items[p.sched_items[it_begin + iq]];
-              ev(p, 9, iq);
-              const uint32_t bar = smem_u32(&ms.qfull[qb]);
-              mbar_expect_tx(bar, it.n_warps * (4096 + C::XB) + (uint32_t)sizeof(ItemRec));
-              bulk_g2s(smem_u32(&ms.rec[qb]), p.item_recs + p.sched_items[it_begin + iq], sizeof(ItemRec), bar);
-              for (int o = 0; o < it.n_warps; ++o) {
-                const uint8_t* src = p.stage + (int64_t)(it.warp_off + o) * kStageBytes;
-                bulk_g2s(sbase + C::OFF_Q + qb * 16384 + o * 2048, src, 2048, bar);
-                bulk_g2s(sbase + C::OFF_Q + qb * 16384 + 8192 + o * 2048, src + 2048, 2048, bar);
-                bulk_g2s(sbase + C::OFF_X + qb * kSlots * C::XB + o * C::XB, src + 4096, C::XB, bar);
+            ev(p, 9, iq);
+            const uint8_t* rsrc = (const uint8_t*)(p.item_recs + qitem);
+            if (lane < (int)(sizeof(ItemRec) / 16)) cp_async16(smem_u32(&ms.rec[qb]) + lane * 16, rsrc + lane * 16);
+            for (int o = 0; o < qit.n_warps; ++o) {
+              const uint8_t* src = p.stage + (int64_t)(qit.warp_off + o) * kStageBytes;
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {  // Q image: 2 x 2 KB
+                const int c = lane + 32 * u;
+                cp_async16(sbase + C::OFF_Q + qb * 16384 + (c >> 7) * 8192 + o * 2048 + (c & 127) * 16, src + c * 16);
               }
+              for (int c = lane; c < (int)(C::XB / 16); c += 32)
+                cp_async16(sbase + C::OFF_X + qb * kSlots * C::XB + o * C::XB + c * 16, src + 4096 + c * 16);
             }
+            cp_async_arrive(smem_u32(&ms.qfull[qb]));
             ++iq;
+            if (iq < n_my) {
+              qitem = p.sched_items[it_begin + iq];
+              qit = p.items[qitem];
+            }
             progress = true;
           }
         }
@@ -757,10 +751,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             mma_commit_e(smem_u32(&ms.vempty[nv % C::VS]));
           }
           mma_commit_e(smem_u32(&ms.pfree[pb]));
+          ev(p, 18, T);
         }
       }
     } else if (wid == 11) {
-      // ================= residual loader (cp.async, whole warp) =================
+      // ================= V-side loader (whole warp): V_base halves (TMA, lane 0) + R_v (cp.async) =================
       // R_k tiles (per group) and R_v halves (per slot) are many small contiguous pieces (4 KB per page and
       // owner): 16-byte cp.async by 32 lanes keeps them off the TMA engine, whose per-operation cost would
       // otherwise dominate. The page format is the SW32 operand layout already, so copies are verbatim.
@@ -792,11 +787,19 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
           const int L = T & 31;
           const int ns = __shfl_sync(0xffffffffu, ca.z, L) & 15;
+          const int vh = __shfl_sync(0xffffffffu, ca.z, L) >> 16, bpg = __shfl_sync(0xffffffffu, cbv.w, L);
+          const int vrow = (int)((((int64_t)p.layer * p.nb + bpg) * p.hkv + vh) * kTile);
           const int g0 = __shfl_sync(0xffffffffu, ca.w, L), g1 = __shfl_sync(0xffffffffu, cbv.x, L);
           const int g2 = __shfl_sync(0xffffffffu, cbv.y, L), g3 = __shfl_sync(0xffffffffu, cbv.z, L);
           for (int h = 0; h < 2; ++h) {
             const uint32_t nv = 2 * T + h, slot = nv % C::VS;
             if (nv >= (uint32_t)C::VS) wait_free(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1);
+            if (lane == 0) {  // V_base 64-key half (16 KB, one 3D box)
+              ev(p, 7, nv);
+              const uint32_t bar = smem_u32(&ms.vfull[slot]);
+              mbar_expect_tx(bar, 16384);
+              tma_load_3d(sbase + C::OFF_V + slot * C::VE, &maps.vb, 0, vrow + 64 * h, 0, bar);
+            }
             const uint32_t dst = sbase + C::OFF_V + slot * C::VE + 16384;
 #pragma unroll
             for (int o = 0; o < kSlots; ++o) {
@@ -1144,7 +1147,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           pk[q] = pack_bf16x2(ex2(a), ex2(b2));
         }
         const int pb = T % C::NP;
+        if (tid == 0) ev(p, 16, T);
         if (T >= (uint32_t)C::NP) mbar_wait(smem_u32(&ms.pfree[pb]), ((T / C::NP) - 1) & 1);
+        if (tid == 0) ev(p, 17, T);
         uint8_t* pbuf = smem + C::OFF_P + pb * 16384;
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch)

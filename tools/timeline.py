@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--layers", type=int, default=1)
     ap.add_argument("--tiles", type=int, default=12)
     ap.add_argument("--page", type=int, default=64)
+    ap.add_argument("--detail", type=int, default=-1)
     a = ap.parse_args()
     import torch
     import numpy as np
@@ -67,6 +68,16 @@ def main():
         row2 = [d[e, j] - t0 if d[e, j] else -1 for e in (0, 1, 7, 6)]
         print(f"{j:4d} " + " ".join(f"{x:9d}" for x in row) + f" | {j:3d} " + " ".join(f"{x:9d}" for x in row2))
     print("items: P:Qitem / S:Qfull", [(d[9, i] - t0, d[10, i] - t0) for i in range(16) if d[9, i]])
+    if a.detail >= 0:
+        T = a.detail
+        base = d[0, T]
+        f = lambda e, i: int(d[e, i] - base) if d[e, i] else -1
+        print(f"tile {T} (cycles from its K issue): K issue 0, S kfull {f(1, T)}, S sfree {f(8, T)}, S commit {f(2, T)}, "
+              f"W sfull {f(3, T)}, W pfree-wait {f(16, T)} ok {f(17, T)}, W pfull {f(4, T)}, PV pfull {f(5, T)}, "
+              f"PV commit {f(18, T)}")
+        for h in range(2):
+            n = 2 * T + h
+            print(f"   V entry {n}: TMA issue {f(7, n)}, R_v issue {f(19, n)}, PV both full {f(6, n)}")
     if d[11].any():
         b0 = min(x for x in d[11] if x > 0)
         print("DEFERRED unit pipeline, tile 4 (cycles from first S-side ts wait): w, k: S rb-commit, S wait->ok | key pair wait-ok, pair done")

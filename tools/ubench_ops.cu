@@ -11,10 +11,11 @@ struct Maps { CUtensorMap m; };
 // kind 0: 2D box; 1: 3D box; 2: 1D bulk of `bytes`; 3: cp.async 16B by 32 lanes (bytes per op)
 __global__ void run(const __grid_constant__ Maps mp, const uint8_t* base, int64_t rows, int kind, int bytes, int box_rows,
                     int ops_per_stage, int stages, int iters) {
+  const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[8];
   const int stage_bytes = ops_per_stage * bytes;
-  if (threadIdx.x == 0) { for (int i = 0; i < stages; ++i) mbar_init(smem_u32(&full[i]), kind == 3 ? 32 : 1); fence_mbar_init(); }
+  if (threadIdx.x == 0) { for (int i = 0; i < stages; ++i) mbar_init(smem_u32(&full[i]), kind == 3 ? blockDim.x : 1); fence_mbar_init(); }
   __syncthreads();
   if (kind != 3 && threadIdx.x != 0) return;
   for (int i = 0; i < iters + stages; ++i) {
@@ -30,7 +31,7 @@ __global__ void run(const __grid_constant__ Maps mp, const uint8_t* base, int64_
       else if (kind == 1) tma_load_3d(dst, &mp.m, 0, (int)r, 0, bar);
       else if (kind == 2) asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst), "l"(base + r * 256), "r"(bytes), "r"(bar) : "memory");
       else {
-        for (int c = threadIdx.x; c < bytes / 16; c += 32)
+        for (int c = wid * 32 + lane; c < bytes / 16; c += 32 * nw)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + c * 16), "l"(base + r * 256 + c * 16) : "memory");
       }
     }
@@ -44,14 +45,18 @@ int main() {
   void* buf; cudaMalloc(&buf, big); cudaMemset(buf, 0, big);
   cudaFuncSetAttribute(run, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const uint64_t rows = big / 256;
+  const uint64_t rows_big = big / 256;
   struct C { const char* name; int kind, bytes, box_rows, box_cols; } cs[] = {
       {"3D {64,128,2} 32KB", 1, 32768, 128, 64}, {"3D {64,64,2} 16KB", 1, 16384, 64, 64},
       {"2D {64,128} 16KB", 0, 16384, 128, 64}, {"2D {64,64} 8KB", 0, 8192, 64, 64},
       {"2D {16,128} 4KB (32B rows)", 0, 4096, 128, 16}, {"2D {64,32} 4KB", 0, 4096, 32, 64},
       {"1D bulk 32KB", 2, 32768, 128, 0}, {"1D bulk 16KB", 2, 16384, 64, 0}, {"1D bulk 4KB", 2, 4096, 16, 0},
       {"cp.async 4KB", 3, 4096, 16, 0}, {"cp.async 32KB", 3, 32768, 128, 0}};
+  for (int foot = 0; foot < 2; ++foot)
+  for (int nwarps : {1, 2, 4})
   for (auto c : cs) {
+    if (c.kind != 3 && nwarps > 1) continue;
+    const uint64_t rows = foot ? rows_big : (32ull << 20) / 256;  // 32 MB: L2-resident
     Maps mp;
     if (c.kind == 1) mp.m = fkv::make_tmap_3d_bf16_halves(buf, rows, c.box_rows);
     else if (c.kind == 0) mp.m = fkv::make_tmap_2d_bf16(buf, rows, 128, 256, c.box_cols, c.box_rows, c.box_cols == 64 ? 128 : 32);
@@ -62,13 +67,13 @@ int main() {
       float best = 1e30f;
       for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(e0);
-        run<<<nsm, 32, stages * ops * c.bytes>>>(mp, (const uint8_t*)buf, rows - 256, c.kind, c.bytes, c.box_rows, ops, stages, iters);
+        run<<<nsm, 32 * nwarps, stages * ops * c.bytes>>>(mp, (const uint8_t*)buf, rows - 256, c.kind, c.bytes, c.box_rows, ops, stages, iters);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         if (rep && ms < best) best = ms;
       }
       const double bytes = (double)nsm * iters * ops * c.bytes;
-      printf("%-28s ring %3d KB (%2d ops/stage): %6.0f GB/s  %6.1f ns/op/SM  %s\n", c.name, stages * ops * c.bytes / 1024, ops,
+      printf("%s w%d %-28s ring %3d KB (%2d ops/stage): %6.0f GB/s  %6.1f ns/op/SM  %s\n", foot ? "HBM" : "L2 ", nwarps, c.name, stages * ops * c.bytes / 1024, ops,
              bytes / best / 1e6, best * 1e6 / (iters * ops), cudaGetErrorString(cudaGetLastError()));
     }
   }
