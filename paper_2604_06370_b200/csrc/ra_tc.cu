@@ -49,8 +49,9 @@ using namespace sm100;
 
 constexpr int kD = 128, kR = 16, kTile = 128, kRows = 64, kSlots = 4;
 constexpr int kKlBufs = 4;
-// TMEM columns: S^T x2 | O^T | A^T | KL [wg][4 bufs] x 32 (DEFERRED)
-constexpr uint32_t T_S = 0, T_O = 128, T_A = 192, T_KL = 256;
+// TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
+// NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
+constexpr uint32_t T_KL = 256;
 
 template <bool kDef>
 struct Cfg {
@@ -61,7 +62,15 @@ struct Cfg {
   static constexpr int VS = 3;                   // V-side ring (26 KB: 64-key half of V_base | R_v 4 slots | ones)
   static constexpr int NP = 2;                   // P^T buffers (16 KB)
   static constexpr int NQ = kDef ? 1 : 2;        // per-item Q / X buffers
-  static constexpr int AB = kDef ? 1 : 2;        // O^T / A^T accumulator sets in TMEM (NONE: the KL columns are free)
+  // Accumulator layout switches (both measured on B200): split accumulation chains (SH / PAR = 2) do not help, a
+  // tcgen05.mma costs ~120 cycles for N <= 128 whether or not it depends on the previous one
+  // (tools/ubench_mma.cu); double-buffered O^T / A^T (AB = 2) overlap an item's epilogue with the next item.
+  static constexpr int AB = kDef ? 1 : 2;        // O^T / A^T accumulator sets in TMEM
+  static constexpr int SH = 1;                   // S^T accumulation chains (d-halves)
+  static constexpr int PAR = 1;                  // O^T / A^T accumulation chains (key-chunk parity)
+  __host__ __device__ static constexpr uint32_t tS(int sb, int h) { return SH == 1 ? 64 * sb : 128 * sb + 64 * h; }
+  __host__ __device__ static constexpr uint32_t tO(int ab, int par) { return 128 + 128 * ab + 64 * par * 0; }
+  __host__ __device__ static constexpr uint32_t tA(int ab, int par) { return 192 + 128 * ab + 64 * par * 0; }
   static constexpr uint32_t XB = kDef ? 4096 : 512;  // per-slot X image: packed B_k | q~
   static constexpr uint32_t VE = 26624;
   static constexpr uint32_t OFF_V = 0;
@@ -188,6 +197,11 @@ __device__ __forceinline__ void uf2(uint64_t v, float& a, float& b) {
 __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
   uint64_t r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
 __device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
@@ -495,7 +509,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
         }
         if (!busy) break;
-        if (!progress) __nanosleep(20);
+        if (!progress) __nanosleep(200);  // polling warps have issue priority: yield the SMSP to the key warps
       }
       asm volatile("cp.async.wait_all;\n" ::: "memory");
     } else if (wid == 8 && lane == 0) {
@@ -605,7 +619,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
         }
         if (!busy) break;
-        if (!progress) __nanosleep(20);
+        if (!progress) __nanosleep(200);  // polling warps have issue priority: yield the SMSP to the key warps
       }
     } else if (wid == 9) {
       // ================= S-side MMA issuer (whole warp: uniform operands, one elected lane issues) =================
@@ -639,14 +653,18 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         const uint64_t dq = make_desc(qs, 16, 1024, SWZ_128);
         for (int j = 0; j < n_tiles; ++j, ++T) {
           const int sb = T & 1;
-          const uint32_t sacc = tm + T_S + 64 * sb;
+          const uint32_t sacc = tm + C::tS(sb, 0);
           const uint64_t dk = make_desc(sbase + C::OFF_K + (T % C::KS) * 32768, 16, 1024, SWZ_128);
           const uint32_t rk = sbase + C::OFF_R + (T % C::RS) * 16384;
           auto base_s = [&]() {  // S^T = K_base Q^T over both d-halves (descriptor + (byte offset >> 4))
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-              mma_ss_e(sacc, dk + (uint64_t)(((c >> 2) * 16384 + (c & 3) * 32) >> 4),
-                       dq + (uint64_t)(((c >> 2) * 8192 + (c & 3) * 32) >> 4), id_s, c != 0);
+            for (int i = 0; i < 8; ++i) {
+              // NONE: d-half chains interleaved (0,4,1,5,...) into separate accumulators
+              const int c = C::SH == 2 ? ((i & 1) * 4 + (i >> 1)) : i;
+              const int h = C::SH == 2 ? (c >> 2) : 0;
+              mma_ss_e(tm + C::tS(sb, h), dk + (uint64_t)(((c >> 2) * 16384 + (c & 3) * 32) >> 4),
+                       dq + (uint64_t)(((c >> 2) * 8192 + (c & 3) * 32) >> 4), id_s, C::SH == 2 ? (c & 3) != 0 : c != 0);
+            }
             mma_commit_e(smem_u32(&ms.kempty[T % C::KS]));
           };
           if constexpr (!kDef) {
@@ -663,7 +681,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             for (int g = 0; g < kSlots; ++g) {
               if (g < ng) {
                 const uint32_t o = (gf >> (8 * g)) & 0xff, cnt = (gc >> (8 * g)) & 0xff;
-                mma_ss_e(sacc + 16 * o, dr + (uint64_t)(o * 256), dx + (uint64_t)(o * 32),
+                mma_ss_e(tm + C::tS(sb, C::SH - 1) + 16 * o, dr + (uint64_t)(o * 256), dx + (uint64_t)(o * 32),
                          idesc_bf16(128, 16 * cnt, false, false), 1);
               }
             }
@@ -743,10 +761,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             const uint64_t dv = make_desc(ve, 8192, 1024, SWZ_128), da = make_desc(ve + 16384, 2048, 256, SWZ_32);
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
-              const uint64_t bd = dp + (uint64_t)(((4 * kh + s) * 2048) >> 4);
-              const uint32_t acc = (j > 0 || kh > 0 || s > 0);
-              mma_ss_e(tm + T_O + 128 * ab, dv + (uint64_t)((s * 2048) >> 4), bd, id_pv, acc);
-              mma_ss_e(tm + T_A + 128 * ab, da + (uint64_t)((s * 512) >> 4), bd, id_pv, acc);
+              const int ck = 4 * kh + s, par = ck % C::PAR;  // NONE: two chains per accumulator (key-chunk parity)
+              const uint64_t bd = dp + (uint64_t)((ck * 2048) >> 4);
+              const uint32_t acc = (j > 0 || ck >= C::PAR);
+              mma_ss_e(tm + C::tO(ab, par), dv + (uint64_t)((s * 2048) >> 4), bd, id_pv, acc);
+              mma_ss_e(tm + C::tA(ab, par), da + (uint64_t)((s * 512) >> 4), bd, id_pv, acc);
             }
             mma_commit_e(smem_u32(&ms.vempty[nv % C::VS]));
           }
@@ -763,7 +782,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       const __nv_bfloat16* rvl = (const __nv_bfloat16*)p.res_v + (int64_t)p.layer * p.res_layer_stride;
       const int Pm = P < 64 ? P : 64;
       auto wait_free = [&](uint32_t bar, uint32_t parity) {
-        while (!mbar_test(bar, parity)) __nanosleep(20);
+        mbar_wait(bar, parity);
       };
       auto commit = [&](uint32_t full_bar) { cp_async_arrive(full_bar); };
       if (P == kTile) {
@@ -901,8 +920,19 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       mbar_wait(smem_u32(&ms.pfree[Tl % C::NP]), (Tl / C::NP) & 1);
       tc_fence_after();
       uint32_t o_[32], a_[32];
-      FKV_TMEM_LD32(tm + T_O + 128 * ab + cb + lb, o_);
-      FKV_TMEM_LD32(tm + T_A + 128 * ab + cb + lb, a_);
+      FKV_TMEM_LD32(tm + C::tO(ab, 0) + cb + lb, o_);
+      FKV_TMEM_LD32(tm + C::tA(ab, 0) + cb + lb, a_);
+      if constexpr (C::PAR == 2) {  // sum the key-chunk parity chains
+        uint32_t o1[32];
+        FKV_TMEM_LD32(tm + C::tO(ab, 1) + cb + lb, o1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o_[i] = __float_as_uint(__uint_as_float(o_[i]) + __uint_as_float(o1[i]));
+        FKV_TMEM_LD32(tm + C::tA(ab, 1) + cb + lb, o1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) a_[i] = __float_as_uint(__uint_as_float(a_[i]) + __uint_as_float(o1[i]));
+      }
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(smem_u32(&ms.accfree[ab]));
@@ -944,6 +974,22 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         const int t0 = I.k0 + j * kTile;
         const int t = t0 + kl;
         const bool tvalid = t < I.k1;
+        // visibility of this key for the warpgroup's 32 columns (bit c): in range and, for causal rows, t <= pos
+        uint32_t vm = tvalid ? 0xffffffffu : 0u;
+        if (causal && tvalid) {
+          const int tr = t - I.k0;
+          vm = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 pv = *(const uint4*)(P1 + 8 * q);
+            const uint32_t w4[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              vm |= (uint32_t)(tr < (int)(w4[e] & 0xffffu)) << (8 * q + 2 * e);
+              vm |= (uint32_t)(tr < (int)(w4[e] >> 16)) << (8 * q + 2 * e + 1);
+            }
+          }
+        }
         if constexpr (kDef) {
           const int prow = t0 < p.max_pos ? t0 : p.max_pos - 1;
 #pragma unroll
@@ -1019,7 +1065,21 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         if (tid == 0) ev(p, 3, T);
         tc_fence_after();
         uint32_t sr[32];
-        FKV_TMEM_LD32(tm + T_S + 64 * sb + cb + lb, sr);
+        FKV_TMEM_LD32(tm + C::tS(sb, 0) + cb + lb, sr);
+        if constexpr (C::SH == 2) {  // add the second d-half chain
+          uint32_t s1[32];
+          FKV_TMEM_LD32(tm + C::tS(sb, 1) + cb + lb, s1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const uint64_t a = fadd2(f2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])),
+                                     f2(__uint_as_float(s1[c]), __uint_as_float(s1[c + 1])));
+            float x, y;
+            uf2(a, x, y);
+            sr[c] = __float_as_uint(x);
+            sr[c + 1] = __float_as_uint(y);
+          }
+        }
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(smem_u32(&ms.sfree[sb]));
@@ -1035,20 +1095,14 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             x2[2 * q] = fma2(s01, sc2, f2(-m4.x, -m4.y));
             x2[2 * q + 1] = fma2(s23, sc2, f2(-m4.z, -m4.w));
           }
-          if (causal || !tvalid) {
-            const int tr = t - I.k0;
+          if (vm != 0xffffffffu) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const uint2 pv = *(const uint2*)(P1 + 4 * q);
-              float a, b2, c, d;
-              uf2(x2[2 * q], a, b2);
-              uf2(x2[2 * q + 1], c, d);
-              if (!tvalid || tr >= (int)(pv.x & 0xffffu)) a = -INFINITY;
-              if (!tvalid || tr >= (int)(pv.x >> 16)) b2 = -INFINITY;
-              if (!tvalid || tr >= (int)(pv.y & 0xffffu)) c = -INFINITY;
-              if (!tvalid || tr >= (int)(pv.y >> 16)) d = -INFINITY;
-              x2[2 * q] = f2(a, b2);
-              x2[2 * q + 1] = f2(c, d);
+            for (int q = 0; q < 16; ++q) {
+              float a, b2;
+              uf2(x2[q], a, b2);
+              a = (vm >> (2 * q)) & 1u ? a : -INFINITY;
+              b2 = (vm >> (2 * q + 1)) & 1u ? b2 : -INFINITY;
+              x2[q] = f2(a, b2);
             }
           }
 #pragma unroll
@@ -1059,7 +1113,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
         }
         // lazy rescaling: only when some score exceeds the running max by > 2^8
+        if (tid == 0) ev(p, 20, T);
         if (bar_or(bar_id, 128, mx > 8.0f)) {
+          if (tid == 0) ev(p, 21, T);
           float mo[32];
           {
             const float4* mp = (const float4*)&ms.m_run[cb];
@@ -1072,7 +1128,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           float v[32];
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
-            const bool ok = tvalid && (!causal || t - I.k0 < (int)P1[c]);
+            const bool ok = (vm >> c) & 1u;
             v[c] = ok ? __uint_as_float(sr[c]) * scl : -INFINITY;
           }
 #pragma unroll
@@ -1088,8 +1144,10 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
           // lane l holds the warp's max for column cb + l
           named_bar_sync(bar_id, 128);
+          if (tid == 0) ev(p, 22, T);
           if (v[0] > -INFINITY) atomic_max_f(&ms.m_run[cb + lane], v[0]);
           named_bar_sync(bar_id, 128);
+          if (tid == 0) ev(p, 23, T);
           float mn[32];
           bool resc = false;
           {
@@ -1102,20 +1160,18 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
           float al[32];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            al[c] = 1.f;
-            if (mn[c] != mo[c]) {
-              al[c] = mo[c] == -INFINITY ? 0.f : ex2(mo[c] - mn[c]);
-              resc |= mo[c] != -INFINITY;
-            }
+          for (int c = 0; c < 32; ++c) {  // branch-free: ex2(0) = 1 for unchanged columns
+            const bool fresh = mo[c] == -INFINITY;
+            al[c] = fresh ? 0.f : ex2(mo[c] - mn[c]);
+            resc |= !fresh && (mn[c] != mo[c]);
           }
           if (resc && j > 0) {
             // rescale this group's columns of O^T and A^T by alpha (all PV up to tile T-1 complete)
             mbar_wait(smem_u32(&ms.pfree[(T - 1) % C::NP]), ((T - 1) / C::NP) & 1);
             tc_fence_after();
 #pragma unroll
-            for (int part = 0; part < 2; ++part) {
-              const uint32_t base = tm + (part ? T_A : T_O) + 128 * (ii % C::AB) + cb + lb;
+            for (int part = 0; part < 2 * C::PAR; ++part) {
+              const uint32_t base = tm + ((part & 1) ? C::tA(ii % C::AB, part >> 1) : C::tO(ii % C::AB, part >> 1)) + cb + lb;
               uint32_t r[32];
               FKV_TMEM_LD32(base, r);
               tmem_ld_wait();
@@ -1127,12 +1183,13 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             tmem_st_wait();
             tc_fence_before();
           }
+          if (tid == 0) ev(p, 24, T);
           // recompute with the updated running max (a column with no visible key keeps -inf -> p = 0)
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const float m0 = mn[2 * q], m1 = mn[2 * q + 1];
-            const bool ok0 = tvalid && (!causal || t - I.k0 < (int)P1[2 * q]);
-            const bool ok1 = tvalid && (!causal || t - I.k0 < (int)P1[2 * q + 1]);
+            const bool ok0 = (vm >> (2 * q)) & 1u;
+            const bool ok1 = (vm >> (2 * q + 1)) & 1u;
             const float x0 = ok0 ? __uint_as_float(sr[2 * q]) * scl - (m0 == -INFINITY ? 0.f : m0) : -INFINITY;
             const float x1 = ok1 ? __uint_as_float(sr[2 * q + 1]) * scl - (m1 == -INFINITY ? 0.f : m1) : -INFINITY;
             x2[q] = f2(x0, x1);

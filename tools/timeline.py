@@ -75,6 +75,8 @@ def main():
         print(f"tile {T} (cycles from its K issue): K issue 0, S kfull {f(1, T)}, S sfree {f(8, T)}, S commit {f(2, T)}, "
               f"W sfull {f(3, T)}, W pfree-wait {f(16, T)} ok {f(17, T)}, W pfull {f(4, T)}, PV pfull {f(5, T)}, "
               f"PV commit {f(18, T)}")
+        print(f"   key warps: sfull {f(3, T)}, before bar_or {f(20, T)}, slow {f(21, T)}, pre-atomic {f(22, T)}, "
+              f"post-atomic {f(23, T)}, pre-recompute {f(24, T)}, pfree-wait {f(16, T)}")
         for h in range(2):
             n = 2 * T + h
             print(f"   V entry {n}: TMA issue {f(7, n)}, R_v issue {f(19, n)}, PV both full {f(6, n)}")
