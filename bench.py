@@ -434,7 +434,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--mode", default="deferred", choices=["deferred", "none"])
+    ap.add_argument("--mode", default="none", choices=["deferred", "none"],
+                    help="none = the north-star split q(K_base + R_K B_K)^T = qK_base^T + (qB_K^T)R_K^T (default); "
+                         "deferred = the paper's RoPE on the rebuilt residual (Alg.1), DESIGN.md C-1")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

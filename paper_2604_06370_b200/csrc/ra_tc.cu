@@ -1015,47 +1015,30 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               NS[2 * e] = f2(-ss[0], -ss[1]); NS[2 * e + 1] = f2(-ss[2], -ss[3]);
             }
             // two units per step: one TMEM load/store round trip and one barrier wait for both
-            for (int g = 0; g < I.n_groups; g += 2) {
-              const int nu = (g + 1 < I.n_groups) ? 2 : 1;
-              uint32_t x[2][16], y[2][16], lh[2][16];
-#pragma unroll
-              for (int u = 0; u < 2; ++u)
-                if (u < nu) mbar_wait(smem_u32(&ms.klfull[w][(U + u) % kKlBufs]), ((U + u) / kKlBufs) & 1);
+            // one unit at a time (keeps the key warps within their register budget: no spills)
+            for (int g = 0; g < I.n_groups; ++g) {
+              uint32_t x[16], y[16], lh[16];
+              const uint32_t b = U % kKlBufs;
+              mbar_wait(smem_u32(&ms.klfull[w][b]), (U / kKlBufs) & 1);
               if (T == 4 && kl == 0) ev(p, 13, 32 * w + q * I.n_groups + g);
               tc_fence_after();
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                if (u < nu) {
-                  const uint32_t kt = tm + T_KL + 128 * w + 32 * ((U + u) % kKlBufs) + lb;
-                  FKV_TMEM_LD16(kt, x[u]);
-                  FKV_TMEM_LD16(kt + 16, y[u]);
-                }
-              }
+              const uint32_t kt = tm + T_KL + 128 * w + 32 * b + lb;
+              FKV_TMEM_LD16(kt, x);
+              FKV_TMEM_LD16(kt + 16, y);
               tmem_ld_wait();
 #pragma unroll
-              for (int u = 0; u < 2; ++u) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const uint64_t X = f2(__uint_as_float(x[u][2 * e]), __uint_as_float(x[u][2 * e + 1]));
-                  const uint64_t Y = f2(__uint_as_float(y[u][2 * e]), __uint_as_float(y[u][2 * e + 1]));
-                  lh[u][e] = pack2(fma2(Y, NS[e], mul2(X, Cs[e])));      // x cos - y sin  (d)
-                  lh[u][8 + e] = pack2(fma2(X, Ss[e], mul2(Y, Cs[e])));  // x sin + y cos  (d + 64)
-                }
+              for (int e = 0; e < 8; ++e) {
+                const uint64_t X = f2(__uint_as_float(x[2 * e]), __uint_as_float(x[2 * e + 1]));
+                const uint64_t Y = f2(__uint_as_float(y[2 * e]), __uint_as_float(y[2 * e + 1]));
+                lh[e] = pack2(fma2(Y, NS[e], mul2(X, Cs[e])));      // x cos - y sin  (d)
+                lh[8 + e] = pack2(fma2(X, Ss[e], mul2(Y, Cs[e])));  // x sin + y cos  (d + 64)
               }
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                if (u < nu) {
-                  const uint32_t kt = tm + T_KL + 128 * w + 32 * ((U + u) % kKlBufs) + lb;
-                  FKV_TMEM_ST16(kt, lh[u]);
-                }
-              }
+              FKV_TMEM_ST16(kt, lh);
               tmem_st_wait();
               tc_fence_before();
-#pragma unroll
-              for (int u = 0; u < 2; ++u)
-                if (u < nu) mbar_arrive(smem_u32(&ms.klready[w][(U + u) % kKlBufs]));
+              mbar_arrive(smem_u32(&ms.klready[w][b]));
               if (T == 4 && kl == 0) ev(p, 14, 32 * w + q * I.n_groups + g);
-              U += nu;
+              ++U;
             }
           }
         }
