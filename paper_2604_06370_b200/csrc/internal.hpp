@@ -163,7 +163,8 @@ struct Plan {
   uint64_t generation = 0;
   int32_t n_seqs = 0;
   int64_t n_rows_q = 0;  // total query rows (sum q_len)
-  int32_t kernel = 0;    // 0 mma grouped, 1 simt
+  int32_t kernel = 0;    // 0 mma grouped, 1 simt, 2 tcgen05
+  int32_t tc_rows = 64;  // tcgen05: query rows per CTA
   std::vector<DevSeq> seqs;
   std::vector<int32_t> base_pages, res_pages;
   std::vector<DevItem> items;

@@ -36,14 +36,17 @@ cudaError_t launch_kv_write(const PoolView& pv, int32_t layer, const WriteRun* r
                             cudaStream_t s);
 cudaError_t launch_cow_copy(const PoolView& pv, const CopyOp* ops, int32_t n_ops, cudaStream_t s);
 
-// Per-item header of the persistent tcgen05 kernel, staged into shared memory with the item's Q rows (176 B).
-struct ItemRec {
+// Per-item header of the persistent tcgen05 kernel, staged into shared memory with the item's Q rows.
+// S = slots (16 query rows each): 4 (64-row CTAs, 176 B) or 8 (128-row CTAs, 336 B).
+template <int S>
+struct ItemRecT {
   int32_t k0, k1, n_tiles, meta;  // meta = n_slots | n_groups << 4 | group-first slot mask << 8 | kv head << 16
-  int32_t n_rows[4];              // query rows of each slot
-  int32_t entry_off[4];           // first partial entry of each slot
-  uint16_t pos1[64];              // per query column: position - k0 + 1 (key t visible iff t - k0 < pos1), 0 = none
+  int32_t n_rows[S];              // query rows of each slot
+  int32_t entry_off[S];           // first partial entry of each slot
+  uint16_t pos1[16 * S];          // per query column: position - k0 + 1 (key t visible iff t - k0 < pos1), 0 = none
 };
-static_assert(sizeof(ItemRec) == 176, "ItemRec");
+static_assert(sizeof(ItemRecT<4>) == 176 && sizeof(ItemRecT<8>) == 336, "ItemRec");
+constexpr int kTileRecInts = 16;  // tile record: t0, k1, meta, base page, residual page of slots 0..7, pad
 
 struct AttnParams {
   const void* base_k;
@@ -79,11 +82,12 @@ struct AttnParams {
   const int32_t* sched_items;
   int32_t n_ctas;
   // per-CTA tile records, CTA c owns records [tile_ptr[c], tile_ptr[c+1]) in its processing order:
-  // {t0, k1, meta = n_slots | n_groups << 4 | group-first slot mask << 8, res page of slots 0..3, base page}
-  // (pages only meaningful when P == 128: one page per tile)
+  // {t0, k1, meta (as ItemRecT::meta), base page, residual page of slots 0..7, pad} (kTileRecInts ints; pages are
+  // only meaningful when P == 128: one page per tile)
   const int32_t* tile_ptr;
   const int4* tile_recs;
-  const ItemRec* item_recs;  // per plan item
+  const void* item_recs;  // per plan item: ItemRecT<tc_rows / 16>
+  int32_t tc_rows;        // query rows per CTA of the tcgen05 kernel (64 | 128)
   int32_t max_pos;
   int32_t tc_prefetch;  // L2 prefetch distance in tiles (tcgen05 producer; 0 = off)
   uint8_t* stage;  // per-warp-slot staged operand images (ws region, kStageBytes each)

@@ -54,7 +54,17 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
                      P >= 8 && !(flags & (FKV_PLAN_FORCE_SIMT | FKV_PLAN_FORCE_MMA));
   const bool mma_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && !(flags & FKV_PLAN_FORCE_SIMT);
   pl.kernel = tc_ok ? 2 : (mma_ok ? 0 : 1);
-  const int kWarpsPerCta = pl.kernel == 2 ? 4 : 8;
+  // tcgen05: 64 query rows per CTA. NONE also has a 128-row variant (FKV_TC_ROWS=128): every MMA instruction then
+  // covers N = 128 rows (a tcgen05.mma costs ~120 cycles for any N <= 128, tools/ubench_mma.cu), but its key warps
+  // (64 columns each, SIMT row sums, single P^T buffer) are the bottleneck today, so it is not the default;
+  // DEFERRED is 64-row only (its K_lora buffers need the TMEM)
+  if (pl.kernel == 2) {
+    const char* renv = getenv("FKV_TC_ROWS");
+    pl.tc_rows = renv ? atoi(renv) : 64;
+    if (pl.tc_rows != 64 && pl.tc_rows != 128) pl.tc_rows = 64;
+    if (c.cfg.rope_mode != FKV_ROPE_NONE) pl.tc_rows = 64;
+  }
+  const int kWarpsPerCta = pl.kernel == 2 ? pl.tc_rows / kRowsPerWarp : 8;
   const int kTileKeys = pl.kernel == 2 ? 128 : 64;
   pl.generation = c.generation;
   pl.n_seqs = n;
@@ -192,7 +202,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   if (pl.kernel == 2) {
     const char* penv = getenv("FKV_PIECE_TILES");
     split_tiles = penv ? std::max<int64_t>(1, atoll(penv)) : std::max<int64_t>(4, total_tiles / (2 * sms));
-    split_tiles = std::min<int64_t>(split_tiles, 511);  // ItemRec::pos1 is 16-bit relative to the item start
+    split_tiles = std::min<int64_t>(split_tiles, 511);  // ItemRecT::pos1 is 16-bit relative to the item start
   } else {
     const char* wenv = getenv("FKV_SPLIT_WAVES");
     const double waves = wenv ? atof(wenv) : 2.0;
@@ -267,30 +277,36 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
       pl.sched_items.insert(pl.sched_items.end(), v.begin(), v.end());
       pl.sched_ptr.push_back((int32_t)pl.sched_items.size());
     }
-    // item records (k::ItemRec)
-    pl.item_recs.assign(pl.items.size() * sizeof(k::ItemRec), 0);
-    for (size_t i = 0; i < pl.items.size(); ++i) {
-      const DevItem& it = pl.items[i];
-      k::ItemRec r{};
-      r.k0 = it.key_begin;
-      r.k1 = it.key_end;
-      r.n_tiles = (it.key_end - it.key_begin + kTileKeys - 1) / kTileKeys;
-      int32_t ng = 0, gmask = 0;
-      for (int o = 0; o < it.n_warps; ++o) {
-        const DevWarp& w = pl.warps[it.warp_off + o];
-        const bool first = o == 0 || w.res_off != pl.warps[it.warp_off + o - 1].res_off ||
-                           w.adapter_slot != pl.warps[it.warp_off + o - 1].adapter_slot;
-        if (first) { ++ng; gmask |= 1 << o; }
-        r.n_rows[o] = w.n_rows;
-        r.entry_off[o] = w.entry_off;
-        for (int j = 0; j < w.n_rows; ++j) {
-          const int64_t v = (int64_t)pl.rows[w.row_off + j].pos - it.key_begin + 1;
-          r.pos1[16 * o + j] = (uint16_t)std::min<int64_t>(65535, std::max<int64_t>(0, v));
+    // item records (k::ItemRecT<slots>)
+    auto build_recs = [&](auto tag) {
+      using Rec = decltype(tag);
+      constexpr int S = (int)(sizeof(Rec::n_rows) / sizeof(int32_t));
+      pl.item_recs.assign(pl.items.size() * sizeof(Rec), 0);
+      for (size_t i = 0; i < pl.items.size(); ++i) {
+        const DevItem& it = pl.items[i];
+        if (it.n_warps > S) throw Error(FKV_E_INVALID, "plan: item has too many slots");
+        Rec r{};
+        r.k0 = it.key_begin;
+        r.k1 = it.key_end;
+        r.n_tiles = (it.key_end - it.key_begin + kTileKeys - 1) / kTileKeys;
+        int32_t ng = 0, gmask = 0;
+        for (int o = 0; o < it.n_warps; ++o) {
+          const DevWarp& w = pl.warps[it.warp_off + o];
+          const bool first = o == 0 || w.res_off != pl.warps[it.warp_off + o - 1].res_off ||
+                             w.adapter_slot != pl.warps[it.warp_off + o - 1].adapter_slot;
+          if (first) { ++ng; gmask |= 1 << o; }
+          r.n_rows[o] = w.n_rows;
+          r.entry_off[o] = w.entry_off;
+          for (int j = 0; j < w.n_rows; ++j) {
+            const int64_t v = (int64_t)pl.rows[w.row_off + j].pos - it.key_begin + 1;
+            r.pos1[16 * o + j] = (uint16_t)std::min<int64_t>(65535, std::max<int64_t>(0, v));
+          }
         }
+        r.meta = it.n_warps | (ng << 4) | (gmask << 8) | (it.kv_head << 16);
+        std::memcpy(pl.item_recs.data() + i * sizeof(Rec), &r, sizeof(r));
       }
-      r.meta = it.n_warps | (ng << 4) | (gmask << 8) | (it.kv_head << 16);
-      std::memcpy(pl.item_recs.data() + i * sizeof(k::ItemRec), &r, sizeof(r));
-    }
+    };
+    if (pl.tc_rows == 128) build_recs(k::ItemRecT<8>{}); else build_recs(k::ItemRecT<4>{});
     // tile records (the residual loader and the TMA producer stream them instead of chasing page tables)
     pl.tile_ptr.assign(1, 0);
     pl.tile_recs.clear();
@@ -307,12 +323,13 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
         meta |= (ng << 4) | (gmask << 8) | (it.kv_head << 16);
         for (int32_t t0 = it.key_begin; t0 < it.key_end; t0 += kTileKeys) {
           const int32_t sl = t0 / P;
-          int32_t rec[8] = {t0, it.key_end, meta, -1, -1, -1, -1, pl.base_pages[it.base_off + sl]};
-          for (int o = 0; o < it.n_warps; ++o) rec[3 + o] = pl.res_pages[pl.warps[it.warp_off + o].res_off + sl];
-          pl.tile_recs.insert(pl.tile_recs.end(), rec, rec + 8);
+          int32_t rec[k::kTileRecInts] = {t0, it.key_end, meta, pl.base_pages[it.base_off + sl]};
+          for (int o = 0; o < 8; ++o) rec[4 + o] = -1;
+          for (int o = 0; o < it.n_warps; ++o) rec[4 + o] = pl.res_pages[pl.warps[it.warp_off + o].res_off + sl];
+          pl.tile_recs.insert(pl.tile_recs.end(), rec, rec + k::kTileRecInts);
         }
       }
-      pl.tile_ptr.push_back((int32_t)(pl.tile_recs.size() / 8));
+      pl.tile_ptr.push_back((int32_t)(pl.tile_recs.size() / k::kTileRecInts));
     }
   }
   if (entries > INT32_MAX) throw Error(FKV_E_INVALID, "plan: too many partial entries");
@@ -428,7 +445,8 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.sched_items = (const int32_t*)(base + p.off_sitems);
   a.tile_ptr = (const int32_t*)(base + p.off_tptr);
   a.tile_recs = (const int4*)(base + p.off_trecs);
-  a.item_recs = (const k::ItemRec*)(base + p.off_irecs);
+  a.item_recs = base + p.off_irecs;
+  a.tc_rows = p.tc_rows;
   a.n_ctas = p.n_ctas;
   a.stage = p.kernel == 2 ? (uint8_t*)ws + p.stage_off : nullptr;
   cudaError_t e = cudaSuccess;

@@ -47,51 +47,59 @@ namespace k {
 namespace {
 using namespace sm100;
 
-constexpr int kD = 128, kR = 16, kTile = 128, kRows = 64, kSlots = 4;
+constexpr int kD = 128, kR = 16, kTile = 128, kMaxSlots = 8;
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
 constexpr uint32_t T_KL = 256;
 
-template <bool kDef>
+template <bool kDef, int kRowsT>
 struct Cfg {
+  static constexpr int ROWS = kRowsT, SLOTS = kRowsT / 16;
+  static constexpr bool ONES = kRowsT == 64;    // A^T has a free slot for the all-ones rows (row sums l)
   // R_k (small) is single-buffered with its pages L2-prefetched two tiles ahead; V_base / R_v wait for softmax(T):
-  // a deeper ring; P^T double-buffered so softmax(T+1) overlaps PV(T)
-  static constexpr int KS = 2;                   // K_base ring (32 KB: one 128-key tile, both d-halves)
-  static constexpr int RS = 1;                   // R_k ring (16 KB: 4 slots x 128 keys x 32 B), L2-prefetched
-  static constexpr int VS = 3;                   // V-side ring (26 KB: 64-key half of V_base | R_v 4 slots | ones)
-  static constexpr int NP = 2;                   // P^T buffers (16 KB)
-  static constexpr int NQ = kDef ? 1 : 2;        // per-item Q / X buffers
+  // a deeper ring; 64-row CTAs: P^T double-buffered so softmax(T+1) overlaps PV(T)
+  static constexpr int KS = kRowsT == 128 ? 1 : 2;  // K_base ring (32 KB: one 128-key tile, both d-halves)
+  static constexpr int RS = 1;                      // R_k ring (4 KB per slot)
+  static constexpr int VS = kRowsT == 128 ? 2 : 3;  // V-side ring (64-key half of V_base | R_v per slot | ones)
+  static constexpr int NP = kRowsT == 128 ? 1 : 2;  // P^T buffers
+  static constexpr int NQ = (kDef || kRowsT == 128) ? 1 : 2;  // per-item Q / X buffers
   // Accumulator layout switches (both measured on B200): split accumulation chains (SH / PAR = 2) do not help, a
   // tcgen05.mma costs ~120 cycles for N <= 128 whether or not it depends on the previous one
   // (tools/ubench_mma.cu); double-buffered O^T / A^T (AB = 2) overlap an item's epilogue with the next item.
-  static constexpr int AB = kDef ? 1 : 2;        // O^T / A^T accumulator sets in TMEM
+  static constexpr int AB = (kDef || kRowsT == 128) ? 1 : 2;  // O^T / A^T accumulator sets in TMEM
   static constexpr int SH = 1;                   // S^T accumulation chains (d-halves)
   static constexpr int PAR = 1;                  // O^T / A^T accumulation chains (key-chunk parity)
-  __host__ __device__ static constexpr uint32_t tS(int sb, int h) { return SH == 1 ? 64 * sb : 128 * sb + 64 * h; }
-  __host__ __device__ static constexpr uint32_t tO(int ab, int par) { return 128 + 128 * ab + 64 * par * 0; }
-  __host__ __device__ static constexpr uint32_t tA(int ab, int par) { return 192 + 128 * ab + 64 * par * 0; }
+  __host__ __device__ static constexpr uint32_t tS(int sb, int h) { return ROWS * sb + 0 * h; }
+  __host__ __device__ static constexpr uint32_t tO(int ab, int par) { return 2 * ROWS + 2 * ROWS * ab + 0 * par; }
+  __host__ __device__ static constexpr uint32_t tA(int ab, int par) { return 3 * ROWS + 2 * ROWS * ab + 0 * par; }
   static constexpr uint32_t XB = kDef ? 4096 : 512;  // per-slot X image: packed B_k | q~
-  static constexpr uint32_t VE = 26624;
+  static constexpr uint32_t QB = ROWS * 256;         // Q buffer: [2 d-halves][ROWS][128 B]
+  static constexpr uint32_t PB = ROWS * 256;         // P^T buffer: [ROWS / 64][128 keys / 8][8][64 cols x 2 B]
+  static constexpr uint32_t RB = SLOTS * 4096;       // R_k entry: [slot][128 keys][32 B]
+  static constexpr uint32_t VE = 16384 + SLOTS * 2048 + (ONES ? 2048 : 0);
   static constexpr uint32_t OFF_V = 0;
   static constexpr uint32_t OFF_K = OFF_V + VS * VE;
   static constexpr uint32_t OFF_R = OFF_K + KS * 32768;
-  static constexpr uint32_t OFF_Q = OFF_R + RS * 16384;  // [NQ][2 d-halves][64 rows][128 B]
-  static constexpr uint32_t OFF_P = OFF_Q + NQ * 16384;  // [NP][128 keys / 8][8][64 cols x 2 B]
-  static constexpr uint32_t OFF_X = OFF_P + NP * 16384;  // [NQ][4 slots][XB]
-  static constexpr uint32_t OFF_MISC = OFF_X + NQ * kSlots * XB;
-  static constexpr uint32_t SMEM = OFF_MISC + 1024;
+  static constexpr uint32_t OFF_Q = OFF_R + RS * RB;
+  static constexpr uint32_t OFF_P = OFF_Q + NQ * QB;
+  static constexpr uint32_t OFF_X = OFF_P + NP * PB;  // [NQ][SLOTS][XB]
+  static constexpr uint32_t OFF_MISC = OFF_X + NQ * SLOTS * XB;
+  static constexpr uint32_t MISCB = kRowsT == 128 ? 4096 : 1024;
+  static constexpr uint32_t SMEM = OFF_MISC + MISCB;
   static_assert(SMEM <= 232448, "shared memory");
+  static_assert(!(kDef && kRowsT != 64), "DEFERRED runs 64-row CTAs");
 };
 
-struct Misc {
-  uint64_t kfull[2], kempty[2], rfull[1], rempty[1], vfull[3], vempty[3], rvfull[3], qfull[2], qempty[2], sfull[2], sfree[2], pfull[2], pfree[2],
-      accfree[2], klfull[2][kKlBufs], klready[2][kKlBufs];
-  alignas(16) float m_run[kRows];
-  alignas(16) ItemRec rec[2];  // per-item header (staged with the item's Q rows; NQ buffers)
+template <class C>
+struct MiscT {
+  uint64_t kfull[2], kempty[2], rfull[1], rempty[1], vfull[3], vempty[3], rvfull[3], qfull[2], qempty[2], sfull[2],
+      sfree[2], pfull[2], pfree[2], accfree[2], klfull[2][kKlBufs], klready[2][kKlBufs];
+  alignas(16) float m_run[C::ROWS];
+  alignas(16) float lw[C::ONES ? 4 : 4 * C::ROWS];  // no all-ones slot: row-sum partials per key warp [4][ROWS]
+  alignas(16) ItemRecT<C::SLOTS> rec[C::NQ];         // per-item header (staged with the item's Q rows)
   uint32_t tmem_base;
 };
-static_assert(sizeof(Misc) <= 1024, "misc");
 
 struct TcMaps {
   // kb: P == 128: 3D {64, 128, 2} (a whole tile, both d-halves), else 2D {64, P}; vb: P >= 64: 3D {64, 64, 2},
@@ -101,7 +109,7 @@ struct TcMaps {
 
 struct ItemInfo {
   int h, k0, k1, base_off, warp_off, n_slots, n_groups, n_tiles;
-  int g_first[kSlots], g_cnt[kSlots], slot_res[kSlots];
+  int g_first[kMaxSlots], g_cnt[kMaxSlots], slot_res[kMaxSlots];
 };
 
 __device__ __forceinline__ void load_item(const AttnParams& p, int idx, ItemInfo& I) {
@@ -114,7 +122,7 @@ __device__ __forceinline__ void load_item(const AttnParams& p, int idx, ItemInfo
   I.n_slots = it.n_warps;
   I.n_tiles = (it.key_end - it.key_begin + kTile - 1) / kTile;
   int ng = 0, prev_res = -1, prev_ad = -1;
-  for (int o = 0; o < kSlots; ++o) {
+  for (int o = 0; o < kMaxSlots; ++o) {
     if (o < it.n_warps) {
       const DevWarp w = p.warps[it.warp_off + o];
       I.slot_res[o] = w.res_off;
@@ -133,7 +141,19 @@ __device__ __forceinline__ void load_item(const AttnParams& p, int idx, ItemInfo
 }
 
 // group structure from a staged item header
-__device__ __forceinline__ void item_from_rec(const ItemRec& r, ItemInfo& I) {
+// tile record (kTileRecInts ints): a = (t0, k1, meta, base page), b / c = residual pages of slots 0..3 / 4..7
+struct TileRec {
+  int4 a, b, c;
+  __device__ __forceinline__ int page(int o) const {
+    switch (o) {
+      case 0: return b.x; case 1: return b.y; case 2: return b.z; case 3: return b.w;
+      case 4: return c.x; case 5: return c.y; case 6: return c.z; default: return c.w;
+    }
+  }
+};
+
+template <class Rec>
+__device__ __forceinline__ void item_from_rec(const Rec& r, ItemInfo& I) {
   I.k0 = r.k0;
   I.k1 = r.k1;
   I.n_tiles = r.n_tiles;
@@ -164,7 +184,7 @@ __device__ __forceinline__ void load_item_lite(const AttnParams& p, int idx, Ite
   I.n_tiles = (it.key_end - it.key_begin + kTile - 1) / kTile;
   int ng = 0, prev_res = -1, prev_ad = -1;
 #pragma unroll
-  for (int o = 0; o < kSlots; ++o) {
+  for (int o = 0; o < kMaxSlots; ++o) {
     if (o < it.n_warps) {
       const DevWarp w = p.warps[it.warp_off + o];
       if (!(o > 0 && w.res_off == prev_res && w.adapter_slot == prev_ad)) ++ng;
@@ -352,12 +372,17 @@ __global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_warps
 }
 
 // ---------------------------------------------------------------------------
-template <bool kDef>
+template <bool kDef, int kRowsT>
 __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ TcMaps maps, AttnParams p) {
-  using C = Cfg<kDef>;
+  using C = Cfg<kDef, kRowsT>;
+  constexpr int kRows = C::ROWS, kSlots = C::SLOTS;
+  using ItemRec = ItemRecT<kSlots>;
+  using Misc = MiscT<C>;
+  static_assert(sizeof(Misc) <= C::MISCB, "misc");
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   Misc& ms = *reinterpret_cast<Misc*>(smem + C::OFF_MISC);
+  const ItemRec* item_recs = (const ItemRec*)p.item_recs;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (sbase & 1023) __trap();
   const long long t_start = clock64();
@@ -395,8 +420,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
   }
   if (wid == 11) tmem_alloc(smem_u32(&ms.tmem_base), 512);
   // the all-ones R_v slot (index 4) of every V-side entry: A^T lanes 64..79 accumulate the row sums l
-  for (int c = tid; c < C::VS * 128; c += 384)
-    *(uint4*)(smem + C::OFF_V + (c >> 7) * C::VE + 16384 + 4 * 2048 + (c & 127) * 16) =
+  if (C::ONES)
+    for (int c = tid; c < C::VS * 128; c += 384)
+      *(uint4*)(smem + C::OFF_V + (c >> 7) * C::VE + 16384 + kSlots * 2048 + (c & 127) * 16) =
         make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   fence_async_smem();
   tc_fence_before();
@@ -414,20 +440,22 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       const __nv_bfloat16* rkl = (const __nv_bfloat16*)p.res_k + (int64_t)p.layer * p.res_layer_stride;
       const int64_t brow_l = (int64_t)p.layer * p.nb;
       const int r0 = p.tile_ptr[cta], nrec = p.tile_ptr[cta + 1] - r0;
-      auto ldrec = [&](int T, int4& a, int4& b) {
+      auto ldrec = [&](int T, TileRec& r) {
         if (T < nrec) {
-          a = __ldg(&p.tile_recs[2 * (r0 + T)]);
-          b = __ldg(&p.tile_recs[2 * (r0 + T) + 1]);
+          const int4* q = p.tile_recs + (int64_t)(r0 + T) * (kTileRecInts / 4);
+          r.a = __ldg(q);
+          r.b = __ldg(q + 1);
+          r.c = __ldg(q + 2);
         }
       };
-      auto base_row = [&](const int4& a, const int4& b) {  // 2D-view row of the tile's base page
-        return (int)(((brow_l + b.w) * p.hkv + (a.z >> 16)) * kTile);
+      auto base_row = [&](const TileRec& r) {  // 2D-view row of the tile's base page
+        return (int)(((brow_l + r.a.w) * p.hkv + (r.a.z >> 16)) * kTile);
       };
-      int4 kA = make_int4(0, 0, 0, 0), kB = kA, rA = kA, rB = kA, fA = kA, fB = kA;
-      ldrec(0, kA, kB);
-      rA = kA; rB = kB;
+      TileRec kR_ = {}, rR = {}, fR = {};
+      ldrec(0, kR_);
+      rR = kR_;
       constexpr int kPf = 2;  // L2 prefetch distance (tiles) of K_base and R_k
-      ldrec(kPf, fA, fB);
+      ldrec(kPf, fR);
       uint32_t nk = 0, nr = 0;
       int iq = 0;
       int qitem = n_my > 0 ? p.sched_items[it_begin] : 0;
@@ -442,18 +470,17 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               ev(p, 0, nk);
               const uint32_t bar = smem_u32(&ms.kfull[slot]);
               mbar_expect_tx(bar, 32768);
-              tma_load_3d(sbase + C::OFF_K + slot * 32768, &maps.kb, 0, base_row(kA, kB), 0, bar);
+              tma_load_3d(sbase + C::OFF_K + slot * 32768, &maps.kb, 0, base_row(kR_), 0, bar);
             }
             if (nk + kPf < (uint32_t)nrec) {  // R_k pages of tile nk + kPf -> L2 (one 128-byte line per lane)
-              const int pgs[4] = {fA.w, fB.x, fB.y, fB.z};
 #pragma unroll
               for (int o = 0; o < kSlots; ++o)
-                if ((fA.z >> (8 + o)) & 1)
-                  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(rkl + (int64_t)pgs[o] * kTile * kR + lane * 64));
+                if ((fR.a.z >> (8 + o)) & 1)
+                  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(rkl + (int64_t)fR.page(o) * kTile * kR + lane * 64));
             }
             ++nk;
-            ldrec(nk, kA, kB);
-            ldrec(nk + kPf, fA, fB);
+            ldrec(nk, kR_);
+            ldrec(nk + kPf, fR);
             progress = true;
           }
         }
@@ -461,12 +488,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           busy = true;
           const int slot = nr % C::RS;
           if (nr < (uint32_t)C::RS || mbar_test(smem_u32(&ms.rempty[slot]), ((nr / C::RS) - 1) & 1)) {
-            const uint32_t dst = sbase + C::OFF_R + slot * 16384;
-            const int pgs[4] = {rA.w, rB.x, rB.y, rB.z};
+            const uint32_t dst = sbase + C::OFF_R + slot * C::RB;
 #pragma unroll
             for (int o = 0; o < kSlots; ++o) {
-              if ((rA.z >> (8 + o)) & 1) {
-                const __nv_bfloat16* src = rkl + (int64_t)pgs[o] * kTile * kR;
+              if ((rR.a.z >> (8 + o)) & 1) {
+                const __nv_bfloat16* src = rkl + (int64_t)rR.page(o) * kTile * kR;
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                   const int c = lane + 32 * u;
@@ -478,7 +504,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             }
             cp_async_arrive(smem_u32(&ms.rfull[slot]));
             ++nr;
-            ldrec(nr, rA, rB);
+            ldrec(nr, rR);
             progress = true;
           }
         }
@@ -487,14 +513,14 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           const int qb = iq % C::NQ;
           if (iq < C::NQ || mbar_test(smem_u32(&ms.qempty[qb]), ((iq / C::NQ) - 1) & 1)) {
             ev(p, 9, iq);
-            const uint8_t* rsrc = (const uint8_t*)(p.item_recs + qitem);
+            const uint8_t* rsrc = (const uint8_t*)(item_recs + qitem);
             if (lane < (int)(sizeof(ItemRec) / 16)) cp_async16(smem_u32(&ms.rec[qb]) + lane * 16, rsrc + lane * 16);
             for (int o = 0; o < qit.n_warps; ++o) {
               const uint8_t* src = p.stage + (int64_t)(qit.warp_off + o) * kStageBytes;
 #pragma unroll
               for (int u = 0; u < 8; ++u) {  // Q image: 2 x 2 KB
                 const int c = lane + 32 * u;
-                cp_async16(sbase + C::OFF_Q + qb * 16384 + (c >> 7) * 8192 + o * 2048 + (c & 127) * 16, src + c * 16);
+                cp_async16(sbase + C::OFF_Q + qb * C::QB + (c >> 7) * (C::QB / 2) + o * 2048 + (c & 127) * 16, src + c * 16);
               }
               for (int c = lane; c < (int)(C::XB / 16); c += 32)
                 cp_async16(sbase + C::OFF_X + qb * kSlots * C::XB + o * C::XB + c * 16, src + 4096 + c * 16);
@@ -607,11 +633,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             ev(p, 9, iq);
             const uint32_t bar = smem_u32(&ms.qfull[qb]);
             mbar_expect_tx(bar, it.n_warps * (4096 + C::XB) + (uint32_t)sizeof(ItemRec));
-            bulk_g2s(smem_u32(&ms.rec[qb]), p.item_recs + p.sched_items[it_begin + iq], sizeof(ItemRec), bar);
+            bulk_g2s(smem_u32(&ms.rec[qb]), item_recs + p.sched_items[it_begin + iq], sizeof(ItemRec), bar);
             for (int o = 0; o < it.n_warps; ++o) {
               const uint8_t* src = p.stage + (int64_t)(it.warp_off + o) * kStageBytes;
-              bulk_g2s(sbase + C::OFF_Q + qb * 16384 + o * 2048, src, 2048, bar);
-              bulk_g2s(sbase + C::OFF_Q + qb * 16384 + 8192 + o * 2048, src + 2048, 2048, bar);
+              bulk_g2s(sbase + C::OFF_Q + qb * C::QB + o * 2048, src, 2048, bar);
+              bulk_g2s(sbase + C::OFF_Q + qb * C::QB + C::QB / 2 + o * 2048, src + 2048, 2048, bar);
               bulk_g2s(sbase + C::OFF_X + qb * kSlots * C::XB + o * C::XB, src + 4096, C::XB, bar);
             }
             ++iq;
@@ -628,7 +654,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       uint32_t T = 0, U = 0;
       for (int ii = 0; ii < n_my; ++ii) {
         const int qb = ii % C::NQ;
-        const uint32_t qs = sbase + C::OFF_Q + qb * 16384;
+        const uint32_t qs = sbase + C::OFF_Q + qb * C::QB;
         const uint32_t xs = sbase + C::OFF_X + qb * kSlots * C::XB;
         mbar_wait(smem_u32(&ms.qfull[qb]), (ii / C::NQ) & 1);
         ev(p, 10, ii);
@@ -636,17 +662,17 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         // group table of the item, packed 8 bits per group: first slot, slot count
         const int meta = ms.rec[qb].meta, n_tiles = ms.rec[qb].n_tiles;
         const int n_slots = meta & 15;
-        uint32_t gf = 0, gc = 0;
+        uint64_t gf = 0, gc = 0;  // 8 bits per group
         int ng = 0;
 #pragma unroll
         for (int o = 0; o < kSlots; ++o) {
           if (o < n_slots) {
             if ((meta >> (8 + o)) & 1) {
-              gf |= (uint32_t)o << (8 * ng);
-              gc |= 1u << (8 * ng);
+              gf |= (uint64_t)o << (8 * ng);
+              gc |= 1ull << (8 * ng);
               ++ng;
             } else {
-              gc += 1u << (8 * (ng - 1));
+              gc += 1ull << (8 * (ng - 1));
             }
           }
         }
@@ -655,7 +681,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           const int sb = T & 1;
           const uint32_t sacc = tm + C::tS(sb, 0);
           const uint64_t dk = make_desc(sbase + C::OFF_K + (T % C::KS) * 32768, 16, 1024, SWZ_128);
-          const uint32_t rk = sbase + C::OFF_R + (T % C::RS) * 16384;
+          const uint32_t rk = sbase + C::OFF_R + (T % C::RS) * C::RB;
           auto base_s = [&]() {  // S^T = K_base Q^T over both d-halves (descriptor + (byte offset >> 4))
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -663,7 +689,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               const int c = C::SH == 2 ? ((i & 1) * 4 + (i >> 1)) : i;
               const int h = C::SH == 2 ? (c >> 2) : 0;
               mma_ss_e(tm + C::tS(sb, h), dk + (uint64_t)(((c >> 2) * 16384 + (c & 3) * 32) >> 4),
-                       dq + (uint64_t)(((c >> 2) * 8192 + (c & 3) * 32) >> 4), id_s, C::SH == 2 ? (c & 3) != 0 : c != 0);
+                       dq + (uint64_t)(((c >> 2) * (C::QB / 2) + (c & 3) * 32) >> 4), id_s, C::SH == 2 ? (c & 3) != 0 : c != 0);
             }
             mma_commit_e(smem_u32(&ms.kempty[T % C::KS]));
           };
@@ -680,7 +706,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 #pragma unroll
             for (int g = 0; g < kSlots; ++g) {
               if (g < ng) {
-                const uint32_t o = (gf >> (8 * g)) & 0xff, cnt = (gc >> (8 * g)) & 0xff;
+                const uint32_t o = (uint32_t)(gf >> (8 * g)) & 0xff, cnt = (uint32_t)(gc >> (8 * g)) & 0xff;
                 mma_ss_e(tm + C::tS(sb, C::SH - 1) + 16 * o, dr + (uint64_t)(o * 256), dx + (uint64_t)(o * 32),
                          idesc_bf16(128, 16 * cnt, false, false), 1);
               }
@@ -694,7 +720,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             const uint64_t dr = make_desc(rk, 16, 256, SWZ_32), dx = make_desc(xs, 1024, 512, SWZ_64);
             auto rb = [&](int w, int k) {  // KL[w][b] (fp32, 32 cols) = R_k,g B_k,g[:, quarter block 2w + q]
               const int q = k >= ng, g = k - q * ng;
-              const uint32_t o = (gf >> (8 * g)) & 0xff;
+              const uint32_t o = (uint32_t)(gf >> (8 * g)) & 0xff;
               const uint32_t b = (U + k) % kKlBufs;
               mma_ss_e(tm + T_KL + 128 * w + 32 * b, dr + (uint64_t)(o * 256),
                        dx + (uint64_t)((o * 4096 + (2 * w + q) * 1024) >> 4), id_rb, 0);
@@ -703,7 +729,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             };
             auto ts = [&](int w, int k) {  // S^T[:, rows of g] += RoPE(KL)[bf16, in place] Q_g^T over the unit's 32 d
               const int q = k >= ng, g = k - q * ng;
-              const uint32_t o = (gf >> (8 * g)) & 0xff, cnt = (gc >> (8 * g)) & 0xff;
+              const uint32_t o = (uint32_t)(gf >> (8 * g)) & 0xff, cnt = (uint32_t)(gc >> (8 * g)) & 0xff;
               const uint32_t Uk = U + k, b = Uk % kKlBufs;
               if (T == 4) ev(p, 11, 32 * w + k);
               mbar_wait(smem_u32(&ms.klready[w][b]), (Uk / kKlBufs) & 1);
@@ -714,7 +740,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               for (int s2 = 0; s2 < 2; ++s2) {
                 const uint32_t d = 64 * s2 + 32 * w + 16 * q;
                 mma_ts_e(sacc + 16 * o, tm + T_KL + 128 * w + 32 * b + 8 * s2,
-                         dq + (uint64_t)(((d >> 6) * 8192 + 2048 * o + (d & 63) * 2) >> 4), id, 1);
+                         dq + (uint64_t)(((d >> 6) * (C::QB / 2) + 2048 * o + (d & 63) * 2) >> 4), id, 1);
               }
             };
             for (int k = 0; k < n_units && k < kKlBufs; ++k) { rb(0, k); rb(1, k); }
@@ -751,7 +777,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           ev(p, 5, T);
           const int ab = ii % C::AB;
           if (j == 0 && ii >= C::AB) mbar_wait(smem_u32(&ms.accfree[ab]), ((ii / C::AB) - 1) & 1);
-          const uint64_t dp = make_desc(sbase + C::OFF_P + pb * 16384, 16384, 1024, SWZ_128);
+          const uint64_t dp = make_desc(sbase + C::OFF_P + pb * C::PB, 16384, 1024, SWZ_128);
           for (int kh = 0; kh < 2; ++kh, ++nv) {
             mbar_wait(smem_u32(&ms.vfull[nv % C::VS]), (nv / C::VS) & 1);
             mbar_wait(smem_u32(&ms.rvfull[nv % C::VS]), (nv / C::VS) & 1);
@@ -789,27 +815,31 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         // fast path: one page per tile; R_v halves only (R_k is streamed by the producer warp); page ids from
         // the tile records (32 per lane batch, the next batch prefetched)
         const int r0 = p.tile_ptr[cta], nrec = p.tile_ptr[cta + 1] - r0;
-        int4 ca = make_int4(0, 0, 0, 0), cbv = ca, na = ca, nb = ca;
+        TileRec cur = {}, nxt = {};  // lane L holds the record of tile (batch * 32 + L)
         auto load_batch = [&](int base) {
           const int r = base + lane;
           if (r < nrec) {
-            na = __ldg(&p.tile_recs[2 * (r0 + r)]);
-            nb = __ldg(&p.tile_recs[2 * (r0 + r) + 1]);
+            const int4* q = p.tile_recs + (int64_t)(r0 + r) * (kTileRecInts / 4);
+            nxt.a = __ldg(q);
+            nxt.b = __ldg(q + 1);
+            nxt.c = __ldg(q + 2);
           }
         };
         load_batch(0);
         for (int T = 0; T < nrec; ++T) {
           if ((T & 31) == 0) {
-            ca = na;
-            cbv = nb;
+            cur = nxt;
             load_batch(T + 32);
           }
           const int L = T & 31;
-          const int ns = __shfl_sync(0xffffffffu, ca.z, L) & 15;
-          const int vh = __shfl_sync(0xffffffffu, ca.z, L) >> 16, bpg = __shfl_sync(0xffffffffu, cbv.w, L);
-          const int vrow = (int)((((int64_t)p.layer * p.nb + bpg) * p.hkv + vh) * kTile);
-          const int g0 = __shfl_sync(0xffffffffu, ca.w, L), g1 = __shfl_sync(0xffffffffu, cbv.x, L);
-          const int g2 = __shfl_sync(0xffffffffu, cbv.y, L), g3 = __shfl_sync(0xffffffffu, cbv.z, L);
+          TileRec rc;
+          rc.a = make_int4(0, 0, __shfl_sync(0xffffffffu, cur.a.z, L), __shfl_sync(0xffffffffu, cur.a.w, L));
+          rc.b = make_int4(__shfl_sync(0xffffffffu, cur.b.x, L), __shfl_sync(0xffffffffu, cur.b.y, L),
+                           __shfl_sync(0xffffffffu, cur.b.z, L), __shfl_sync(0xffffffffu, cur.b.w, L));
+          rc.c = make_int4(__shfl_sync(0xffffffffu, cur.c.x, L), __shfl_sync(0xffffffffu, cur.c.y, L),
+                           __shfl_sync(0xffffffffu, cur.c.z, L), __shfl_sync(0xffffffffu, cur.c.w, L));
+          const int ns = rc.a.z & 15;
+          const int vrow = (int)((((int64_t)p.layer * p.nb + rc.a.w) * p.hkv + (rc.a.z >> 16)) * kTile);
           for (int h = 0; h < 2; ++h) {
             const uint32_t nv = 2 * T + h, slot = nv % C::VS;
             if (nv >= (uint32_t)C::VS) wait_free(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1);
@@ -823,8 +853,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 #pragma unroll
             for (int o = 0; o < kSlots; ++o) {
               if (o < ns) {
-                const int pg = o == 0 ? g0 : (o == 1 ? g1 : (o == 2 ? g2 : g3));
-                const __nv_bfloat16* src = rvl + ((int64_t)pg * kTile + 64 * h) * kR;
+                const __nv_bfloat16* src = rvl + ((int64_t)rc.page(o) * kTile + 64 * h) * kR;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                   const int c = lane + 32 * u;
@@ -847,7 +876,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           {  // R_k of the item's groups: 4 KB per group at the group's first slot
             const int slot = T % C::RS;
             if (T >= (uint32_t)C::RS) wait_free(smem_u32(&ms.rempty[slot]), ((T / C::RS) - 1) & 1);
-            const uint32_t dst = sbase + C::OFF_R + slot * 16384;
+            const uint32_t dst = sbase + C::OFF_R + slot * C::RB;
             for (int g = 0; g < I.n_groups; ++g) {
               const int o = I.g_first[g];
 #pragma unroll
@@ -890,10 +919,13 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
     // ================= key warps =================
+    // thread = key of the tile = TMEM lane; key warpgroup w owns query columns [CPW w, CPW (w + 1)), processed in
+    // chunks of 32 (one TMEM load of S^T each); DEFERRED (64-row CTAs): also the d-half w of the K_lora rotation
+    constexpr int CPW = kRows / 2, NCH = CPW / 32;
     const int w = wid >> 2;                         // key warpgroup 0/1
     const int kl = tid - 128 * w;                   // key within the tile == TMEM lane
-    const uint32_t lb = (uint32_t)(32 * (wid & 3)) << 16;
-    const int cb = 32 * w;                          // this group's query columns [cb, cb + 32)
+    const int wq = wid & 3;                         // warp within the warpgroup (TMEM lane quarter)
+    const uint32_t lb = (uint32_t)(32 * wq) << 16;
     const uint32_t bar_id = 1 + w;                  // named barrier of this warpgroup
     const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
     const float scl = p.scale_log2;
@@ -912,41 +944,42 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         cst[4 * q + 2] = pack_h2(a.z, b.z); cst[4 * q + 3] = pack_h2(a.w, b.w);
       }
     }
-    // partial entries [m, l, acc[128], acc_r[16]] of item ii, columns [cb, cb+32): l, acc, acc_r (m is written
-    // at the item's end), once PV of its last tile Tl completed; then the accumulators and the header are free
+    // partial entries [m, l, acc[128], acc_r[16]] of item ie: l, acc, acc_r (m is written at the item's end), once PV
+    // of its last tile Tl completed; then the accumulators and the header are free
     auto epilogue = [&](int ie, uint32_t Tl, int qbe) {
       const ItemRec& Re = ms.rec[qbe];
       const int ab = ie % C::AB, ns = Re.meta & 15;
       mbar_wait(smem_u32(&ms.pfree[Tl % C::NP]), (Tl / C::NP) & 1);
       tc_fence_after();
-      uint32_t o_[32], a_[32];
-      FKV_TMEM_LD32(tm + C::tO(ab, 0) + cb + lb, o_);
-      FKV_TMEM_LD32(tm + C::tA(ab, 0) + cb + lb, a_);
-      if constexpr (C::PAR == 2) {  // sum the key-chunk parity chains
-        uint32_t o1[32];
-        FKV_TMEM_LD32(tm + C::tO(ab, 1) + cb + lb, o1);
+#pragma unroll 1
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int cb = CPW * w + 32 * ch;
+        uint32_t o_[32], a_[32];
+        FKV_TMEM_LD32(tm + C::tO(ab, 0) + cb + lb, o_);
+        FKV_TMEM_LD32(tm + C::tA(ab, 0) + cb + lb, a_);
         tmem_ld_wait();
+        if (ch == NCH - 1) {
+          tc_fence_before();
+          mbar_arrive(smem_u32(&ms.accfree[ab]));
+        }
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o_[i] = __float_as_uint(__uint_as_float(o_[i]) + __uint_as_float(o1[i]));
-        FKV_TMEM_LD32(tm + C::tA(ab, 1) + cb + lb, o1);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) a_[i] = __float_as_uint(__uint_as_float(a_[i]) + __uint_as_float(o1[i]));
-      }
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(smem_u32(&ms.accfree[ab]));
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int c = cb + i, o = c >> 4, r = c & 15;
-        if (o < ns && r < Re.n_rows[o]) {
-          float* ent = p.ws + (int64_t)(Re.entry_off[o] + r) * p.entry_stride;
-          ent[2 + kl] = __uint_as_float(o_[i]);                                  // acc[d = kl]
-          if ((kl >> 4) == o) ent[2 + kD + (kl & 15)] = __uint_as_float(a_[i]);  // acc_r[j] of this row's owner
-          if (kl == 64) ent[1] = __uint_as_float(a_[i]);                         // l (all-ones slot)
+        for (int i = 0; i < 32; ++i) {
+          const int c = cb + i, o = c >> 4, r = c & 15;
+          if (o < ns && r < Re.n_rows[o]) {
+            float* ent = p.ws + (int64_t)(Re.entry_off[o] + r) * p.entry_stride;
+            ent[2 + kl] = __uint_as_float(o_[i]);                                  // acc[d = kl]
+            if ((kl >> 4) == o) ent[2 + kD + (kl & 15)] = __uint_as_float(a_[i]);  // acc_r[j] of this row's owner
+            if (kl == 64) {
+              if constexpr (C::ONES) {
+                ent[1] = __uint_as_float(a_[i]);  // l (all-ones slot)
+              } else {
+                ent[1] = ms.lw[c] + ms.lw[kRows + c] + ms.lw[2 * kRows + c] + ms.lw[3 * kRows + c];
+              }
+            }
+          }
         }
       }
-      // this warpgroup is done with the item header
+      // this warpgroup is done with the item header (and the row-sum partials)
       named_bar_sync(bar_id, 128);
       if (kl == 0) mbar_arrive(smem_u32(&ms.qempty[qbe]));
     };
@@ -962,34 +995,29 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       I.n_tiles = R.n_tiles;
       I.n_slots = R.meta & 15;
       I.n_groups = (R.meta >> 4) & 15;
-      const uint16_t* P1 = R.pos1 + cb;  // this group's columns: key t visible iff t - k0 < P1[c]
-      // per-item column state (this warpgroup's 32 columns); the previous item's epilogue is done with m_run
+      // per-item column state of this warpgroup; the previous item's epilogue is done with m_run / lw
       named_bar_sync(bar_id, 128);
-      if (kl < 32) ms.m_run[cb + kl] = -INFINITY;
-      named_bar_sync(bar_id, 128);
-      bool causal = false;
+      if (kl < CPW) {
+        ms.m_run[CPW * w + kl] = -INFINITY;
+        if constexpr (!C::ONES) {
 #pragma unroll
-      for (int c = 0; c < 32; ++c) causal |= (int)P1[c] < I.k1 - I.k0;
+          for (int q = 0; q < 4; ++q) ms.lw[q * kRows + CPW * w + kl] = 0.f;
+        }
+      }
+      named_bar_sync(bar_id, 128);
+      uint32_t causal_mask = 0;  // bit ch: chunk ch has a column that does not see every key of the item
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const uint16_t* P1c = R.pos1 + CPW * w + 32 * ch;
+        bool cz = false;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) cz |= (int)P1c[c] < I.k1 - I.k0;
+        causal_mask |= (uint32_t)cz << ch;
+      }
       for (int j = 0; j < I.n_tiles; ++j, ++T) {
         const int t0 = I.k0 + j * kTile;
         const int t = t0 + kl;
         const bool tvalid = t < I.k1;
-        // visibility of this key for the warpgroup's 32 columns (bit c): in range and, for causal rows, t <= pos
-        uint32_t vm = tvalid ? 0xffffffffu : 0u;
-        if (causal && tvalid) {
-          const int tr = t - I.k0;
-          vm = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint4 pv = *(const uint4*)(P1 + 8 * q);
-            const uint32_t w4[4] = {pv.x, pv.y, pv.z, pv.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              vm |= (uint32_t)(tr < (int)(w4[e] & 0xffffu)) << (8 * q + 2 * e);
-              vm |= (uint32_t)(tr < (int)(w4[e] >> 16)) << (8 * q + 2 * e + 1);
-            }
-          }
-        }
         if constexpr (kDef) {
           const int prow = t0 < p.max_pos ? t0 : p.max_pos - 1;
 #pragma unroll
@@ -1042,159 +1070,200 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             }
           }
         }
-        // ---- online softmax over this group's 32 query columns (Alg1.339-341) ----
         const int sb = T & 1;
-        mbar_wait(smem_u32(&ms.sfull[sb]), (T >> 1) & 1);
-        if (tid == 0) ev(p, 3, T);
-        tc_fence_after();
-        uint32_t sr[32];
-        FKV_TMEM_LD32(tm + C::tS(sb, 0) + cb + lb, sr);
-        if constexpr (C::SH == 2) {  // add the second d-half chain
-          uint32_t s1[32];
-          FKV_TMEM_LD32(tm + C::tS(sb, 1) + cb + lb, s1);
+        const int pb = T % C::NP;
+        uint8_t* pbuf = smem + C::OFF_P + pb * C::PB;
+#pragma unroll 1
+        for (int ch = 0; ch < NCH; ++ch) {
+          // ---- online softmax over the chunk's 32 query columns (Alg1.339-341) ----
+          const int cb = CPW * w + 32 * ch;
+          const uint16_t* P1 = R.pos1 + cb;  // key t visible iff t - k0 < P1[c]
+          uint32_t vm = tvalid ? 0xffffffffu : 0u;
+          if (((causal_mask >> ch) & 1) && tvalid) {
+            const int tr = t - I.k0;
+            vm = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 pv = *(const uint4*)(P1 + 8 * q);
+              const uint32_t w4[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                vm |= (uint32_t)(tr < (int)(w4[e] & 0xffffu)) << (8 * q + 2 * e);
+                vm |= (uint32_t)(tr < (int)(w4[e] >> 16)) << (8 * q + 2 * e + 1);
+              }
+            }
+          }
+          if (ch == 0) {
+            mbar_wait(smem_u32(&ms.sfull[sb]), (T >> 1) & 1);
+            if (tid == 0) ev(p, 3, T);
+            tc_fence_after();
+          }
+          uint32_t sr[32];
+          FKV_TMEM_LD32(tm + C::tS(sb, 0) + cb + lb, sr);
           tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < 32; c += 2) {
-            const uint64_t a = fadd2(f2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])),
-                                     f2(__uint_as_float(s1[c]), __uint_as_float(s1[c + 1])));
-            float x, y;
-            uf2(a, x, y);
-            sr[c] = __float_as_uint(x);
-            sr[c + 1] = __float_as_uint(y);
+          if (ch == NCH - 1) {
+            tc_fence_before();
+            mbar_arrive(smem_u32(&ms.sfree[sb]));
           }
-        }
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(smem_u32(&ms.sfree[sb]));
-        uint64_t x2[16];
-        float mx = -INFINITY;
-        {
-          const float4* mp = (const float4*)&ms.m_run[cb];
+          uint64_t x2[16];
+          float mx = -INFINITY;
+          {
+            const float4* mp = (const float4*)&ms.m_run[cb];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 m4 = mp[q];
-            const uint64_t s01 = f2(__uint_as_float(sr[4 * q]), __uint_as_float(sr[4 * q + 1]));
-            const uint64_t s23 = f2(__uint_as_float(sr[4 * q + 2]), __uint_as_float(sr[4 * q + 3]));
-            x2[2 * q] = fma2(s01, sc2, f2(-m4.x, -m4.y));
-            x2[2 * q + 1] = fma2(s23, sc2, f2(-m4.z, -m4.w));
-          }
-          if (vm != 0xffffffffu) {
+            for (int q = 0; q < 8; ++q) {
+              const float4 m4 = mp[q];
+              const uint64_t s01 = f2(__uint_as_float(sr[4 * q]), __uint_as_float(sr[4 * q + 1]));
+              const uint64_t s23 = f2(__uint_as_float(sr[4 * q + 2]), __uint_as_float(sr[4 * q + 3]));
+              x2[2 * q] = fma2(s01, sc2, f2(-m4.x, -m4.y));
+              x2[2 * q + 1] = fma2(s23, sc2, f2(-m4.z, -m4.w));
+            }
+            if (vm != 0xffffffffu) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                float a, b2;
+                uf2(x2[q], a, b2);
+                a = (vm >> (2 * q)) & 1u ? a : -INFINITY;
+                b2 = (vm >> (2 * q + 1)) & 1u ? b2 : -INFINITY;
+                x2[q] = f2(a, b2);
+              }
+            }
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
               float a, b2;
               uf2(x2[q], a, b2);
-              a = (vm >> (2 * q)) & 1u ? a : -INFINITY;
-              b2 = (vm >> (2 * q + 1)) & 1u ? b2 : -INFINITY;
-              x2[q] = f2(a, b2);
+              mx = max3(mx, a, b2);
             }
           }
+          // lazy rescaling: only when some score exceeds the running max by > 2^8
+          float alpha_l = 1.f;  // this lane's column (cb + lane) rescale factor (row-sum partials)
+          if (tid == 0) ev(p, 20, T);
+          if (bar_or(bar_id, 128, mx > 8.0f)) {
+            if (tid == 0) ev(p, 21, T);
+            float mo[32];
+            {
+              const float4* mp = (const float4*)&ms.m_run[cb];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float4 m4 = mp[q];
+                mo[4 * q] = m4.x; mo[4 * q + 1] = m4.y; mo[4 * q + 2] = m4.z; mo[4 * q + 3] = m4.w;
+              }
+            }
+            const float mo_l = ms.m_run[cb + lane];
+            float v[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const bool ok = (vm >> c) & 1u;
+              v[c] = ok ? __uint_as_float(sr[c]) * scl : -INFINITY;
+            }
+#pragma unroll
+            for (int step = 0; step < 5; ++step) {
+              const int off = 16 >> step, half = 16 >> step;
+              const bool up = lane & off;
+#pragma unroll
+              for (int i = 0; i < half; ++i) {
+                const float send = up ? v[i] : v[i + half];
+                const float keep = up ? v[i + half] : v[i];
+                v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, off));
+              }
+            }
+            // lane l holds the warp's max for column cb + l
+            named_bar_sync(bar_id, 128);
+            if (tid == 0) ev(p, 22, T);
+            if (v[0] > -INFINITY) atomic_max_f(&ms.m_run[cb + lane], v[0]);
+            named_bar_sync(bar_id, 128);
+            if (tid == 0) ev(p, 23, T);
+            float mn[32];
+            bool resc = false;
+            {
+              const float4* mp = (const float4*)&ms.m_run[cb];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float4 m4 = mp[q];
+                mn[4 * q] = m4.x; mn[4 * q + 1] = m4.y; mn[4 * q + 2] = m4.z; mn[4 * q + 3] = m4.w;
+              }
+            }
+            {
+              const float mn_l = ms.m_run[cb + lane];
+              alpha_l = mo_l == -INFINITY ? 0.f : ex2(mo_l - mn_l);
+            }
+            float al[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {  // branch-free: ex2(0) = 1 for unchanged columns
+              const bool fresh = mo[c] == -INFINITY;
+              al[c] = fresh ? 0.f : ex2(mo[c] - mn[c]);
+              resc |= !fresh && (mn[c] != mo[c]);
+            }
+            if (resc && j > 0) {
+              // rescale the chunk's columns of O^T and A^T by alpha (all PV up to tile T-1 complete)
+              mbar_wait(smem_u32(&ms.pfree[(T - 1) % C::NP]), ((T - 1) / C::NP) & 1);
+              tc_fence_after();
+#pragma unroll
+              for (int part = 0; part < 2; ++part) {
+                const uint32_t base = tm + ((part & 1) ? C::tA(ii % C::AB, 0) : C::tO(ii % C::AB, 0)) + cb + lb;
+                uint32_t r[32];
+                FKV_TMEM_LD32(base, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * al[i]);
+                FKV_TMEM_ST16(base, r);
+                FKV_TMEM_ST16(base + 16, (r + 16));
+              }
+              tmem_st_wait();
+              tc_fence_before();
+            }
+            if (tid == 0) ev(p, 24, T);
+            // recompute with the updated running max (a column with no visible key keeps -inf -> p = 0)
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const float m0 = mn[2 * q], m1 = mn[2 * q + 1];
+              const bool ok0 = (vm >> (2 * q)) & 1u;
+              const bool ok1 = (vm >> (2 * q + 1)) & 1u;
+              const float x0 = ok0 ? __uint_as_float(sr[2 * q]) * scl - (m0 == -INFINITY ? 0.f : m0) : -INFINITY;
+              const float x1 = ok1 ? __uint_as_float(sr[2 * q + 1]) * scl - (m1 == -INFINITY ? 0.f : m1) : -INFINITY;
+              x2[q] = f2(x0, x1);
+            }
+          }
+          // P^T row of this key (bf16, MN-major SW128), the chunk's columns
+          uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             float a, b2;
             uf2(x2[q], a, b2);
-            mx = max3(mx, a, b2);
+            pk[q] = pack_bf16x2(ex2(a), ex2(b2));
+          }
+          if (ch == 0) {
+            if (tid == 0) ev(p, 16, T);
+            if (T >= (uint32_t)C::NP) mbar_wait(smem_u32(&ms.pfree[pb]), ((T / C::NP) - 1) & 1);
+            if (tid == 0) ev(p, 17, T);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *(uint4*)(pbuf + mnmajor_off(cb + q * 8, kl, 8, 16384, 1024)) =
+                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          if constexpr (!C::ONES) {
+            // row sums l without an all-ones MMA slot: the warp's 32 keys summed per column (of the bf16 P the
+            // MMA uses), lane l -> column cb + l; per-warp partials, rescaled with the running max
+            float v[32];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              v[2 * q] = __uint_as_float(pk[q] << 16);
+              v[2 * q + 1] = __uint_as_float(pk[q] & 0xffff0000u);
+            }
+#pragma unroll
+            for (int step = 0; step < 5; ++step) {
+              const int off = 16 >> step, half = 16 >> step;
+              const bool up = lane & off;
+#pragma unroll
+              for (int i = 0; i < half; ++i) {
+                const float send = up ? v[i] : v[i + half];
+                const float keep = up ? v[i + half] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+              }
+            }
+            float* lp = &ms.lw[wq * kRows + cb + lane];
+            *lp = *lp * alpha_l + v[0];
           }
         }
-        // lazy rescaling: only when some score exceeds the running max by > 2^8
-        if (tid == 0) ev(p, 20, T);
-        if (bar_or(bar_id, 128, mx > 8.0f)) {
-          if (tid == 0) ev(p, 21, T);
-          float mo[32];
-          {
-            const float4* mp = (const float4*)&ms.m_run[cb];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 m4 = mp[q];
-              mo[4 * q] = m4.x; mo[4 * q + 1] = m4.y; mo[4 * q + 2] = m4.z; mo[4 * q + 3] = m4.w;
-            }
-          }
-          float v[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const bool ok = (vm >> c) & 1u;
-            v[c] = ok ? __uint_as_float(sr[c]) * scl : -INFINITY;
-          }
-#pragma unroll
-          for (int step = 0; step < 5; ++step) {
-            const int off = 16 >> step, half = 16 >> step;
-            const bool up = lane & off;
-#pragma unroll
-            for (int i = 0; i < half; ++i) {
-              const float send = up ? v[i] : v[i + half];
-              const float keep = up ? v[i + half] : v[i];
-              v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, off));
-            }
-          }
-          // lane l holds the warp's max for column cb + l
-          named_bar_sync(bar_id, 128);
-          if (tid == 0) ev(p, 22, T);
-          if (v[0] > -INFINITY) atomic_max_f(&ms.m_run[cb + lane], v[0]);
-          named_bar_sync(bar_id, 128);
-          if (tid == 0) ev(p, 23, T);
-          float mn[32];
-          bool resc = false;
-          {
-            const float4* mp = (const float4*)&ms.m_run[cb];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 m4 = mp[q];
-              mn[4 * q] = m4.x; mn[4 * q + 1] = m4.y; mn[4 * q + 2] = m4.z; mn[4 * q + 3] = m4.w;
-            }
-          }
-          float al[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {  // branch-free: ex2(0) = 1 for unchanged columns
-            const bool fresh = mo[c] == -INFINITY;
-            al[c] = fresh ? 0.f : ex2(mo[c] - mn[c]);
-            resc |= !fresh && (mn[c] != mo[c]);
-          }
-          if (resc && j > 0) {
-            // rescale this group's columns of O^T and A^T by alpha (all PV up to tile T-1 complete)
-            mbar_wait(smem_u32(&ms.pfree[(T - 1) % C::NP]), ((T - 1) / C::NP) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int part = 0; part < 2 * C::PAR; ++part) {
-              const uint32_t base = tm + ((part & 1) ? C::tA(ii % C::AB, part >> 1) : C::tO(ii % C::AB, part >> 1)) + cb + lb;
-              uint32_t r[32];
-              FKV_TMEM_LD32(base, r);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * al[i]);
-              FKV_TMEM_ST16(base, r);
-              FKV_TMEM_ST16(base + 16, (r + 16));
-            }
-            tmem_st_wait();
-            tc_fence_before();
-          }
-          if (tid == 0) ev(p, 24, T);
-          // recompute with the updated running max (a column with no visible key keeps -inf -> p = 0)
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float m0 = mn[2 * q], m1 = mn[2 * q + 1];
-            const bool ok0 = (vm >> (2 * q)) & 1u;
-            const bool ok1 = (vm >> (2 * q + 1)) & 1u;
-            const float x0 = ok0 ? __uint_as_float(sr[2 * q]) * scl - (m0 == -INFINITY ? 0.f : m0) : -INFINITY;
-            const float x1 = ok1 ? __uint_as_float(sr[2 * q + 1]) * scl - (m1 == -INFINITY ? 0.f : m1) : -INFINITY;
-            x2[q] = f2(x0, x1);
-          }
-        }
-        // P^T row of this key (bf16, MN-major SW128), columns [cb, cb + 32)
-        uint32_t pk[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          float a, b2;
-          uf2(x2[q], a, b2);
-          pk[q] = pack_bf16x2(ex2(a), ex2(b2));
-        }
-        const int pb = T % C::NP;
-        if (tid == 0) ev(p, 16, T);
-        if (T >= (uint32_t)C::NP) mbar_wait(smem_u32(&ms.pfree[pb]), ((T / C::NP) - 1) & 1);
-        if (tid == 0) ev(p, 17, T);
-        uint8_t* pbuf = smem + C::OFF_P + pb * 16384;
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch)
-          *(uint4*)(pbuf + mnmajor_off(cb + ch * 8, kl, 8, 16384, 1024)) =
-              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
         fence_async_smem();
         mbar_arrive(smem_u32(&ms.pfull[pb]));
         if (tid == 0) ev(p, 4, T);
@@ -1204,11 +1273,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         }
       }
       // ---- item end: the running max is final -> m of every partial entry now; the accumulators once the
-      // last PV completes (NONE: deferred past the next item's first tile, the PV pipe runs on meanwhile) ----
+      // last PV completes (NONE 64-row: deferred past the next item's first tile, the PV pipe runs on) ----
       if (kl == 64) {
 #pragma unroll 1
-        for (int i = 0; i < 32; ++i) {
-          const int c = cb + i, o = c >> 4, r = c & 15;
+        for (int i = 0; i < CPW; ++i) {
+          const int c = CPW * w + i, o = c >> 4, r = c & 15;
           if (o < I.n_slots && r < R.n_rows[o]) p.ws[(int64_t)(R.entry_off[o] + r) * p.entry_stride] = ms.m_run[c];
         }
       }
@@ -1233,25 +1302,28 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 
 }  // namespace
 
+template <bool kDef, int kRowsT>
+cudaError_t launch_tc_variant(const AttnParams& p, const void* maps, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(ra_tc_kernel<kDef, kRowsT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               Cfg<kDef, kRowsT>::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  ra_tc_kernel<kDef, kRowsT><<<p.n_ctas, 384, Cfg<kDef, kRowsT>::SMEM, s>>>(*(const TcMaps*)maps, p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStream_t s) {
   if (p.n_items == 0) return cudaSuccess;
   if (p.d != kD || p.r != kR || p.dtype != FKV_DTYPE_BF16 || (kTile % p.P) || p.P < 8 || p.n_ctas < 1 || !p.stage)
     return cudaErrorInvalidValue;
-  const bool def = p.rope_mode == FKV_ROPE_DEFERRED;
-  static bool attr[2] = {false, false};
-  if (!attr[def]) {
-    cudaError_t e = def ? cudaFuncSetAttribute(ra_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               Cfg<true>::SMEM)
-                        : cudaFuncSetAttribute(ra_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               Cfg<false>::SMEM);
-    if (e != cudaSuccess) return e;
-    attr[def] = true;
+  if (p.rope_mode == FKV_ROPE_DEFERRED) {
+    if (p.tc_rows != 64) return cudaErrorInvalidValue;
+    return launch_tc_variant<true, 64>(p, maps, s);
   }
-  if (def)
-    ra_tc_kernel<true><<<p.n_ctas, 384, Cfg<true>::SMEM, s>>>(*(const TcMaps*)maps, p);
-  else
-    ra_tc_kernel<false><<<p.n_ctas, 384, Cfg<false>::SMEM, s>>>(*(const TcMaps*)maps, p);
-  return cudaGetLastError();
+  return p.tc_rows == 128 ? launch_tc_variant<false, 128>(p, maps, s) : launch_tc_variant<false, 64>(p, maps, s);
 }
 
 cudaError_t launch_stage(const AttnParams& p, int32_t n_warps, cudaStream_t s) {

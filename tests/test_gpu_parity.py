@@ -66,10 +66,15 @@ def test_device_synth_matches_host_generator():
 
 
 @pytest.mark.parametrize("mode", ["deferred", "none"])
-@pytest.mark.parametrize("kernel", ["tc", "mma", "simt"])
-def test_c1_parity(mode, kernel):
+@pytest.mark.parametrize("kernel", ["tc", "tc128", "mma", "simt"])
+def test_c1_parity(mode, kernel, monkeypatch):
     """configs[0] (C1): 1 layer Llama-3.1-8B shape, r=16, 4 agents forked from a
     2K-token prefix + 128 private + 1 decode token; llama3 RoPE, theta 5e5."""
+    if kernel == "tc128":
+        if mode == "deferred":
+            pytest.skip("the 128-row variant is NONE only")
+        monkeypatch.setenv("FKV_TC_ROWS", "128")
+        kernel = "tc"
     scen = recipes.c1()
     fkv = _ctx(scen, 1, 32, 8, 128, 16, 64, "bf16", mode, theta=500000.0, llama3=True)
     driver.build(fkv, scen, seed=0)
@@ -80,13 +85,15 @@ def test_c1_parity(mode, kernel):
     assert err <= TOL["bf16"], err
 
 
-@pytest.mark.parametrize("mode", ["deferred", "none"])
+@pytest.mark.parametrize("mode,rows", [("deferred", 64), ("none", 64), ("none", 128)])
 @pytest.mark.parametrize("P", [16, 32, 64, 128])
-def test_tc_kernel_page_sizes_and_groups(mode, P):
+def test_tc_kernel_page_sizes_and_groups(mode, rows, P, monkeypatch):
     """tcgen05 kernel: page sizes 16/32/64 (TMA box = one page), owner groups
     with several slots (same-agent branches: 4 branches x g=4 rows = one slot;
     a chunked-prefill owner spanning several slots), key ranges ending inside
-    a page, and multi-tile split items."""
+    a page, and multi-tile split items; 64-row CTAs and (NONE) the 128-row
+    variant (8 slots, row sums reduced on the CUDA cores)."""
+    monkeypatch.setenv("FKV_TC_ROWS", str(rows))
     ag = [recipes.AgentSpec(100, 100, None, 0, False, 700, decode=False)]
     for i in range(3):
         ag.append(recipes.AgentSpec(1000 + i, i, 100, 700, False, 0, decode=False))
