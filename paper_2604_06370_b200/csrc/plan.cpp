@@ -17,6 +17,8 @@
 #include <array>
 #include <map>
 #include <set>
+#include <string>
+#include <unordered_map>
 
 #include "internal.hpp"
 #include "kernels.hpp"
@@ -250,12 +252,31 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
         pl.key_tiles += nt;
         order_key.push_back({ct.k0, pi, (int64_t)ci});
         // cost in KB of shared-memory ingest: base K + V tiles, R_k + R_v per slot, + per-item overhead
-        // per-item overhead (header staging, first-tile softmax setup, epilogue) measured at ~4 tiles
-        item_cost.push_back((nt + 4) * (64 + 8 * it.n_warps));
+        // per-item overhead (header staging, first-tile softmax setup, epilogue) measured at ~4-6 tiles
+        static const int64_t ovh = getenv("FKV_ITEM_OVERHEAD") ? atoll(getenv("FKV_ITEM_OVERHEAD")) : 5;
+        item_cost.push_back((nt + ovh) * (64 + 8 * it.n_warps));
       }
     }
   }
   if (pl.kernel == 2) {
+    // staged operand images (Q rows, q~ / packed B_k) per item slot; the key-range pieces of one row block carry
+    // identical slots, so they share one contiguous block of images (DevItem::pad_[0] = first image)
+    std::unordered_map<std::string, int32_t> img_of;
+    for (DevItem& it : pl.items) {
+      std::string key;
+      for (int o = 0; o < it.n_warps; ++o) {
+        const DevWarp& w = pl.warps[it.warp_off + o];
+        key.append((const char*)&w.adapter_slot, 4);
+        key.append((const char*)&w.n_rows, 4);
+        key.append((const char*)&pl.rows[w.row_off], sizeof(DevRow) * kRowsPerWarp);
+      }
+      auto f = img_of.find(key);
+      if (f == img_of.end()) {
+        f = img_of.emplace(key, (int32_t)pl.stage_src.size()).first;
+        for (int o = 0; o < it.n_warps; ++o) pl.stage_src.push_back(it.warp_off + o);
+      }
+      it.pad_[0] = f->second;
+    }
     // persistent schedule: items in (segment, piece, row block) order, each to the least-loaded CTA, so the
     // row blocks and kv heads that stream the same base / residual pages run at the same time (L2 reuse)
     const int32_t n_items = (int32_t)pl.items.size();
@@ -383,11 +404,12 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   pl.off_tptr = put(pl.blob, pl.tile_ptr);
   pl.off_trecs = put(pl.blob, pl.tile_recs);
   pl.off_irecs = put(pl.blob, pl.item_recs);
+  pl.off_ssrc = put(pl.blob, pl.stage_src);
   pl.blob.resize(align256(pl.blob.size()));
   pl.ws_bytes = align256((size_t)pl.n_entries * (size_t)(2 + d + r) * sizeof(float));
   if (pl.kernel == 2) {
     pl.stage_off = pl.ws_bytes;
-    pl.ws_bytes += align256(pl.warps.size() * (size_t)k::kStageBytes);
+    pl.ws_bytes += align256(pl.stage_src.size() * (size_t)k::kStageBytes);
   }
   return plan.release();
 }
@@ -447,10 +469,11 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.tile_recs = (const int4*)(base + p.off_trecs);
   a.item_recs = base + p.off_irecs;
   a.tc_rows = p.tc_rows;
+  a.stage_src = (const int32_t*)(base + p.off_ssrc);
   a.n_ctas = p.n_ctas;
   a.stage = p.kernel == 2 ? (uint8_t*)ws + p.stage_off : nullptr;
   cudaError_t e = cudaSuccess;
-  if ((phases & FKV_PHASE_MAIN) && p.kernel == 2) e = k::launch_stage(a, (int32_t)p.warps.size(), (cudaStream_t)stream);
+  if ((phases & FKV_PHASE_MAIN) && p.kernel == 2) e = k::launch_stage(a, (int32_t)p.stage_src.size(), (cudaStream_t)stream);
   if (e == cudaSuccess && (phases & FKV_PHASE_MAIN))
     e = p.kernel == 2   ? k::launch_attention_tc(a, c.tc_maps.data(), (cudaStream_t)stream)
         : p.kernel == 0 ? k::launch_attention_mma(a, (cudaStream_t)stream)

@@ -58,11 +58,11 @@ struct Cfg {
   static constexpr int ROWS = kRowsT, SLOTS = kRowsT / 16;
   static constexpr bool ONES = kRowsT == 64;    // A^T has a free slot for the all-ones rows (row sums l)
   // R_k (small) is single-buffered with its pages L2-prefetched two tiles ahead; V_base / R_v wait for softmax(T):
-  // a deeper ring; 64-row CTAs: P^T double-buffered so softmax(T+1) overlaps PV(T)
+  // a deeper ring; P^T in 64-key halves so softmax(T+1) overlaps PV(T)
   static constexpr int KS = kRowsT == 128 ? 1 : 2;  // K_base ring (32 KB: one 128-key tile, both d-halves)
   static constexpr int RS = 1;                      // R_k ring (4 KB per slot)
   static constexpr int VS = kRowsT == 128 ? 2 : 3;  // V-side ring (64-key half of V_base | R_v per slot | ones)
-  static constexpr int NP = kRowsT == 128 ? 1 : 2;  // P^T buffers
+  static constexpr int NPH = kRowsT == 128 ? 3 : 4;  // P^T ring of 64-key halves (PV of half h needs only it)
   static constexpr int NQ = (kDef || kRowsT == 128) ? 1 : 2;  // per-item Q / X buffers
   // Accumulator layout switches (both measured on B200): split accumulation chains (SH / PAR = 2) do not help, a
   // tcgen05.mma costs ~120 cycles for N <= 128 whether or not it depends on the previous one
@@ -75,7 +75,7 @@ struct Cfg {
   __host__ __device__ static constexpr uint32_t tA(int ab, int par) { return 3 * ROWS + 2 * ROWS * ab + 0 * par; }
   static constexpr uint32_t XB = kDef ? 4096 : 512;  // per-slot X image: packed B_k | q~
   static constexpr uint32_t QB = ROWS * 256;         // Q buffer: [2 d-halves][ROWS][128 B]
-  static constexpr uint32_t PB = ROWS * 256;         // P^T buffer: [ROWS / 64][128 keys / 8][8][64 cols x 2 B]
+  static constexpr uint32_t PHB = ROWS * 128;        // P^T half: [ROWS / 64 atoms][64 keys / 8][8][64 cols x 2 B]
   static constexpr uint32_t RB = SLOTS * 4096;       // R_k entry: [slot][128 keys][32 B]
   static constexpr uint32_t VE = 16384 + SLOTS * 2048 + (ONES ? 2048 : 0);
   static constexpr uint32_t OFF_V = 0;
@@ -83,7 +83,7 @@ struct Cfg {
   static constexpr uint32_t OFF_R = OFF_K + KS * 32768;
   static constexpr uint32_t OFF_Q = OFF_R + RS * RB;
   static constexpr uint32_t OFF_P = OFF_Q + NQ * QB;
-  static constexpr uint32_t OFF_X = OFF_P + NP * PB;  // [NQ][SLOTS][XB]
+  static constexpr uint32_t OFF_X = OFF_P + NPH * PHB;  // [NQ][SLOTS][XB]
   static constexpr uint32_t OFF_MISC = OFF_X + NQ * SLOTS * XB;
   static constexpr uint32_t MISCB = kRowsT == 128 ? 4096 : 1024;
   static constexpr uint32_t SMEM = OFF_MISC + MISCB;
@@ -92,9 +92,15 @@ struct Cfg {
 };
 
 template <class C>
+struct kDefOf;
+template <bool D, int R>
+struct kDefOf<Cfg<D, R>> {
+  static constexpr bool value = D;
+};
+template <class C>
 struct MiscT {
   uint64_t kfull[2], kempty[2], rfull[1], rempty[1], vfull[3], vempty[3], rvfull[3], qfull[2], qempty[2], sfull[2],
-      sfree[2], pfull[2], pfree[2], accfree[2], klfull[2][kKlBufs], klready[2][kKlBufs];
+      sfree[2], pfull[4], pfree[4], accfree[2], kl[kDefOf<C>::value ? 4 * kKlBufs : 1];  // kl: DEFERRED klfull | klready
   alignas(16) float m_run[C::ROWS];
   alignas(16) float lw[C::ONES ? 4 : 4 * C::ROWS];  // no all-ones slot: row-sum partials per key warp [4][ROWS]
   alignas(16) ItemRecT<C::SLOTS> rec[C::NQ];         // per-item header (staged with the item's Q rows)
@@ -312,12 +318,12 @@ __device__ __forceinline__ int perm_d(int n) {
 // memory images the main kernel bulk-copies: Q rows (K-major SW128, both
 // d-halves, 2 KB each) and q~ = Q B_k^T (NONE, K-major SW32, 512 B) or B_k^h
 // with permuted columns (DEFERRED, MN-major SW64 quarter blocks, 4 KB).
-__global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_warps) {
-  const int wi = blockIdx.x;
-  if (wi >= n_warps) return;
+__global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_images) {
+  const int ii = blockIdx.x;
+  if (ii >= n_images) return;
   __shared__ __align__(16) float qs[16][kD];
-  const DevWarp w = p.warps[wi];
-  uint8_t* img = p.stage + (int64_t)wi * kStageBytes;
+  const DevWarp w = p.warps[p.stage_src[ii]];
+  uint8_t* img = p.stage + (int64_t)ii * kStageBytes;
   const int tid = threadIdx.x;
   const DevItem* dummy = nullptr;
   (void)dummy;
@@ -406,15 +412,19 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       mbar_init(smem_u32(&ms.qempty[i]), 3);  // S-side commit + one arrive per key warpgroup
       mbar_init(smem_u32(&ms.sfull[i]), 1);
       mbar_init(smem_u32(&ms.sfree[i]), 256);
-      mbar_init(smem_u32(&ms.pfull[i]), 256);
+      mbar_init(smem_u32(&ms.pfull[i]), 128);  // the key threads of one 64-key half (both warpgroups)
       mbar_init(smem_u32(&ms.pfree[i]), 1);
+      mbar_init(smem_u32(&ms.pfull[2 + i]), 128);
+      mbar_init(smem_u32(&ms.pfree[2 + i]), 1);
     }
     mbar_init(smem_u32(&ms.accfree[0]), 256);
     mbar_init(smem_u32(&ms.accfree[1]), 256);
     for (int w = 0; w < 2; ++w)
       for (int b = 0; b < kKlBufs; ++b) {
-        mbar_init(smem_u32(&ms.klfull[w][b]), 1);
-        mbar_init(smem_u32(&ms.klready[w][b]), 128);
+        if (kDef) {
+          mbar_init(smem_u32(&ms.kl[w * kKlBufs + b]), 1);                 // klfull
+          mbar_init(smem_u32(&ms.kl[2 * kKlBufs + w * kKlBufs + b]), 128);  // klready
+        }
       }
     fence_mbar_init();
   }
@@ -516,7 +526,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             const uint8_t* rsrc = (const uint8_t*)(item_recs + qitem);
             if (lane < (int)(sizeof(ItemRec) / 16)) cp_async16(smem_u32(&ms.rec[qb]) + lane * 16, rsrc + lane * 16);
             for (int o = 0; o < qit.n_warps; ++o) {
-              const uint8_t* src = p.stage + (int64_t)(qit.warp_off + o) * kStageBytes;
+              const uint8_t* src = p.stage + (int64_t)(qit.pad_[0] + o) * kStageBytes;
 #pragma unroll
               for (int u = 0; u < 8; ++u) {  // Q image: 2 x 2 KB
                 const int c = lane + 32 * u;
@@ -635,7 +645,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             mbar_expect_tx(bar, it.n_warps * (4096 + C::XB) + (uint32_t)sizeof(ItemRec));
             bulk_g2s(smem_u32(&ms.rec[qb]), item_recs + p.sched_items[it_begin + iq], sizeof(ItemRec), bar);
             for (int o = 0; o < it.n_warps; ++o) {
-              const uint8_t* src = p.stage + (int64_t)(it.warp_off + o) * kStageBytes;
+              const uint8_t* src = p.stage + (int64_t)(it.pad_[0] + o) * kStageBytes;
               bulk_g2s(sbase + C::OFF_Q + qb * C::QB + o * 2048, src, 2048, bar);
               bulk_g2s(sbase + C::OFF_Q + qb * C::QB + C::QB / 2 + o * 2048, src + 2048, 2048, bar);
               bulk_g2s(sbase + C::OFF_X + qb * kSlots * C::XB + o * C::XB, src + 4096, C::XB, bar);
@@ -724,7 +734,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               const uint32_t b = (U + k) % kKlBufs;
               mma_ss_e(tm + T_KL + 128 * w + 32 * b, dr + (uint64_t)(o * 256),
                        dx + (uint64_t)((o * 4096 + (2 * w + q) * 1024) >> 4), id_rb, 0);
-              mma_commit_e(smem_u32(&ms.klfull[w][b]));
+              mma_commit_e(smem_u32(&ms.kl[w * kKlBufs + b]));
               if (T == 4) ev(p, 15, 32 * w + k);
             };
             auto ts = [&](int w, int k) {  // S^T[:, rows of g] += RoPE(KL)[bf16, in place] Q_g^T over the unit's 32 d
@@ -732,7 +742,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               const uint32_t o = (uint32_t)(gf >> (8 * g)) & 0xff, cnt = (uint32_t)(gc >> (8 * g)) & 0xff;
               const uint32_t Uk = U + k, b = Uk % kKlBufs;
               if (T == 4) ev(p, 11, 32 * w + k);
-              mbar_wait(smem_u32(&ms.klready[w][b]), (Uk / kKlBufs) & 1);
+              mbar_wait(smem_u32(&ms.kl[2 * kKlBufs + w * kKlBufs + b]), (Uk / kKlBufs) & 1);
               if (T == 4) ev(p, 12, 32 * w + k);
               tc_fence_after();
               const uint32_t id = idesc_bf16(128, 16 * cnt, false, false);
@@ -772,13 +782,14 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         mbar_wait(smem_u32(&ms.qfull[qb]), (ii / C::NQ) & 1);
         const int n_tiles = ms.rec[qb].n_tiles;
         for (int j = 0; j < n_tiles; ++j, ++T) {
-          const int pb = T % C::NP;
-          mbar_wait(smem_u32(&ms.pfull[pb]), (T / C::NP) & 1);
-          ev(p, 5, T);
           const int ab = ii % C::AB;
           if (j == 0 && ii >= C::AB) mbar_wait(smem_u32(&ms.accfree[ab]), ((ii / C::AB) - 1) & 1);
-          const uint64_t dp = make_desc(sbase + C::OFF_P + pb * C::PB, 16384, 1024, SWZ_128);
           for (int kh = 0; kh < 2; ++kh, ++nv) {
+            // P^T half kh of tile T = ring entry nv (the V-side entries run in the same order)
+            const int ps = nv % C::NPH;
+            mbar_wait(smem_u32(&ms.pfull[ps]), (nv / C::NPH) & 1);
+            if (kh == 0) ev(p, 5, T);
+            const uint64_t dp = make_desc(sbase + C::OFF_P + ps * C::PHB, 8192, 1024, SWZ_128);
             mbar_wait(smem_u32(&ms.vfull[nv % C::VS]), (nv / C::VS) & 1);
             mbar_wait(smem_u32(&ms.rvfull[nv % C::VS]), (nv / C::VS) & 1);
             ev(p, 6, nv);
@@ -788,14 +799,14 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
               const int ck = 4 * kh + s, par = ck % C::PAR;  // NONE: two chains per accumulator (key-chunk parity)
-              const uint64_t bd = dp + (uint64_t)((ck * 2048) >> 4);
+              const uint64_t bd = dp + (uint64_t)((s * 2048) >> 4);
               const uint32_t acc = (j > 0 || ck >= C::PAR);
               mma_ss_e(tm + C::tO(ab, par), dv + (uint64_t)((s * 2048) >> 4), bd, id_pv, acc);
               mma_ss_e(tm + C::tA(ab, par), da + (uint64_t)((s * 512) >> 4), bd, id_pv, acc);
             }
             mma_commit_e(smem_u32(&ms.vempty[nv % C::VS]));
+            mma_commit_e(smem_u32(&ms.pfree[ps]));
           }
-          mma_commit_e(smem_u32(&ms.pfree[pb]));
           ev(p, 18, T);
         }
       }
@@ -949,7 +960,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
     auto epilogue = [&](int ie, uint32_t Tl, int qbe) {
       const ItemRec& Re = ms.rec[qbe];
       const int ab = ie % C::AB, ns = Re.meta & 15;
-      mbar_wait(smem_u32(&ms.pfree[Tl % C::NP]), (Tl / C::NP) & 1);
+      for (uint32_t np = 2 * Tl; np < 2 * Tl + 2; ++np) mbar_wait(smem_u32(&ms.pfree[np % C::NPH]), (np / C::NPH) & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int ch = 0; ch < NCH; ++ch) {
@@ -1047,7 +1058,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             for (int g = 0; g < I.n_groups; ++g) {
               uint32_t x[16], y[16], lh[16];
               const uint32_t b = U % kKlBufs;
-              mbar_wait(smem_u32(&ms.klfull[w][b]), (U / kKlBufs) & 1);
+              mbar_wait(smem_u32(&ms.kl[w * kKlBufs + b]), (U / kKlBufs) & 1);
               if (T == 4 && kl == 0) ev(p, 13, 32 * w + q * I.n_groups + g);
               tc_fence_after();
               const uint32_t kt = tm + T_KL + 128 * w + 32 * b + lb;
@@ -1064,15 +1075,16 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               FKV_TMEM_ST16(kt, lh);
               tmem_st_wait();
               tc_fence_before();
-              mbar_arrive(smem_u32(&ms.klready[w][b]));
+              mbar_arrive(smem_u32(&ms.kl[2 * kKlBufs + w * kKlBufs + b]));
               if (T == 4 && kl == 0) ev(p, 14, 32 * w + q * I.n_groups + g);
               ++U;
             }
           }
         }
         const int sb = T & 1;
-        const int pb = T % C::NP;
-        uint8_t* pbuf = smem + C::OFF_P + pb * C::PB;
+        // this thread's P^T half (keys 0..63 | 64..127) = ring entry 2T + half
+        const uint32_t np = 2 * T + (kl >> 6), ps = np % C::NPH;
+        uint8_t* pbuf = smem + C::OFF_P + ps * C::PHB;
 #pragma unroll 1
         for (int ch = 0; ch < NCH; ++ch) {
           // ---- online softmax over the chunk's 32 query columns (Alg1.339-341) ----
@@ -1195,7 +1207,8 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             }
             if (resc && j > 0) {
               // rescale the chunk's columns of O^T and A^T by alpha (all PV up to tile T-1 complete)
-              mbar_wait(smem_u32(&ms.pfree[(T - 1) % C::NP]), ((T - 1) / C::NP) & 1);
+              for (uint32_t q2 = 2 * (T - 1); q2 < 2 * T; ++q2)
+                mbar_wait(smem_u32(&ms.pfree[q2 % C::NPH]), (q2 / C::NPH) & 1);
               tc_fence_after();
 #pragma unroll
               for (int part = 0; part < 2; ++part) {
@@ -1233,12 +1246,12 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
           if (ch == 0) {
             if (tid == 0) ev(p, 16, T);
-            if (T >= (uint32_t)C::NP) mbar_wait(smem_u32(&ms.pfree[pb]), ((T / C::NP) - 1) & 1);
+            if (np >= (uint32_t)C::NPH) mbar_wait(smem_u32(&ms.pfree[ps]), ((np / C::NPH) - 1) & 1);
             if (tid == 0) ev(p, 17, T);
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            *(uint4*)(pbuf + mnmajor_off(cb + q * 8, kl, 8, 16384, 1024)) =
+            *(uint4*)(pbuf + mnmajor_off(cb + q * 8, kl & 63, 8, 8192, 1024)) =
                 make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
           if constexpr (!C::ONES) {
             // row sums l without an all-ones MMA slot: the warp's 32 keys summed per column (of the bf16 P the
@@ -1265,7 +1278,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
         }
         fence_async_smem();
-        mbar_arrive(smem_u32(&ms.pfull[pb]));
+        mbar_arrive(smem_u32(&ms.pfull[ps]));
         if (tid == 0) ev(p, 4, T);
         if (C::AB > 1 && j == 0 && pend_ii >= 0) {
           epilogue(pend_ii, pend_Tl, pend_qb);
@@ -1326,9 +1339,9 @@ cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStrea
   return p.tc_rows == 128 ? launch_tc_variant<false, 128>(p, maps, s) : launch_tc_variant<false, 64>(p, maps, s);
 }
 
-cudaError_t launch_stage(const AttnParams& p, int32_t n_warps, cudaStream_t s) {
-  if (n_warps <= 0) return cudaSuccess;
-  ra_stage_kernel<<<n_warps, 128, 0, s>>>(p, n_warps);
+cudaError_t launch_stage(const AttnParams& p, int32_t n_images, cudaStream_t s) {
+  if (n_images <= 0) return cudaSuccess;
+  ra_stage_kernel<<<n_images, 128, 0, s>>>(p, n_images);
   return cudaGetLastError();
 }
 
