@@ -148,6 +148,7 @@ __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p, int6
 
 template <typename T>
 __global__ void combine_kernel(AttnParams p) {
+  // one warp per output row: merge the split partials (m, l, acc, acc_r) and apply the late V fusion (Eq.4)
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= p.n_out_rows) return;
@@ -157,29 +158,50 @@ __global__ void combine_kernel(AttnParams p) {
   const int slot = p.seqs[seq].adapter_slot;
   const int e0 = p.out_ptr[warp], e1 = p.out_ptr[warp + 1];
   const int d = p.d, r = p.r;
-  float M = -INFINITY;
-  for (int e = e0; e < e1; ++e) {
-    const float* ent = p.ws + (int64_t)p.out_entries[e] * p.entry_stride;
-    if (ent[1] > 0.f) M = fmaxf(M, ent[0]);
-  }
   constexpr int kMaxD = 256 / 32;
   float acc[kMaxD];
 #pragma unroll
   for (int c = 0; c < kMaxD; ++c) acc[c] = 0.f;
   float accr0 = 0.f, accr1 = 0.f, l = 0.f;
-  for (int e = e0; e < e1; ++e) {
-    const float* ent = p.ws + (int64_t)p.out_entries[e] * p.entry_stride;
-    if (!(ent[1] > 0.f)) continue;
-    const float w = exp2f(ent[0] - M);
-    l += w * ent[1];
+  float Mrun = -INFINITY;
+  for (int eb = e0; eb < e1; eb += 32) {
+    // up to 32 entries at once: lane i reads entry eb + i's (m, l); weights 2^(m_i - M) (entries with l > 0 only)
+    const int ne = min(32, e1 - eb);
+    const float* my = lane < ne ? p.ws + (int64_t)p.out_entries[eb + lane] * p.entry_stride : nullptr;
+    const float mi = my ? my[0] : -INFINITY, li = my ? my[1] : 0.f;
+    const bool ok = li > 0.f;
+    float M = ok ? mi : -INFINITY;
 #pragma unroll
-    for (int c = 0; c < kMaxD; ++c)
-      if (lane + 32 * c < d) acc[c] += w * ent[2 + lane + 32 * c];
-    if (lane < r) accr0 += w * ent[2 + d + lane];
-    if (lane + 32 < r) accr1 += w * ent[2 + d + lane + 32];
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    M = fmaxf(M, Mrun);
+    if (Mrun != -INFINITY && M != Mrun) {  // more than 32 entries: rescale the earlier batches
+      const float sc = exp2f(Mrun - M);
+      l *= sc; accr0 *= sc; accr1 *= sc;
+#pragma unroll
+      for (int c = 0; c < kMaxD; ++c) acc[c] *= sc;
+    }
+    Mrun = M;
+    const float wi = ok ? exp2f(mi - M) : 0.f;
+    float lsum = wi * li;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    l += lsum;
+#pragma unroll 4
+    for (int i = 0; i < ne; ++i) {
+      const float w = __shfl_sync(0xffffffffu, wi, i);
+      const float* ent = p.ws + (int64_t)p.out_entries[eb + i] * p.entry_stride;
+      if (w != 0.f) {
+#pragma unroll
+        for (int c = 0; c < kMaxD; ++c)
+          if (lane + 32 * c < d) acc[c] += w * ent[2 + lane + 32 * c];
+        if (lane < r) accr0 += w * ent[2 + d + lane];
+        if (lane + 32 < r) accr1 += w * ent[2 + d + lane + 32];
+      }
+    }
   }
   // late fusion: O = (acc + acc_r . B_v^h) / l   (Alg1.349-350)
   const T* bv = (const T*)p.adapters[2 * slot + 1] + (int64_t)p.layer * p.adapter_layer_stride + (int64_t)h * r * d;
+#pragma unroll 8
   for (int j = 0; j < r; ++j) {
     const float a = __shfl_sync(0xffffffffu, j < 32 ? accr0 : accr1, j & 31);
 #pragma unroll

@@ -360,18 +360,25 @@ __global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_image
       *(uint4*)(img + 4096 + mnmajor_off(n8, jj, 4, 1024, 512)) = v;
     }
   } else {
+    // q~[row][j] = sum_d Q[row][d] B_k[j][d]: B_k^h (4 KB) through shared memory, 2 outputs per thread
+    __shared__ __align__(16) float bs[kR][kD + 4];
+    for (int c = tid; c < kR * kD / 8; c += 128) {
+      const int jj = c >> 4, d8 = (c & 15) * 8;
+      const uint4 bv = __ldg((const uint4*)(Bk + jj * kD + d8));
+      const __nv_bfloat162* b2 = (const __nv_bfloat162*)&bv;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 b = __bfloat1622float2(b2[e]);
+        bs[jj][d8 + 2 * e] = b.x;
+        bs[jj][d8 + 2 * e + 1] = b.y;
+      }
+    }
+    __syncthreads();
     for (int c = tid; c < 16 * kR; c += 128) {
       const int row = c >> 4, jj = c & 15;
       float acc = 0.f;
-      for (int d8 = 0; d8 < kD; d8 += 8) {
-        const uint4 bv = __ldg((const uint4*)(Bk + jj * kD + d8));
-        const __nv_bfloat162* b2 = (const __nv_bfloat162*)&bv;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 b = __bfloat1622float2(b2[e]);
-          acc += qs[row][d8 + 2 * e] * b.x + qs[row][d8 + 2 * e + 1] * b.y;
-        }
-      }
+#pragma unroll 8
+      for (int dd = 0; dd < kD; ++dd) acc += qs[row][dd] * bs[jj][dd];
       *(__nv_bfloat16*)(img + 4096 + kmajor_off(row, jj, 2, 256, 0)) = __float2bfloat16_rn(row < w.n_rows ? acc : 0.f);
     }
   }
