@@ -209,3 +209,23 @@ def test_kv_head_shard_parity(mode):
     err, pl = _run_and_check(fkv, scen, 21, 0, "bf16", mode, h0=4)
     assert pl.info.kernel == 2
     assert err <= TOL["bf16"], err
+
+
+@pytest.mark.parametrize("mode", ["none", "deferred"])
+def test_many_splits_combine(mode, monkeypatch):
+    """One-tile key-range pieces (FKV_PIECE_TILES=1) over a ~5K-key shared prefix: every output row merges
+    ~40 split partials, which exercises the combine kernel's multi-batch (> 32 entries) path and items that
+    share their staged Q / q~ images."""
+    monkeypatch.setenv("FKV_PIECE_TILES", "1")
+    ag = [recipes.AgentSpec(100, 100, None, 0, False, 5000, decode=False)]
+    for i in range(2):
+        ag.append(recipes.AgentSpec(1000 + i, i, 100, 5000, False, 0, decode=False))
+        for b in range(2):
+            ag.append(recipes.AgentSpec(10 * i + b, i, 1000 + i, 5000, True, 40 + 9 * b))
+    scen = recipes.Scenario("manysplits", ag, q_len=1)
+    fkv = _ctx(scen, 1, 32, 8, 128, 16, 128, "bf16", mode)
+    driver.build(fkv, scen, seed=5)
+    err, pl = _run_and_check(fkv, scen, 5, 0, "bf16", mode)
+    assert pl.info.kernel == 2
+    assert pl.info.n_items > 8 * 40, pl.info.n_items
+    assert err <= TOL["bf16"], err
