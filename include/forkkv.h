@@ -95,6 +95,12 @@ typedef struct fkv_config {
 /* Device pools (caller-owned), element type = config.dtype.
  *   base_k, base_v : [L][n_base_pages][Hkv_local][P][d]   (K post-RoPE)
  *   res_k,  res_v  : [L][n_res_pages][P][r]                (no RoPE)
+ *                    bf16 with r = 16: row i of a page stores element j at column
+ *                    j ^ (8 * ((i >> 2) & 1)) (the tcgen05 32-byte-swizzled operand
+ *                    order). The pools are written only through
+ *                    fkv_write_kv and are otherwise opaque to the caller.
+ *   Pools must hold finite values (e.g. zero-initialised): tiles are read whole and
+ *   rows beyond a sequence's length are masked after the products, not skipped.
  *   rope_cos, rope_sin : fp32 [max_pos][d/2], built host-side in fp64
  *                        (fkv_build_rope_table) — reading C-2, SURVEY H7. */
 typedef struct fkv_buffers {

@@ -4,10 +4,10 @@
 // share a base-page segment.
 //
 // Persistent kernel: one CTA per SM walks its list of plan items (kv head h,
-// key range [k0, k1) of a shared segment, up to 4 "slots" of 16 query rows; a
+// key range [k0, k1) of a shared segment, up to 4 (8) "slots" of 16 query rows; a
 // slot belongs to one residual owner = adapter + residual pages; consecutive
 // slots of one owner form a group).  Keys sit on the TMEM lanes (M = 128 keys
-// per tile), the item's 64 query rows on N, so every per-owner residual term
+// per tile), the item's 64 (128) query rows on N, so every per-owner residual term
 // is an N-slice of the same accumulator:
 //
 //   Stage 1 (Alg1.332-336)  S^T  = K_base Q^T                          [SS]
@@ -25,15 +25,16 @@
 //                           accumulates the row sums l)                 [SS]
 //   Stage 3 (Alg1.348-350)  combine kernel (late V fusion, Eq.4).
 //
-// 12 warps: warp 8 = TMA producer (K-side ring of 16 KB slabs: K_base d-half
-// 0/1 and R_k of the item's groups; V-side ring of 64-key halves: V_base +
-// R_v + ones; per-item Q / q~ / packed-B_k images), warp 9 = S-side MMA
-// issuer, warp 10 = PV-side MMA issuer, warp 11 = TMEM allocator (the
-// control warps have the high warp ids, which win the issue arbiter), warps
-// 0..7 = key warps (thread = TMEM lane = key of the tile; key warpgroup w owns query
-// columns [32w, 32w+32) and, in DEFERRED, the d-half w of the rotation).
-// S^T is double-buffered in TMEM so S(j+1) overlaps softmax(j); P^T is
-// double-buffered in smem so PV(j) overlaps softmax(j+1).
+// 12 warps (control warps have the high ids, which win the issue arbiter):
+//   warp 8  producer: K_base tiles (TMA, one 3D box per tile), R_k pages and the per-item header / Q / X images
+//           (16-byte cp.async by all lanes), page ids from the plan's tile records;
+//   warp 9  S-side MMA issuer, warp 10 PV-side MMA issuer (whole warps, one elected lane per instruction);
+//   warp 11 TMEM allocator, then the V-side loader: V_base 64-key halves (TMA) + R_v pages (cp.async);
+//   warps 0..7 key warps: thread = TMEM lane = key of the tile; key warpgroup w owns query columns
+//           [rows/2 w, rows/2 (w+1)) (chunks of 32) and, in DEFERRED, the d-half w of the K_lora rotation.
+// S^T is double-buffered in TMEM so S(j+1) overlaps softmax(j); P^T is a ring of 64-key halves so PV(j)
+// overlaps softmax(j+1).  Template parameters: mode (NONE / DEFERRED) and query rows per CTA (64, or 128 for
+// NONE with 8 slots and CUDA-core row sums).  DESIGN.md §4 has the measured cost model.
 #include <cuda_bf16.h>
 
 #include <cstddef>
