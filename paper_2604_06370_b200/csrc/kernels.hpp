@@ -40,7 +40,9 @@ cudaError_t launch_cow_copy(const PoolView& pv, const CopyOp* ops, int32_t n_ops
 // S = slots (16 query rows each): 4 (64-row CTAs, 176 B) or 8 (128-row CTAs, 336 B).
 template <int S>
 struct ItemRecT {
-  int32_t k0, k1, n_tiles, meta;  // meta = n_slots | n_groups << 4 | group-first slot mask << 8 | kv head << 16
+  // n_tiles: bits 0..15 tiles, bit 16 + g: 32-column chunk g has a causally masked query column;
+  // meta = n_slots | n_groups << 4 | group-first slot mask << 8 | kv head << 16
+  int32_t k0, k1, n_tiles, meta;
   int32_t n_rows[S];              // query rows of each slot
   int32_t entry_off[S];           // first partial entry of each slot
   uint16_t pos1[16 * S];          // per query column: position - k0 + 1 (key t visible iff t - k0 < pos1), 0 = none
@@ -94,6 +96,8 @@ struct AttnParams {
   uint8_t* stage;  // per-warp-slot staged operand images (ws region, kStageBytes each)
   int32_t res_swz;  // residual rows stored in SW32 order (see res_col)
 };
+// partial entry: [m, l, pad, pad, acc[D], acc_r[r]] (acc 16-byte aligned: vector stores / loads)
+constexpr int kEntAcc = 4;
 constexpr int kStageBytes = 8192;
 
 // Residual page format (bf16, r = 16): row i of a page holds R[i][j] at column j ^ (8 * ((i >> 2) & 1)), i.e.

@@ -193,9 +193,9 @@ __global__ void combine_kernel(AttnParams p) {
       if (w != 0.f) {
 #pragma unroll
         for (int c = 0; c < kMaxD; ++c)
-          if (lane + 32 * c < d) acc[c] += w * ent[2 + lane + 32 * c];
-        if (lane < r) accr0 += w * ent[2 + d + lane];
-        if (lane + 32 < r) accr1 += w * ent[2 + d + lane + 32];
+          if (lane + 32 * c < d) acc[c] += w * ent[kEntAcc + lane + 32 * c];
+        if (lane < r) accr0 += w * ent[kEntAcc + d + lane];
+        if (lane + 32 < r) accr1 += w * ent[kEntAcc + d + lane + 32];
       }
     }
   }
@@ -356,9 +356,9 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnParams p) {
     const float mi = __shfl_sync(0xffffffffu, m, i), li = __shfl_sync(0xffffffffu, l, i);
     if (lane == 0) { ent[0] = mi; ent[1] = li; }
 #pragma unroll
-    for (int c = 0; c < NC; ++c) ent[2 + lane + 32 * c] = acc[i][c];
-    if (lane < r) ent[2 + D + lane] = accr[i][0];
-    if (lane + 32 < r) ent[2 + D + lane + 32] = accr[i][1];
+    for (int c = 0; c < NC; ++c) ent[kEntAcc + lane + 32 * c] = acc[i][c];
+    if (lane < r) ent[kEntAcc + D + lane] = accr[i][0];
+    if (lane + 32 < r) ent[kEntAcc + D + lane + 32] = accr[i][1];
   }
 }
 

@@ -324,6 +324,11 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
           }
         }
         r.meta = it.n_warps | (ng << 4) | (gmask << 8) | (it.kv_head << 16);
+        // bits 16..: per 32-column chunk, some real query column does not see every key of the item (causal masking;
+        // the kernel masks unused columns from n_rows)
+        for (int o = 0; o < it.n_warps; ++o)
+          for (int j = 0; j < r.n_rows[o]; ++j)
+            if ((int64_t)r.pos1[16 * o + j] < (int64_t)it.key_end - it.key_begin) r.n_tiles |= 1 << (16 + (16 * o + j) / 32);
         std::memcpy(pl.item_recs.data() + i * sizeof(Rec), &r, sizeof(r));
       }
     };
@@ -406,7 +411,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   pl.off_irecs = put(pl.blob, pl.item_recs);
   pl.off_ssrc = put(pl.blob, pl.stage_src);
   pl.blob.resize(align256(pl.blob.size()));
-  pl.ws_bytes = align256((size_t)pl.n_entries * (size_t)(2 + d + r) * sizeof(float));
+  pl.ws_bytes = align256((size_t)pl.n_entries * (size_t)(k::kEntAcc + d + r) * sizeof(float));
   if (pl.kernel == 2) {
     pl.stage_off = pl.ws_bytes;
     pl.ws_bytes += align256(pl.stage_src.size() * (size_t)k::kStageBytes);
@@ -455,7 +460,7 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.d = (int32_t)d; a.r = (int32_t)r; a.rope_mode = c.cfg.rope_mode; a.dtype = c.cfg.dtype;
   a.n_items = (int32_t)p.items.size();
   a.n_out_rows = (int32_t)(p.n_rows_q * c.hq_local);
-  a.entry_stride = (int32_t)(2 + d + r);
+  a.entry_stride = (int32_t)(k::kEntAcc + d + r);
   if (scale <= 0.f) scale = 1.0f / std::sqrt((float)d);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.dbg = (long long*)c.dbg;

@@ -377,13 +377,13 @@ __global__ void __launch_bounds__(kThreads, 1) ra_mma_kernel(AttnParams p) {
     }
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) {
-      ent[2 + nt * 8 + cq] = o_acc[nt][half * 2];
-      ent[2 + nt * 8 + cq + 1] = o_acc[nt][half * 2 + 1];
+      ent[kEntAcc + nt * 8 + cq] = o_acc[nt][half * 2];
+      ent[kEntAcc + nt * 8 + cq + 1] = o_acc[nt][half * 2 + 1];
     }
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      ent[2 + kD + nt * 8 + cq] = r_acc[nt][half * 2];
-      ent[2 + kD + nt * 8 + cq + 1] = r_acc[nt][half * 2 + 1];
+      ent[kEntAcc + kD + nt * 8 + cq] = r_acc[nt][half * 2];
+      ent[kEntAcc + kD + nt * 8 + cq + 1] = r_acc[nt][half * 2 + 1];
     }
   }
 }

@@ -57,14 +57,18 @@ constexpr uint32_t T_KL = 256;
 template <bool kDef, int kRowsT>
 struct Cfg {
   static constexpr int ROWS = kRowsT, SLOTS = kRowsT / 16;
-  static constexpr bool ONES = kRowsT == 64;    // A^T has a free slot for the all-ones rows (row sums l)
+  // NONE, 64 rows: PV as O_ext = P [V | R_v of the 4 slots] with the query rows on the TMEM lanes: 8 MMA
+  // instructions of N = 192 per tile instead of 16 (O^T and A^T separately); row sums on the CUDA cores
+  static constexpr bool PVROW = !kDef && kRowsT == 64;
+  static constexpr bool ONES = kRowsT == 64 && !PVROW;  // A^T has a free slot for the all-ones rows (row sums l)
   // R_k (small) is single-buffered with its pages L2-prefetched two tiles ahead; V_base / R_v wait for softmax(T):
   // a deeper ring; P^T in 64-key halves so softmax(T+1) overlaps PV(T)
   static constexpr int KS = kRowsT == 128 ? 1 : 2;  // K_base ring (32 KB: one 128-key tile, both d-halves)
   static constexpr int RS = 1;                      // R_k ring (4 KB per slot)
   static constexpr int VS = kRowsT == 128 ? 2 : 3;  // V-side ring (64-key half of V_base | R_v per slot | ones)
   static constexpr int NPH = kRowsT == 128 ? 3 : 4;  // P^T ring of 64-key halves (PV of half h needs only it)
-  static constexpr int NQ = (kDef || kRowsT == 128) ? 1 : 2;  // per-item Q / X buffers
+  static constexpr int NQ = (kDef || kRowsT == 128) ? 1 : 2;  // per-item Q / X buffers (freed by the S-side MMAs)
+  static constexpr int NRC = 4;  // per-item header ring (held by the key warps until the item's epilogue)
   // Accumulator layout switches (both measured on B200): split accumulation chains (SH / PAR = 2) do not help, a
   // tcgen05.mma costs ~120 cycles for N <= 128 whether or not it depends on the previous one
   // (tools/ubench_mma.cu); double-buffered O^T / A^T (AB = 2) overlap an item's epilogue with the next item.
@@ -78,7 +82,10 @@ struct Cfg {
   static constexpr uint32_t QB = ROWS * 256;         // Q buffer: [2 d-halves][ROWS][128 B]
   static constexpr uint32_t PHB = ROWS * 128;        // P^T half: [ROWS / 64 atoms][64 keys / 8][8][64 cols x 2 B]
   static constexpr uint32_t RB = SLOTS * 4096;       // R_k entry: [slot][128 keys][32 B]
-  static constexpr uint32_t VE = 16384 + SLOTS * 2048 + (ONES ? 2048 : 0);
+  // V-side entry: PVROW: [V d-half 0 | V d-half 1 | R_v 4 slots interleaved per key] as three SW128 MN-major atoms
+  // of 64 columns (8 KB each); otherwise [V half 16 KB | R_v per slot 2 KB | ones 2 KB]
+  static constexpr uint32_t VE = PVROW ? 24576 : 16384 + SLOTS * 2048 + (ONES ? 2048 : 0);
+  __host__ __device__ static constexpr uint32_t tOX(int ab) { return 128 + 192 * ab; }  // PVROW: O_ext [64 rows][192]
   static constexpr uint32_t OFF_V = 0;
   static constexpr uint32_t OFF_K = OFF_V + VS * VE;
   static constexpr uint32_t OFF_R = OFF_K + KS * 32768;
@@ -86,7 +93,7 @@ struct Cfg {
   static constexpr uint32_t OFF_P = OFF_Q + NQ * QB;
   static constexpr uint32_t OFF_X = OFF_P + NPH * PHB;  // [NQ][SLOTS][XB]
   static constexpr uint32_t OFF_MISC = OFF_X + NQ * SLOTS * XB;
-  static constexpr uint32_t MISCB = kRowsT == 128 ? 4096 : 1024;
+  static constexpr uint32_t MISCB = kRowsT == 128 ? 5120 : (PVROW ? 4096 : 2048);
   static constexpr uint32_t SMEM = OFF_MISC + MISCB;
   static_assert(SMEM <= 232448, "shared memory");
   static_assert(!(kDef && kRowsT != 64), "DEFERRED runs 64-row CTAs");
@@ -101,10 +108,11 @@ struct kDefOf<Cfg<D, R>> {
 template <class C>
 struct MiscT {
   uint64_t kfull[2], kempty[2], rfull[1], rempty[1], vfull[3], vempty[3], rvfull[3], qfull[2], qempty[2], sfull[2],
-      sfree[2], pfull[4], pfree[4], accfree[2], kl[kDefOf<C>::value ? 4 * kKlBufs : 1];  // kl: DEFERRED klfull | klready
-  alignas(16) float m_run[C::ROWS];
-  alignas(16) float lw[C::ONES ? 4 : 4 * C::ROWS];  // no all-ones slot: row-sum partials per key warp [4][ROWS]
-  alignas(16) ItemRecT<C::SLOTS> rec[C::NQ];         // per-item header (staged with the item's Q rows)
+      sfree[2], pfull[4], pfree[4], accfree[2], recfull[C::NRC], recempty[C::NRC], kl[kDefOf<C>::value ? 4 * kKlBufs : 1];  // kl: DEFERRED klfull | klready
+  // running column max (PVROW: two buffers by item parity, reset by the item's end, so items start barrier-free)
+  alignas(16) float m_run[(C::PVROW ? 2 : 1) * C::ROWS];
+  alignas(16) float lw[C::ONES ? 4 : (C::PVROW ? 2 : 1) * 4 * C::ROWS];  // row-sum partials per key warp [4][ROWS]
+  alignas(16) ItemRecT<C::SLOTS> rec[C::NRC];        // per-item header ring
   uint32_t tmem_base;
 };
 
@@ -163,7 +171,7 @@ template <class Rec>
 __device__ __forceinline__ void item_from_rec(const Rec& r, ItemInfo& I) {
   I.k0 = r.k0;
   I.k1 = r.k1;
-  I.n_tiles = r.n_tiles;
+  I.n_tiles = r.n_tiles & 0xffff;
   I.n_slots = r.meta & 15;
   int ng = 0;
   for (int o = 0; o < I.n_slots; ++o) {
@@ -303,6 +311,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 
 // diagnostics: clock64 stamp of pipeline event e for index j (< 256) of CTA dbg_block (fkv_debug_timeline)
+// (EV: the kernel-uniform dbg_on test first, so the stamps cost one predicated branch when off)
+#define EV(e, j)                 \
+  do {                           \
+    if (dbg_on) ev(p, e, j);     \
+  } while (0)
 __device__ __forceinline__ void ev(const AttnParams& p, int e, uint32_t j) {
   if (p.dbg && (int)blockIdx.x == p.dbg_block && j < 256) p.dbg[e * 256 + j] = clock64();
 }
@@ -401,6 +414,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
   if (sbase & 1023) __trap();
   const long long t_start = clock64();
   const int cta = blockIdx.x;
+  const bool dbg_on = p.dbg != nullptr && cta == p.dbg_block;
   const int it_begin = p.sched_ptr[cta], it_end = p.sched_ptr[cta + 1];
   const int n_my = it_end - it_begin;
   const int P = p.P;
@@ -417,13 +431,17 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&ms.qfull[i]), p.P == kTile ? 32 : 1);  // fast path: one cp.async arrive per lane
-      mbar_init(smem_u32(&ms.qempty[i]), 3);  // S-side commit + one arrive per key warpgroup
+      mbar_init(smem_u32(&ms.qempty[i]), 1);  // S-side commit (the last MMA reading Q / X)
       mbar_init(smem_u32(&ms.sfull[i]), 1);
       mbar_init(smem_u32(&ms.sfree[i]), 256);
       mbar_init(smem_u32(&ms.pfull[i]), 128);  // the key threads of one 64-key half (both warpgroups)
       mbar_init(smem_u32(&ms.pfree[i]), 1);
       mbar_init(smem_u32(&ms.pfull[2 + i]), 128);
       mbar_init(smem_u32(&ms.pfree[2 + i]), 1);
+    }
+    for (int i = 0; i < C::NRC; ++i) {
+      mbar_init(smem_u32(&ms.recfull[i]), p.P == kTile ? 32 : 1);
+      mbar_init(smem_u32(&ms.recempty[i]), 2);  // one arrive per key warpgroup after the item's epilogue
     }
     mbar_init(smem_u32(&ms.accfree[0]), 256);
     mbar_init(smem_u32(&ms.accfree[1]), 256);
@@ -437,6 +455,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
     fence_mbar_init();
   }
   if (wid == 11) tmem_alloc(smem_u32(&ms.tmem_base), 512);
+  for (int c = tid; c < (C::PVROW ? 2 : 1) * C::ROWS; c += 384) ms.m_run[c] = -INFINITY;
   // the all-ones R_v slot (index 4) of every V-side entry: A^T lanes 64..79 accumulate the row sums l
   if (C::ONES)
     for (int c = tid; c < C::VS * 128; c += 384)
@@ -475,7 +494,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       constexpr int kPf = 2;  // L2 prefetch distance (tiles) of K_base and R_k
       ldrec(kPf, fR);
       uint32_t nk = 0, nr = 0;
-      int iq = 0;
+      int iq = 0, irc = 0;
       int qitem = n_my > 0 ? p.sched_items[it_begin] : 0;
       DevItem qit = p.items[qitem];
       for (;;) {
@@ -485,7 +504,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           const int slot = nk % C::KS;
           if (nk < (uint32_t)C::KS || mbar_test(smem_u32(&ms.kempty[slot]), ((nk / C::KS) - 1) & 1)) {
             if (lane == 0) {
-              ev(p, 0, nk);
+              EV(0, nk);
               const uint32_t bar = smem_u32(&ms.kfull[slot]);
               mbar_expect_tx(bar, 32768);
               tma_load_3d(sbase + C::OFF_K + slot * 32768, &maps.kb, 0, base_row(kR_), 0, bar);
@@ -530,9 +549,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           busy = true;
           const int qb = iq % C::NQ;
           if (iq < C::NQ || mbar_test(smem_u32(&ms.qempty[qb]), ((iq / C::NQ) - 1) & 1)) {
-            ev(p, 9, iq);
-            const uint8_t* rsrc = (const uint8_t*)(item_recs + qitem);
-            if (lane < (int)(sizeof(ItemRec) / 16)) cp_async16(smem_u32(&ms.rec[qb]) + lane * 16, rsrc + lane * 16);
+            EV(9, iq);
             for (int o = 0; o < qit.n_warps; ++o) {
               const uint8_t* src = p.stage + (int64_t)(qit.pad_[0] + o) * kStageBytes;
 #pragma unroll
@@ -552,6 +569,17 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             progress = true;
           }
         }
+        if (irc < n_my) {  // per-item header ring (runs ahead of the Q images)
+          busy = true;
+          const int rb = irc % C::NRC;
+          if (irc < C::NRC || mbar_test(smem_u32(&ms.recempty[rb]), ((irc / C::NRC) - 1) & 1)) {
+            const uint8_t* rsrc = (const uint8_t*)(item_recs + p.sched_items[it_begin + irc]);
+            if (lane < (int)(sizeof(ItemRec) / 16)) cp_async16(smem_u32(&ms.rec[rb]) + lane * 16, rsrc + lane * 16);
+            cp_async_arrive(smem_u32(&ms.recfull[rb]));
+            ++irc;
+            progress = true;
+          }
+        }
         if (!busy) break;
         if (!progress) __nanosleep(200);  // polling warps have issue priority: yield the SMSP to the key warps
       }
@@ -564,7 +592,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       const int Pm = P < 64 ? P : 64;
       const int pf = p.tc_prefetch;
       ItemInfo Ik, Iv;
-      int ik = 0, jk = 0, iv = 0, jv = 0, eh = 0, iq = 0;
+      int ik = 0, jk = 0, iv = 0, jv = 0, eh = 0, iq = 0, irc = 0;
       uint32_t nk = 0, nv = 0;
       if (n_my > 0) { load_item(p, p.sched_items[it_begin], Ik); Iv = Ik; }
       auto brow = [&](const ItemInfo& I, int sl) {
@@ -584,7 +612,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           const int slot = nk % C::KS;
           if (nk < (uint32_t)C::KS || mbar_test(smem_u32(&ms.kempty[slot]), ((nk / C::KS) - 1) & 1)) {
             const uint32_t dst = sbase + C::OFF_K + slot * 32768, bar = smem_u32(&ms.kfull[slot]);
-            ev(p, 0, nk);
+            EV(0, nk);
             const int t0 = Ik.k0 + jk * kTile;
             if (pf > 0 && P == kTile) {
               // L2 prefetch of the K_base / V_base tiles pf tiles ahead (L2 is the deep buffer, smem the short one)
@@ -620,7 +648,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           const int slot = nv % C::VS;
           if (nv < (uint32_t)C::VS || mbar_test(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1)) {
             const uint32_t dst = sbase + C::OFF_V + slot * C::VE, bar = smem_u32(&ms.vfull[slot]);
-            ev(p, 7, nv);
+            EV(7, nv);
             mbar_expect_tx(bar, 16384);
             for (int q = 0; q < 64 / Pm; ++q) {
               const int t = Iv.k0 + jv * kTile + 64 * eh + q * Pm;
@@ -648,10 +676,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           const int qb = iq % C::NQ;
           if (iq < C::NQ || mbar_test(smem_u32(&ms.qempty[qb]), ((iq / C::NQ) - 1) & 1)) {
             const DevItem it = p.items[p.sched_items[it_begin + iq]];
-            ev(p, 9, iq);
+            EV(9, iq);
             const uint32_t bar = smem_u32(&ms.qfull[qb]);
-            mbar_expect_tx(bar, it.n_warps * (4096 + C::XB) + (uint32_t)sizeof(ItemRec));
-            bulk_g2s(smem_u32(&ms.rec[qb]), item_recs + p.sched_items[it_begin + iq], sizeof(ItemRec), bar);
+            mbar_expect_tx(bar, it.n_warps * (4096 + C::XB));
             for (int o = 0; o < it.n_warps; ++o) {
               const uint8_t* src = p.stage + (int64_t)(it.pad_[0] + o) * kStageBytes;
               bulk_g2s(sbase + C::OFF_Q + qb * C::QB + o * 2048, src, 2048, bar);
@@ -659,6 +686,17 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               bulk_g2s(sbase + C::OFF_X + qb * kSlots * C::XB + o * C::XB, src + 4096, C::XB, bar);
             }
             ++iq;
+            progress = true;
+          }
+        }
+        if (irc < n_my) {  // per-item header ring
+          busy = true;
+          const int rb = irc % C::NRC;
+          if (irc < C::NRC || mbar_test(smem_u32(&ms.recempty[rb]), ((irc / C::NRC) - 1) & 1)) {
+            const uint32_t bar = smem_u32(&ms.recfull[rb]);
+            mbar_expect_tx(bar, (uint32_t)sizeof(ItemRec));
+            bulk_g2s(smem_u32(&ms.rec[rb]), item_recs + p.sched_items[it_begin + irc], sizeof(ItemRec), bar);
+            ++irc;
             progress = true;
           }
         }
@@ -674,11 +712,12 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         const int qb = ii % C::NQ;
         const uint32_t qs = sbase + C::OFF_Q + qb * C::QB;
         const uint32_t xs = sbase + C::OFF_X + qb * kSlots * C::XB;
+        mbar_wait(smem_u32(&ms.recfull[ii % C::NRC]), (ii / C::NRC) & 1);
         mbar_wait(smem_u32(&ms.qfull[qb]), (ii / C::NQ) & 1);
-        ev(p, 10, ii);
+        EV(10, ii);
         tc_fence_after();
         // group table of the item, packed 8 bits per group: first slot, slot count
-        const int meta = ms.rec[qb].meta, n_tiles = ms.rec[qb].n_tiles;
+        const int meta = ms.rec[ii % C::NRC].meta, n_tiles = ms.rec[ii % C::NRC].n_tiles & 0xffff;
         const int n_slots = meta & 15;
         uint64_t gf = 0, gc = 0;  // 8 bits per group
         int ng = 0;
@@ -713,9 +752,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           };
           if constexpr (!kDef) {
             if (T >= 2) mbar_wait(smem_u32(&ms.sfree[sb]), ((T >> 1) - 1) & 1);
-            ev(p, 8, T);
+            EV(8, T);
             mbar_wait(smem_u32(&ms.kfull[T % C::KS]), (T / C::KS) & 1);
-            ev(p, 1, T);
+            EV(1, T);
             tc_fence_after();
             base_s();
             mbar_wait(smem_u32(&ms.rfull[T % C::RS]), (T / C::RS) & 1);
@@ -743,15 +782,15 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               mma_ss_e(tm + T_KL + 128 * w + 32 * b, dr + (uint64_t)(o * 256),
                        dx + (uint64_t)((o * 4096 + (2 * w + q) * 1024) >> 4), id_rb, 0);
               mma_commit_e(smem_u32(&ms.kl[w * kKlBufs + b]));
-              if (T == 4) ev(p, 15, 32 * w + k);
+              if (T == 4) EV(15, 32 * w + k);
             };
             auto ts = [&](int w, int k) {  // S^T[:, rows of g] += RoPE(KL)[bf16, in place] Q_g^T over the unit's 32 d
               const int q = k >= ng, g = k - q * ng;
               const uint32_t o = (uint32_t)(gf >> (8 * g)) & 0xff, cnt = (uint32_t)(gc >> (8 * g)) & 0xff;
               const uint32_t Uk = U + k, b = Uk % kKlBufs;
-              if (T == 4) ev(p, 11, 32 * w + k);
+              if (T == 4) EV(11, 32 * w + k);
               mbar_wait(smem_u32(&ms.kl[2 * kKlBufs + w * kKlBufs + b]), (Uk / kKlBufs) & 1);
-              if (T == 4) ev(p, 12, 32 * w + k);
+              if (T == 4) EV(12, 32 * w + k);
               tc_fence_after();
               const uint32_t id = idesc_bf16(128, 16 * cnt, false, false);
 #pragma unroll
@@ -763,9 +802,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             };
             for (int k = 0; k < n_units && k < kKlBufs; ++k) { rb(0, k); rb(1, k); }
             if (T >= 2) mbar_wait(smem_u32(&ms.sfree[sb]), ((T >> 1) - 1) & 1);
-            ev(p, 8, T);
+            EV(8, T);
             mbar_wait(smem_u32(&ms.kfull[T % C::KS]), (T / C::KS) & 1);
-            ev(p, 1, T);
+            EV(1, T);
             tc_fence_after();
             base_s();
             for (int k = 0; k < n_units; ++k) {
@@ -777,18 +816,19 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             U += n_units;
           }
           mma_commit_e(smem_u32(&ms.sfull[sb]));
-          ev(p, 2, T);
+          EV(2, T);
         }
         mma_commit_e(smem_u32(&ms.qempty[qb]));
       }
     } else if (wid == 10) {
       // ================= PV-side MMA issuer (whole warp, one elected lane issues) =================
       const uint32_t id_pv = idesc_bf16(128, kRows, true, true);
+      const uint32_t id_px = idesc_bf16(128, 192, true, true);
       uint32_t nv = 0, T = 0;
       for (int ii = 0; ii < n_my; ++ii) {
         const int qb = ii % C::NQ;
-        mbar_wait(smem_u32(&ms.qfull[qb]), (ii / C::NQ) & 1);
-        const int n_tiles = ms.rec[qb].n_tiles;
+        mbar_wait(smem_u32(&ms.recfull[ii % C::NRC]), (ii / C::NRC) & 1);
+        const int n_tiles = ms.rec[ii % C::NRC].n_tiles & 0xffff;
         for (int j = 0; j < n_tiles; ++j, ++T) {
           const int ab = ii % C::AB;
           if (j == 0 && ii >= C::AB) mbar_wait(smem_u32(&ms.accfree[ab]), ((ii / C::AB) - 1) & 1);
@@ -796,14 +836,26 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             // P^T half kh of tile T = ring entry nv (the V-side entries run in the same order)
             const int ps = nv % C::NPH;
             mbar_wait(smem_u32(&ms.pfull[ps]), (nv / C::NPH) & 1);
-            if (kh == 0) ev(p, 5, T);
+            if (kh == 0) EV(5, T);
             const uint64_t dp = make_desc(sbase + C::OFF_P + ps * C::PHB, 8192, 1024, SWZ_128);
             mbar_wait(smem_u32(&ms.vfull[nv % C::VS]), (nv / C::VS) & 1);
             mbar_wait(smem_u32(&ms.rvfull[nv % C::VS]), (nv / C::VS) & 1);
-            ev(p, 6, nv);
+            EV(6, nv);
             tc_fence_after();
             const uint32_t ve = sbase + C::OFF_V + (nv % C::VS) * C::VE;
             const uint64_t dv = make_desc(ve, 8192, 1024, SWZ_128), da = make_desc(ve + 16384, 2048, 256, SWZ_32);
+            if constexpr (C::PVROW) {
+              // O_ext[rows on lanes][V d | R_v slots] += P [V | R_v]: A = P from the P^T half (MN-major, the
+              // second 64-row atom aliases the first: LBO = 0, lanes 64..127 duplicate the rows), B = the V-side entry
+              const uint64_t pa = make_desc(sbase + C::OFF_P + ps * C::PHB, 0, 1024, SWZ_128);
+#pragma unroll
+              for (int s = 0; s < 4; ++s)
+                mma_ss_e(tm + C::tOX(ab), pa + (uint64_t)((s * 2048) >> 4), dv + (uint64_t)((s * 2048) >> 4), id_px,
+                         (j > 0 || kh > 0 || s > 0));
+              mma_commit_e(smem_u32(&ms.vempty[nv % C::VS]));
+              mma_commit_e(smem_u32(&ms.pfree[ps]));
+              continue;
+            }
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
               const int ck = 4 * kh + s, par = ck % C::PAR;  // NONE: two chains per accumulator (key-chunk parity)
@@ -815,7 +867,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             mma_commit_e(smem_u32(&ms.vempty[nv % C::VS]));
             mma_commit_e(smem_u32(&ms.pfree[ps]));
           }
-          ev(p, 18, T);
+          EV(18, T);
         }
       }
     } else if (wid == 11) {
@@ -830,6 +882,17 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         mbar_wait(bar, parity);
       };
       auto commit = [&](uint32_t full_bar) { cp_async_arrive(full_bar); };
+      // destination of 16-B chunk c (key c >> 1, physical page chunk c & 1) of slot o's R_v half: verbatim SW32
+      // (per-slot 2 KB operand), or PVROW: column 16 o + 8 hq of the SW128 MN-major [V | R_v] atom, hq the
+      // logical half the page's SW32 swizzle put in that chunk
+      auto rv_off = [&](int o, int c) -> uint32_t {
+        if constexpr (C::PVROW) {
+          const int key = c >> 1, hq = (c & 1) ^ ((key >> 2) & 1);
+          return mnmajor_off(16 * o + 8 * hq, key, 8, 0, 1024);
+        } else {
+          return (uint32_t)(o * 2048 + c * 16);
+        }
+      };
       if (P == kTile) {
         // fast path: one page per tile; R_v halves only (R_k is streamed by the producer warp); page ids from
         // the tile records (32 per lane batch, the next batch prefetched)
@@ -863,7 +926,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             const uint32_t nv = 2 * T + h, slot = nv % C::VS;
             if (nv >= (uint32_t)C::VS) wait_free(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1);
             if (lane == 0) {  // V_base 64-key half (16 KB, one 3D box)
-              ev(p, 7, nv);
+              EV(7, nv);
               const uint32_t bar = smem_u32(&ms.vfull[slot]);
               mbar_expect_tx(bar, 16384);
               tma_load_3d(sbase + C::OFF_V + slot * C::VE, &maps.vb, 0, vrow + 64 * h, 0, bar);
@@ -876,7 +939,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                   const int c = lane + 32 * u;
-                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + o * 2048 + c * 16),
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + rv_off(o, c)),
                                "l"(src + c * 8)
                                : "memory");
                 }
@@ -923,7 +986,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
                 const int tt = t < I.k1 ? t : I.k0;
                 const int rp = p.res_pages[I.slot_res[o] + tt / P];
                 const __nv_bfloat16* src = rvl + ((int64_t)rp * P + tt % P) * kR + (c & 1) * 8;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + o * 2048 + c * 16), "l"(src)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + rv_off(o, c)), "l"(src)
                              : "memory");
               }
             }
@@ -970,6 +1033,46 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       const int ab = ie % C::AB, ns = Re.meta & 15;
       for (uint32_t np = 2 * Tl; np < 2 * Tl + 2; ++np) mbar_wait(smem_u32(&ms.pfree[np % C::NPH]), (np / C::NPH) & 1);
       tc_fence_after();
+      if constexpr (C::PVROW) {
+        // rows on the TMEM lanes: row c = 32 (wq & 1) + lane sits in lane quarters wq & 1 and (wq & 1) + 2 (the A
+        // operand's second atom duplicates the rows); the lazy rescale keeps columns [0, 96) current in the first
+        // copy and [96, 192) in the second, so all 8 key warps share the stores as: warp (w, wq) writes its rows'
+        // columns [48 q, 48 q + 48), q = 2 (wq >> 1) + w: acc (16-byte stores) and the row owner's acc_r
+        const int c = 32 * (wq & 1) + lane, o = c >> 4, r = c & 15, q = 2 * (wq >> 1) + w;
+        const bool valid = o < ns && r < Re.n_rows[o];
+        float* ent = p.ws + (int64_t)(Re.entry_off[o < ns ? o : 0] + r) * p.entry_stride + kEntAcc;
+        const uint32_t base = tm + C::tOX(ab) + 48 * q + lb;
+        uint32_t x[48];
+        FKV_TMEM_LD16(base, x);
+        FKV_TMEM_LD16(base + 16, (x + 16));
+        FKV_TMEM_LD16(base + 32, (x + 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(smem_u32(&ms.accfree[ab]));
+        if (valid) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const int col = 48 * q + 16 * k;  // warp-uniform
+            if (col < kD) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                *(float4*)(ent + col + 4 * i) =
+                    make_float4(__uint_as_float(x[16 * k + 4 * i]), __uint_as_float(x[16 * k + 4 * i + 1]),
+                                __uint_as_float(x[16 * k + 4 * i + 2]), __uint_as_float(x[16 * k + 4 * i + 3]));
+            } else if ((col - kD) / 16 == o) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                *(float4*)(ent + kD + 4 * i) =
+                    make_float4(__uint_as_float(x[16 * k + 4 * i]), __uint_as_float(x[16 * k + 4 * i + 1]),
+                                __uint_as_float(x[16 * k + 4 * i + 2]), __uint_as_float(x[16 * k + 4 * i + 3]));
+            }
+          }
+        }
+        named_bar_sync(bar_id, 128);
+        if (kl == 0) mbar_arrive(smem_u32(&ms.recempty[qbe]));
+        if (tid == 0) EV(27, ie);
+        return;
+      }
 #pragma unroll 1
       for (int ch = 0; ch < NCH; ++ch) {
         const int cb = CPW * w + 32 * ch;
@@ -986,8 +1089,8 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           const int c = cb + i, o = c >> 4, r = c & 15;
           if (o < ns && r < Re.n_rows[o]) {
             float* ent = p.ws + (int64_t)(Re.entry_off[o] + r) * p.entry_stride;
-            ent[2 + kl] = __uint_as_float(o_[i]);                                  // acc[d = kl]
-            if ((kl >> 4) == o) ent[2 + kD + (kl & 15)] = __uint_as_float(a_[i]);  // acc_r[j] of this row's owner
+            ent[kEntAcc + kl] = __uint_as_float(o_[i]);                                  // acc[d = kl]
+            if ((kl >> 4) == o) ent[kEntAcc + kD + (kl & 15)] = __uint_as_float(a_[i]);  // acc_r[j] of this row's owner
             if (kl == 64) {
               if constexpr (C::ONES) {
                 ent[1] = __uint_as_float(a_[i]);  // l (all-ones slot)
@@ -1000,39 +1103,50 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       }
       // this warpgroup is done with the item header (and the row-sum partials)
       named_bar_sync(bar_id, 128);
-      if (kl == 0) mbar_arrive(smem_u32(&ms.qempty[qbe]));
+      if (kl == 0) mbar_arrive(smem_u32(&ms.recempty[qbe]));
     };
     int pend_ii = -1, pend_qb = 0;
     uint32_t pend_Tl = 0;
     for (int ii = 0; ii < n_my; ++ii) {
-      const int qb = ii % C::NQ;
-      mbar_wait(smem_u32(&ms.qfull[qb]), (ii / C::NQ) & 1);
+      const int qb = ii % C::NRC;  // header ring entry
+      mbar_wait(smem_u32(&ms.recfull[qb]), (ii / C::NRC) & 1);
       const ItemRec& R = ms.rec[qb];
       ItemLite I;
       I.k0 = R.k0;
       I.k1 = R.k1;
-      I.n_tiles = R.n_tiles;
+      I.n_tiles = R.n_tiles & 0xffff;
       I.n_slots = R.meta & 15;
       I.n_groups = (R.meta >> 4) & 15;
-      // per-item column state of this warpgroup; the previous item's epilogue is done with m_run / lw
-      named_bar_sync(bar_id, 128);
-      if (kl < CPW) {
-        ms.m_run[CPW * w + kl] = -INFINITY;
-        if constexpr (!C::ONES) {
+      float* const mrun = ms.m_run + (C::PVROW ? (ii & 1) * kRows : 0);
+      float* const lwb = ms.lw + (C::PVROW ? (ii & 1) * 4 * kRows : 0);
+      if constexpr (!C::PVROW) {
+        // per-item column state of this warpgroup; the previous item's epilogue is done with m_run / lw
+        named_bar_sync(bar_id, 128);
+        if (kl < CPW) {
+          ms.m_run[CPW * w + kl] = -INFINITY;
+          if constexpr (!C::ONES) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) ms.lw[q * kRows + CPW * w + kl] = 0.f;
+            for (int q = 0; q < 4; ++q) ms.lw[q * kRows + CPW * w + kl] = 0.f;
+          }
         }
+        named_bar_sync(bar_id, 128);
       }
-      named_bar_sync(bar_id, 128);
-      uint32_t causal_mask = 0;  // bit ch: chunk ch has a column that does not see every key of the item
+      // PVROW: this thread's per-column partial row sums (its keys, fp32 p) over the item's tiles, pairs of columns;
+      // reduced over the keys once at the item end
+      uint64_t lsum2[C::PVROW ? 16 : 1];
+#pragma unroll
+      for (int q = 0; q < (C::PVROW ? 16 : 1); ++q) lsum2[q] = 0;
+      // bit ch: chunk ch has a query column that does not see every key of the item (planner, n_tiles >> 16)
+      const uint32_t causal_mask = ((uint32_t)R.n_tiles >> (16 + NCH * w)) & ((1u << NCH) - 1);
+      // used query columns of each chunk (slot o < n_slots, row < n_rows[o]); unused ones are masked like invisible
+      uint32_t colmask[NCH];
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
-        const uint16_t* P1c = R.pos1 + CPW * w + 32 * ch;
-        bool cz = false;
-#pragma unroll
-        for (int c = 0; c < 32; ++c) cz |= (int)P1c[c] < I.k1 - I.k0;
-        causal_mask |= (uint32_t)cz << ch;
+        const int o0 = (CPW * w + 32 * ch) >> 4;
+        const int n0 = o0 < I.n_slots ? R.n_rows[o0] : 0, n1 = o0 + 1 < I.n_slots ? R.n_rows[o0 + 1] : 0;
+        colmask[ch] = (n0 >= 16 ? 0xffffu : (1u << n0) - 1) | ((n1 >= 16 ? 0xffffu : (1u << n1) - 1) << 16);
       }
+      if (tid == 0) EV(25, ii);
       for (int j = 0; j < I.n_tiles; ++j, ++T) {
         const int t0 = I.k0 + j * kTile;
         const int t = t0 + kl;
@@ -1067,7 +1181,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               uint32_t x[16], y[16], lh[16];
               const uint32_t b = U % kKlBufs;
               mbar_wait(smem_u32(&ms.kl[w * kKlBufs + b]), (U / kKlBufs) & 1);
-              if (T == 4 && kl == 0) ev(p, 13, 32 * w + q * I.n_groups + g);
+              if (T == 4 && kl == 0) EV(13, 32 * w + q * I.n_groups + g);
               tc_fence_after();
               const uint32_t kt = tm + T_KL + 128 * w + 32 * b + lb;
               FKV_TMEM_LD16(kt, x);
@@ -1084,7 +1198,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               tmem_st_wait();
               tc_fence_before();
               mbar_arrive(smem_u32(&ms.kl[2 * kKlBufs + w * kKlBufs + b]));
-              if (T == 4 && kl == 0) ev(p, 14, 32 * w + q * I.n_groups + g);
+              if (T == 4 && kl == 0) EV(14, 32 * w + q * I.n_groups + g);
               ++U;
             }
           }
@@ -1098,7 +1212,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           // ---- online softmax over the chunk's 32 query columns (Alg1.339-341) ----
           const int cb = CPW * w + 32 * ch;
           const uint16_t* P1 = R.pos1 + cb;  // key t visible iff t - k0 < P1[c]
-          uint32_t vm = tvalid ? 0xffffffffu : 0u;
+          uint32_t vm = tvalid ? colmask[ch] : 0u;
           if (((causal_mask >> ch) & 1) && tvalid) {
             const int tr = t - I.k0;
             vm = 0;
@@ -1115,7 +1229,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
           if (ch == 0) {
             mbar_wait(smem_u32(&ms.sfull[sb]), (T >> 1) & 1);
-            if (tid == 0) ev(p, 3, T);
+            if (tid == 0) EV(3, T);
             tc_fence_after();
           }
           uint32_t sr[32];
@@ -1128,7 +1242,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           uint64_t x2[16];
           float mx = -INFINITY;
           {
-            const float4* mp = (const float4*)&ms.m_run[cb];
+            const float4* mp = (const float4*)&mrun[cb];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               const float4 m4 = mp[q];
@@ -1156,46 +1270,44 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
           // lazy rescaling: only when some score exceeds the running max by > 2^8
           float alpha_l = 1.f;  // this lane's column (cb + lane) rescale factor (row-sum partials)
-          if (tid == 0) ev(p, 20, T);
+          if (tid == 0) EV(20, T);
           if (bar_or(bar_id, 128, mx > 8.0f)) {
-            if (tid == 0) ev(p, 21, T);
+            if (tid == 0) EV(21, T);
+            // first tile of the item: every column is fresh (m = -inf), nothing to read back or rescale
+            const bool first = j == 0;
             float mo[32];
-            {
-              const float4* mp = (const float4*)&ms.m_run[cb];
+            if (!first) {
+              const float4* mp = (const float4*)&mrun[cb];
 #pragma unroll
               for (int q = 0; q < 8; ++q) {
                 const float4 m4 = mp[q];
                 mo[4 * q] = m4.x; mo[4 * q + 1] = m4.y; mo[4 * q + 2] = m4.z; mo[4 * q + 3] = m4.w;
               }
             }
-            const float mo_l = ms.m_run[cb + lane];
+            const float mo_l = first ? -INFINITY : mrun[cb + lane];
             float v[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
               const bool ok = (vm >> c) & 1u;
               v[c] = ok ? __uint_as_float(sr[c]) * scl : -INFINITY;
             }
+            // per-column max over the warp's 32 keys (redux.sync.max.f32, sm_100a); lane l keeps column cb + l
 #pragma unroll
-            for (int step = 0; step < 5; ++step) {
-              const int off = 16 >> step, half = 16 >> step;
-              const bool up = lane & off;
-#pragma unroll
-              for (int i = 0; i < half; ++i) {
-                const float send = up ? v[i] : v[i + half];
-                const float keep = up ? v[i + half] : v[i];
-                v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, off));
-              }
+            for (int c = 0; c < 32; ++c) {
+              float r;
+              asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v[c]));
+              if (lane == c) v[0] = r;
             }
-            // lane l holds the warp's max for column cb + l
+            // lane l holds the warp's max for column cb + l; every thread has read the old maxima (mo)
+            if (!first) named_bar_sync(bar_id, 128);
+            if (tid == 0) EV(22, T);
+            if (v[0] > -INFINITY) atomic_max_f(&mrun[cb + lane], v[0]);
             named_bar_sync(bar_id, 128);
-            if (tid == 0) ev(p, 22, T);
-            if (v[0] > -INFINITY) atomic_max_f(&ms.m_run[cb + lane], v[0]);
-            named_bar_sync(bar_id, 128);
-            if (tid == 0) ev(p, 23, T);
+            if (tid == 0) EV(23, T);
             float mn[32];
             bool resc = false;
             {
-              const float4* mp = (const float4*)&ms.m_run[cb];
+              const float4* mp = (const float4*)&mrun[cb];
 #pragma unroll
               for (int q = 0; q < 8; ++q) {
                 const float4 m4 = mp[q];
@@ -1203,36 +1315,59 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               }
             }
             {
-              const float mn_l = ms.m_run[cb + lane];
+              const float mn_l = mrun[cb + lane];
               alpha_l = mo_l == -INFINITY ? 0.f : ex2(mo_l - mn_l);
             }
             float al[32];
+            if (!first) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {  // branch-free: ex2(0) = 1 for unchanged columns
-              const bool fresh = mo[c] == -INFINITY;
-              al[c] = fresh ? 0.f : ex2(mo[c] - mn[c]);
-              resc |= !fresh && (mn[c] != mo[c]);
+              for (int c = 0; c < 32; ++c) {  // branch-free: ex2(0) = 1 for unchanged columns
+                const bool fresh = mo[c] == -INFINITY;
+                al[c] = fresh ? 0.f : ex2(mo[c] - mn[c]);
+                resc |= !fresh && (mn[c] != mo[c]);
+              }
+              if constexpr (C::PVROW) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) lsum2[q] = mul2(lsum2[q], f2(al[2 * q], al[2 * q + 1]));
+              }
             }
             if (resc && j > 0) {
               // rescale the chunk's columns of O^T and A^T by alpha (all PV up to tile T-1 complete)
               for (uint32_t q2 = 2 * (T - 1); q2 < 2 * T; ++q2)
                 mbar_wait(smem_u32(&ms.pfree[q2 % C::NPH]), (q2 / C::NPH) & 1);
               tc_fence_after();
+              if constexpr (C::PVROW) {
+                // rows on lanes: this lane's row 32 w + lane (quarters w, w + 2), 96 columns each, times alpha_l
+                if ((wq & 1) == w) {
+                  const uint32_t base = tm + C::tOX(ii % C::AB) + 96 * (wq >> 1) + lb;
 #pragma unroll
-              for (int part = 0; part < 2; ++part) {
-                const uint32_t base = tm + ((part & 1) ? C::tA(ii % C::AB, 0) : C::tO(ii % C::AB, 0)) + cb + lb;
-                uint32_t r[32];
-                FKV_TMEM_LD32(base, r);
-                tmem_ld_wait();
+                  for (int part = 0; part < 3; ++part) {
+                    uint32_t r[32];
+                    FKV_TMEM_LD32(base + 32 * part, r);
+                    tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * al[i]);
-                FKV_TMEM_ST16(base, r);
-                FKV_TMEM_ST16(base + 16, (r + 16));
+                    for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha_l);
+                    FKV_TMEM_ST16(base + 32 * part, r);
+                    FKV_TMEM_ST16(base + 32 * part + 16, (r + 16));
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int part = 0; part < 2; ++part) {
+                  const uint32_t base = tm + ((part & 1) ? C::tA(ii % C::AB, 0) : C::tO(ii % C::AB, 0)) + cb + lb;
+                  uint32_t r[32];
+                  FKV_TMEM_LD32(base, r);
+                  tmem_ld_wait();
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * al[i]);
+                  FKV_TMEM_ST16(base, r);
+                  FKV_TMEM_ST16(base + 16, (r + 16));
+                }
               }
               tmem_st_wait();
               tc_fence_before();
             }
-            if (tid == 0) ev(p, 24, T);
+            if (tid == 0) EV(24, T);
             // recompute with the updated running max (a column with no visible key keeps -inf -> p = 0)
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -1250,18 +1385,20 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           for (int q = 0; q < 16; ++q) {
             float a, b2;
             uf2(x2[q], a, b2);
-            pk[q] = pack_bf16x2(ex2(a), ex2(b2));
+            const float ea = ex2(a), eb = ex2(b2);
+            pk[q] = pack_bf16x2(ea, eb);
+            if constexpr (C::PVROW) lsum2[q] = fadd2(lsum2[q], f2(ea, eb));
           }
           if (ch == 0) {
-            if (tid == 0) ev(p, 16, T);
+            if (tid == 0) EV(16, T);
             if (np >= (uint32_t)C::NPH) mbar_wait(smem_u32(&ms.pfree[ps]), ((np / C::NPH) - 1) & 1);
-            if (tid == 0) ev(p, 17, T);
+            if (tid == 0) EV(17, T);
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             *(uint4*)(pbuf + mnmajor_off(cb + q * 8, kl & 63, 8, 8192, 1024)) =
                 make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-          if constexpr (!C::ONES) {
+          if constexpr (!C::ONES && !C::PVROW) {
             // row sums l without an all-ones MMA slot: the warp's 32 keys summed per column (of the bf16 P the
             // MMA uses), lane l -> column cb + l; per-warp partials, rescaled with the running max
             float v[32];
@@ -1281,13 +1418,13 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
                 v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
               }
             }
-            float* lp = &ms.lw[wq * kRows + cb + lane];
+            float* lp = &lwb[wq * kRows + cb + lane];
             *lp = *lp * alpha_l + v[0];
           }
         }
         fence_async_smem();
         mbar_arrive(smem_u32(&ms.pfull[ps]));
-        if (tid == 0) ev(p, 4, T);
+        if (tid == 0) EV(4, T);
         if (C::AB > 1 && j == 0 && pend_ii >= 0) {
           epilogue(pend_ii, pend_Tl, pend_qb);
           pend_ii = -1;
@@ -1295,11 +1432,42 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       }
       // ---- item end: the running max is final -> m of every partial entry now; the accumulators once the
       // last PV completes (NONE 64-row: deferred past the next item's first tile, the PV pipe runs on) ----
-      if (kl == 64) {
+      if (tid == 0) EV(26, ii);
+      if constexpr (C::PVROW) {
+        // m and l of row 32 w + kl (the epilogue is deferred past the next item's start, which resets m_run / lw):
+        // the thread partials reduced over the warp's 32 keys (lane l -> column 32 w + l), then over the 4 warps
+        {
+          float v[32];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) uf2(lsum2[q], v[2 * q], v[2 * q + 1]);
+#pragma unroll
+          for (int step = 0; step < 5; ++step) {
+            const int off = 16 >> step, half = 16 >> step;
+            const bool up = lane & off;
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+              const float send = up ? v[i] : v[i + half];
+              const float keep = up ? v[i + half] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+          }
+          lwb[wq * kRows + 32 * w + lane] = v[0];
+        }
+        named_bar_sync(bar_id, 128);
+        if (kl < 32) {
+          const int c = 32 * w + kl, o = c >> 4, r = c & 15;
+          if (o < I.n_slots && r < R.n_rows[o]) {
+            float* ent = p.ws + (int64_t)(R.entry_off[o] + r) * p.entry_stride;
+            ent[0] = mrun[c];
+            ent[1] = lwb[c] + lwb[kRows + c] + lwb[2 * kRows + c] + lwb[3 * kRows + c];
+          }
+          mrun[c] = -INFINITY;  // this buffer's next item (ii + 2) starts fresh
+        }
+      } else if (kl == 64) {
 #pragma unroll 1
         for (int i = 0; i < CPW; ++i) {
           const int c = CPW * w + i, o = c >> 4, r = c & 15;
-          if (o < I.n_slots && r < R.n_rows[o]) p.ws[(int64_t)(R.entry_off[o] + r) * p.entry_stride] = ms.m_run[c];
+          if (o < I.n_slots && r < R.n_rows[o]) p.ws[(int64_t)(R.entry_off[o] + r) * p.entry_stride] = mrun[c];
         }
       }
       if (C::AB == 1) {

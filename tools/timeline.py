@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--tiles", type=int, default=12)
     ap.add_argument("--page", type=int, default=64)
     ap.add_argument("--detail", type=int, default=-1)
+    ap.add_argument("--first", type=int, default=0)
     a = ap.parse_args()
     import torch
     import numpy as np
@@ -59,15 +60,16 @@ def main():
     torch.cuda.synchronize()
     lib.fkv_debug_timeline(fkv.ctx, None, 0)
     d = dbg.view(32, 256).cpu().numpy()
-    t0 = d[d > 0].min()
+    t0 = d[:30][d[:30] > 0].min()
     print("per tile T (S/W/PV events) and per ring entry (K slab 3/tile, V entry 2/tile), cycles from first event")
     cols = [8, 2, 3, 4, 5]
     print("   T " + " ".join(f"{EV[e]:>9s}" for e in cols) + " |  n " + " ".join(f"{EV[e]:>9s}" for e in (0, 1, 7, 6)))
-    for j in range(a.tiles):
+    for j in range(a.first, a.first + a.tiles):
         row = [d[e, j] - t0 if d[e, j] else -1 for e in cols]
         row2 = [d[e, j] - t0 if d[e, j] else -1 for e in (0, 1, 7, 6)]
         print(f"{j:4d} " + " ".join(f"{x:9d}" for x in row) + f" | {j:3d} " + " ".join(f"{x:9d}" for x in row2))
-    print("items: P:Qitem / S:Qfull", [(d[9, i] - t0, d[10, i] - t0) for i in range(16) if d[9, i]])
+    print("items: P:Qitem / S:Qfull", [(int(d[9, i] - t0), int(d[10, i] - t0)) for i in range(64) if d[9, i]])
+    print("key warps per item: start / end / epilogue done", [(int(d[25, i] - t0), int(d[26, i] - t0), int(d[27, i] - t0) if d[27, i] else -1) for i in range(64) if d[25, i]])
     if a.detail >= 0:
         T = a.detail
         base = d[0, T]
@@ -88,6 +90,12 @@ def main():
                 i = 32 * w + k
                 f = lambda e: (d[e, i] - b0) if d[e, i] else -1
                 print(f"  w{w} k{k}: rb {f(15):7d}  ts-wait {f(11):7d} ok {f(12):7d} | keys ok {f(13):7d} done {f(14):7d}")
+    pf = [int(d[4, j]) for j in range(256) if d[4, j]]
+    if len(pf) > 1:
+        gaps = np.diff(np.array(pf))
+        print("W:pfull period per tile (cycles):", " ".join(str(int(g)) for g in gaps))
+        print(f"  first W:pfull {pf[0] - t0}, median period {int(np.median(gaps))}, sum of periods > 1.5x median "
+              f"{int(gaps[gaps > 1.5 * np.median(gaps)].sum())}")
     dur, nt = d[30, :148], d[31, :148]
     if dur.any():
         o = np.argsort(dur)
