@@ -96,13 +96,14 @@ void ctx_create(Ctx& c, const fkv_config& cfg, const fkv_buffers* buf) {
         // see TcMaps in ra_tc.cu: K_base whole tiles (3D, both d-halves) when P = 128, V_base 64-key halves,
         // residual pages as 128-byte rows (the page format is already the SW32 operand layout, res_col)
         const uint32_t Pm = P < 64 ? (uint32_t)P : 64u;
-        CUtensorMap m[4];
+        CUtensorMap m[5];
         m[0] = P == 128 ? make_tmap_3d_bf16_halves(buf->base_k, brows, 128)
                         : make_tmap_2d_bf16(buf->base_k, brows, 128, 256, 64, P, 128);
         m[1] = P >= 64 ? make_tmap_3d_bf16_halves(buf->base_v, brows, 64)
                        : make_tmap_2d_bf16(buf->base_v, brows, 128, 256, 64, P, 128);
         m[2] = make_tmap_2d_bf16(buf->res_k, rrows / 4, 64, 128, 64, P / 4, 0);
         m[3] = make_tmap_2d_bf16(buf->res_v, rrows / 4, 64, 128, 64, Pm / 4, 0);
+        m[4] = make_tmap_2d_bf16(buf->base_k, brows, 128, 256, 64, P, 128);  // K_base d-half boxes
         c.tc_maps.assign((const uint8_t*)m, (const uint8_t*)m + sizeof(m));
         c.has_tc_maps = true;
       }

@@ -114,7 +114,7 @@ struct Ctx {
   std::unordered_map<int32_t, int32_t> adapter_slot;
   uint64_t generation = 1;
   bool has_tc_maps = false;
-  std::vector<uint8_t> tc_maps;  // 4 CUtensorMap (base K, base V, R_k, R_v) for the tcgen05 kernel
+  std::vector<uint8_t> tc_maps;  // 5 CUtensorMap (base K, base V, R_k, R_v, K d-halves) for the tcgen05 kernel
   std::string last_error;
   size_t elem = 2;
   void* dbg = nullptr;  // diagnostics buffer (fkv_debug_timeline)

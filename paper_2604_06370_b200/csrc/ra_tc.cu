@@ -59,14 +59,16 @@ struct Cfg {
   static constexpr int ROWS = kRowsT, SLOTS = kRowsT / 16;
   // NONE, 64 rows: PV as O_ext = P [V | R_v of the 4 slots] with the query rows on the TMEM lanes: 8 MMA
   // instructions of N = 192 per tile instead of 16 (O^T and A^T separately); row sums on the CUDA cores
-  static constexpr bool PVROW = !kDef && kRowsT == 64;
+  static constexpr bool PVROW = !kDef;
   static constexpr bool ONES = kRowsT == 64 && !PVROW;  // A^T has a free slot for the all-ones rows (row sums l)
   // R_k (small) is single-buffered with its pages L2-prefetched two tiles ahead; V_base / R_v wait for softmax(T):
   // a deeper ring; P^T in 64-key halves so softmax(T+1) overlaps PV(T)
-  static constexpr int KS = kRowsT == 128 ? 1 : 2;  // K_base ring (32 KB: one 128-key tile, both d-halves)
+  // K_base ring in 16-KB d-half units (a 128-key tile = 2 units): 4 units = two whole tiles (one 3D TMA box per
+  // tile); 128-row CTAs: 3 units (each d-half its own box, S(T+1)'s first half streams in while S(T) runs)
+  static constexpr int KU = kRowsT == 128 ? 3 : 4;
   static constexpr int RS = 1;                      // R_k ring (4 KB per slot)
   static constexpr int VS = kRowsT == 128 ? 2 : 3;  // V-side ring (64-key half of V_base | R_v per slot | ones)
-  static constexpr int NPH = kRowsT == 128 ? 3 : 4;  // P^T ring of 64-key halves (PV of half h needs only it)
+  static constexpr int NPH = kRowsT == 128 ? 2 : 4;  // P^T ring of 64-key halves (PV of half h needs only it)
   static constexpr int NQ = (kDef || kRowsT == 128) ? 1 : 2;  // per-item Q / X buffers (freed by the S-side MMAs)
   static constexpr int NRC = 4;  // per-item header ring (held by the key warps until the item's epilogue)
   // Accumulator layout switches (both measured on B200): split accumulation chains (SH / PAR = 2) do not help, a
@@ -84,16 +86,18 @@ struct Cfg {
   static constexpr uint32_t RB = SLOTS * 4096;       // R_k entry: [slot][128 keys][32 B]
   // V-side entry: PVROW: [V d-half 0 | V d-half 1 | R_v 4 slots interleaved per key] as three SW128 MN-major atoms
   // of 64 columns (8 KB each); otherwise [V half 16 KB | R_v per slot 2 KB | ones 2 KB]
-  static constexpr uint32_t VE = PVROW ? 24576 : 16384 + SLOTS * 2048 + (ONES ? 2048 : 0);
-  __host__ __device__ static constexpr uint32_t tOX(int ab) { return 128 + 192 * ab; }  // PVROW: O_ext [64 rows][192]
+  static constexpr uint32_t VE = 16384 + SLOTS * 2048 + (ONES ? 2048 : 0);
+  // PVROW: O_ext [rows on lanes][V d 128 | R_v 16 per slot] at TMEM column 2 ROWS (after the two S^T buffers)
+  static constexpr int OXW = 128 + 16 * SLOTS;
+  __host__ __device__ static constexpr uint32_t tOX(int ab) { return 2 * ROWS + OXW * ab; }
   static constexpr uint32_t OFF_V = 0;
   static constexpr uint32_t OFF_K = OFF_V + VS * VE;
-  static constexpr uint32_t OFF_R = OFF_K + KS * 32768;
+  static constexpr uint32_t OFF_R = OFF_K + KU * 16384;
   static constexpr uint32_t OFF_Q = OFF_R + RS * RB;
   static constexpr uint32_t OFF_P = OFF_Q + NQ * QB;
   static constexpr uint32_t OFF_X = OFF_P + NPH * PHB;  // [NQ][SLOTS][XB]
   static constexpr uint32_t OFF_MISC = OFF_X + NQ * SLOTS * XB;
-  static constexpr uint32_t MISCB = kRowsT == 128 ? 5120 : (PVROW ? 4096 : 2048);
+  static constexpr uint32_t MISCB = kRowsT == 128 ? 7168 : (PVROW ? 4096 : 2048);
   static constexpr uint32_t SMEM = OFF_MISC + MISCB;
   static_assert(SMEM <= 232448, "shared memory");
   static_assert(!(kDef && kRowsT != 64), "DEFERRED runs 64-row CTAs");
@@ -107,7 +111,7 @@ struct kDefOf<Cfg<D, R>> {
 };
 template <class C>
 struct MiscT {
-  uint64_t kfull[2], kempty[2], rfull[1], rempty[1], vfull[3], vempty[3], rvfull[3], qfull[2], qempty[2], sfull[2],
+  uint64_t kfull[4], kempty[4], rfull[1], rempty[1], vfull[3], vempty[3], rvfull[3], qfull[2], qempty[2], sfull[2],
       sfree[2], pfull[4], pfree[4], accfree[2], recfull[C::NRC], recempty[C::NRC], kl[kDefOf<C>::value ? 4 * kKlBufs : 1];  // kl: DEFERRED klfull | klready
   // running column max (PVROW: two buffers by item parity, reset by the item's end, so items start barrier-free)
   alignas(16) float m_run[(C::PVROW ? 2 : 1) * C::ROWS];
@@ -119,7 +123,7 @@ struct MiscT {
 struct TcMaps {
   // kb: P == 128: 3D {64, 128, 2} (a whole tile, both d-halves), else 2D {64, P}; vb: P >= 64: 3D {64, 64, 2},
   // else 2D {64, P}; rk / rv: the residual pool viewed as 128-byte rows, {64, P / 4} / {64, min(P, 64) / 4}
-  CUtensorMap kb, vb, rk, rv;
+  CUtensorMap kb, vb, rk, rv, kh;  // kh: K_base d-half boxes {64, 128} (P = 128, 3-unit K ring)
 };
 
 struct ItemInfo {
@@ -411,6 +415,18 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
   Misc& ms = *reinterpret_cast<Misc*>(smem + C::OFF_MISC);
   const ItemRec* item_recs = (const ItemRec*)p.item_recs;
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  // K ring: d-half h of tile T in unit (2T + h) % KU, its (2T + h) / KU-th use; one 3D box (one barrier) per tile
+  // when the two units of a tile are adjacent (KU = 4, P = 128)
+  const bool k_single = C::KU == 4 && p.P == kTile;
+  auto k_unit = [](uint32_t T, int h) { return (int)((2 * T + h) % C::KU); };
+  auto k_use = [](uint32_t T, int h) { return (2 * T + h) / C::KU; };
+  auto k_free = [&](uint32_t T) {  // both units of tile T free (the S MMAs of their previous tile completed)
+    bool ok = true;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (2 * T + h >= (uint32_t)C::KU) ok = ok && mbar_test(smem_u32(&ms.kempty[k_unit(T, h)]), (k_use(T, h) - 1) & 1);
+    return ok;
+  };
   if (sbase & 1023) __trap();
   const long long t_start = clock64();
   const int cta = blockIdx.x;
@@ -421,7 +437,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 
   // ---------------- setup ----------------
   if (tid == 0) {
-    for (int i = 0; i < C::KS; ++i) { mbar_init(smem_u32(&ms.kfull[i]), 1); mbar_init(smem_u32(&ms.kempty[i]), 1); }
+    for (int i = 0; i < C::KU; ++i) { mbar_init(smem_u32(&ms.kfull[i]), 1); mbar_init(smem_u32(&ms.kempty[i]), 1); }
     // rfull / rvfull: one cp.async.mbarrier.arrive.noinc per lane of the copying warp
     for (int i = 0; i < C::RS; ++i) { mbar_init(smem_u32(&ms.rfull[i]), 32); mbar_init(smem_u32(&ms.rempty[i]), 1); }
     for (int i = 0; i < C::VS; ++i) {
@@ -473,7 +489,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       // ================= producer, fast path (P = 128: one page per tile), whole warp =================
       // TMA (lane 0): K_base tiles; cp.async (all lanes): R_k tiles and the per-item header / Q / X images.
       // Page ids come from the tile records, each stream's next record preloaded (no page-table chasing).
-      tma_prefetch_desc(&maps.kb); tma_prefetch_desc(&maps.vb);
+      tma_prefetch_desc(&maps.kb); tma_prefetch_desc(&maps.vb); tma_prefetch_desc(&maps.kh);
       const __nv_bfloat16* rkl = (const __nv_bfloat16*)p.res_k + (int64_t)p.layer * p.res_layer_stride;
       const int64_t brow_l = (int64_t)p.layer * p.nb;
       const int r0 = p.tile_ptr[cta], nrec = p.tile_ptr[cta + 1] - r0;
@@ -499,15 +515,23 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       DevItem qit = p.items[qitem];
       for (;;) {
         bool busy = false, progress = false;
-        if (nk < (uint32_t)nrec) {  // K_base tile (32 KB, one 3D box)
+        if (nk < (uint32_t)nrec) {  // K_base tile (32 KB: one 3D box, or one 2D box per d-half unit)
           busy = true;
-          const int slot = nk % C::KS;
-          if (nk < (uint32_t)C::KS || mbar_test(smem_u32(&ms.kempty[slot]), ((nk / C::KS) - 1) & 1)) {
+          if (k_free(nk)) {
             if (lane == 0) {
               EV(0, nk);
-              const uint32_t bar = smem_u32(&ms.kfull[slot]);
-              mbar_expect_tx(bar, 32768);
-              tma_load_3d(sbase + C::OFF_K + slot * 32768, &maps.kb, 0, base_row(kR_), 0, bar);
+              if (k_single) {
+                const uint32_t bar = smem_u32(&ms.kfull[k_unit(nk, 0)]);
+                mbar_expect_tx(bar, 32768);
+                tma_load_3d(sbase + C::OFF_K + k_unit(nk, 0) * 16384, &maps.kb, 0, base_row(kR_), 0, bar);
+              } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const uint32_t bar = smem_u32(&ms.kfull[k_unit(nk, h)]);
+                  mbar_expect_tx(bar, 16384);
+                  tma_load_2d(sbase + C::OFF_K + k_unit(nk, h) * 16384, &maps.kh, 64 * h, base_row(kR_), bar);
+                }
+              }
             }
             if (nk + kPf < (uint32_t)nrec) {  // R_k pages of tile nk + kPf -> L2 (one 128-byte line per lane)
 #pragma unroll
@@ -609,9 +633,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         // K_base tile (32 KB)
         if (ik < n_my) {
           busy = true;
-          const int slot = nk % C::KS;
-          if (nk < (uint32_t)C::KS || mbar_test(smem_u32(&ms.kempty[slot]), ((nk / C::KS) - 1) & 1)) {
-            const uint32_t dst = sbase + C::OFF_K + slot * 32768, bar = smem_u32(&ms.kfull[slot]);
+          if (k_free(nk)) {
             EV(0, nk);
             const int t0 = Ik.k0 + jk * kTile;
             if (pf > 0 && P == kTile) {
@@ -626,15 +648,23 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
                 tma_prefetch_l2_3d(&maps.vb, 0, row + 64, 0);
               }
             }
-            mbar_expect_tx(bar, 32768);
-            if (P == kTile) {
-              tma_load_3d(dst, &maps.kb, 0, brow(Ik, (t0 < Ik.k1 ? t0 : Ik.k0) / P), 0, bar);
+            if (k_single) {
+              const uint32_t bar = smem_u32(&ms.kfull[k_unit(nk, 0)]);
+              mbar_expect_tx(bar, 32768);
+              tma_load_3d(sbase + C::OFF_K + k_unit(nk, 0) * 16384, &maps.kb, 0,
+                          brow(Ik, (t0 < Ik.k1 ? t0 : Ik.k0) / P), 0, bar);
             } else {
-              for (int q = 0; q < kTile / P; ++q) {
-                const int t = t0 + q * P;
-                const int row = brow(Ik, (t < Ik.k1 ? t : Ik.k0) / P);
-                tma_load_2d(dst + q * P * 128, &maps.kb, 0, row, bar);
-                tma_load_2d(dst + 16384 + q * P * 128, &maps.kb, 64, row, bar);
+              for (int h = 0; h < 2; ++h) {
+                const uint32_t dst = sbase + C::OFF_K + k_unit(nk, h) * 16384, bar = smem_u32(&ms.kfull[k_unit(nk, h)]);
+                mbar_expect_tx(bar, 16384);
+                for (int q = 0; q < kTile / P; ++q) {
+                  const int t = t0 + q * P;
+                  const int row = brow(Ik, (t < Ik.k1 ? t : Ik.k0) / P);
+                  if (P == kTile)
+                    tma_load_2d(dst, &maps.kh, 64 * h, row, bar);
+                  else
+                    tma_load_2d(dst + q * P * 128, &maps.kb, 64 * h, row, bar);
+                }
               }
             }
             ++nk;
@@ -737,25 +767,28 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         for (int j = 0; j < n_tiles; ++j, ++T) {
           const int sb = T & 1;
           const uint32_t sacc = tm + C::tS(sb, 0);
-          const uint64_t dk = make_desc(sbase + C::OFF_K + (T % C::KS) * 32768, 16, 1024, SWZ_128);
+
           const uint32_t rk = sbase + C::OFF_R + (T % C::RS) * C::RB;
           auto base_s = [&]() {  // S^T = K_base Q^T over both d-halves (descriptor + (byte offset >> 4))
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              // NONE: d-half chains interleaved (0,4,1,5,...) into separate accumulators
-              const int c = C::SH == 2 ? ((i & 1) * 4 + (i >> 1)) : i;
-              const int h = C::SH == 2 ? (c >> 2) : 0;
-              mma_ss_e(tm + C::tS(sb, h), dk + (uint64_t)(((c >> 2) * 16384 + (c & 3) * 32) >> 4),
-                       dq + (uint64_t)(((c >> 2) * (C::QB / 2) + (c & 3) * 32) >> 4), id_s, C::SH == 2 ? (c & 3) != 0 : c != 0);
+            for (int h = 0; h < 2; ++h) {
+              const int u = k_unit(T, h);
+              if (h == 0 || !k_single) {
+                mbar_wait(smem_u32(&ms.kfull[k_single ? k_unit(T, 0) : u]), k_use(T, k_single ? 0 : h) & 1);
+                if (h == 0) EV(1, T);
+                tc_fence_after();
+              }
+              const uint64_t dk = make_desc(sbase + C::OFF_K + u * 16384, 16, 1024, SWZ_128);
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                mma_ss_e(tm + C::tS(sb, 0), dk + (uint64_t)((c * 32) >> 4),
+                         dq + (uint64_t)((h * (C::QB / 2) + c * 32) >> 4), id_s, h > 0 || c > 0);
+              mma_commit_e(smem_u32(&ms.kempty[u]));
             }
-            mma_commit_e(smem_u32(&ms.kempty[T % C::KS]));
           };
           if constexpr (!kDef) {
             if (T >= 2) mbar_wait(smem_u32(&ms.sfree[sb]), ((T >> 1) - 1) & 1);
             EV(8, T);
-            mbar_wait(smem_u32(&ms.kfull[T % C::KS]), (T / C::KS) & 1);
-            EV(1, T);
-            tc_fence_after();
             base_s();
             mbar_wait(smem_u32(&ms.rfull[T % C::RS]), (T / C::RS) & 1);
             tc_fence_after();
@@ -803,9 +836,6 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             for (int k = 0; k < n_units && k < kKlBufs; ++k) { rb(0, k); rb(1, k); }
             if (T >= 2) mbar_wait(smem_u32(&ms.sfree[sb]), ((T >> 1) - 1) & 1);
             EV(8, T);
-            mbar_wait(smem_u32(&ms.kfull[T % C::KS]), (T / C::KS) & 1);
-            EV(1, T);
-            tc_fence_after();
             base_s();
             for (int k = 0; k < n_units; ++k) {
               ts(0, k);
@@ -823,7 +853,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
     } else if (wid == 10) {
       // ================= PV-side MMA issuer (whole warp, one elected lane issues) =================
       const uint32_t id_pv = idesc_bf16(128, kRows, true, true);
-      const uint32_t id_px = idesc_bf16(128, 192, true, true);
+      const uint32_t id_px = idesc_bf16(128, C::OXW, true, true);
       uint32_t nv = 0, T = 0;
       for (int ii = 0; ii < n_my; ++ii) {
         const int qb = ii % C::NQ;
@@ -847,7 +877,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             if constexpr (C::PVROW) {
               // O_ext[rows on lanes][V d | R_v slots] += P [V | R_v]: A = P from the P^T half (MN-major, the
               // second 64-row atom aliases the first: LBO = 0, lanes 64..127 duplicate the rows), B = the V-side entry
-              const uint64_t pa = make_desc(sbase + C::OFF_P + ps * C::PHB, 0, 1024, SWZ_128);
+              const uint64_t pa = make_desc(sbase + C::OFF_P + ps * C::PHB, kRows == 128 ? 8192 : 0, 1024, SWZ_128);
 #pragma unroll
               for (int s = 0; s < 4; ++s)
                 mma_ss_e(tm + C::tOX(ab), pa + (uint64_t)((s * 2048) >> 4), dv + (uint64_t)((s * 2048) >> 4), id_px,
@@ -888,7 +918,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       auto rv_off = [&](int o, int c) -> uint32_t {
         if constexpr (C::PVROW) {
           const int key = c >> 1, hq = (c & 1) ^ ((key >> 2) & 1);
-          return mnmajor_off(16 * o + 8 * hq, key, 8, 0, 1024);
+          return mnmajor_off(16 * o + 8 * hq, key, 8, 8192, 1024);
         } else {
           return (uint32_t)(o * 2048 + c * 16);
         }
@@ -1033,7 +1063,50 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       const int ab = ie % C::AB, ns = Re.meta & 15;
       for (uint32_t np = 2 * Tl; np < 2 * Tl + 2; ++np) mbar_wait(smem_u32(&ms.pfree[np % C::NPH]), (np / C::NPH) & 1);
       tc_fence_after();
-      if constexpr (C::PVROW) {
+      if constexpr (C::PVROW && kRows == 128) {
+        // rows on the TMEM lanes: row c = 32 wq + lane; warpgroup 0 writes acc (columns [0, 128)), warpgroup 1 the
+        // row owner's acc_r (one 32-column load covers the two slots of the warp's rows)
+        const int c = 32 * wq + lane, o = c >> 4, r = c & 15;
+        const bool valid = o < ns && r < Re.n_rows[o];
+        float* ent = p.ws + (int64_t)(Re.entry_off[o < ns ? o : 0] + r) * p.entry_stride + kEntAcc;
+        if (w == 0) {
+#pragma unroll 1
+          for (int part = 0; part < 4; ++part) {
+            uint32_t x[32];
+            FKV_TMEM_LD32(tm + C::tOX(ab) + 32 * part + lb, x);
+            tmem_ld_wait();
+            if (part == 3) {
+              tc_fence_before();
+              mbar_arrive(smem_u32(&ms.accfree[ab]));
+            }
+            if (valid) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                *(float4*)(ent + 32 * part + 4 * i) =
+                    make_float4(__uint_as_float(x[4 * i]), __uint_as_float(x[4 * i + 1]), __uint_as_float(x[4 * i + 2]),
+                                __uint_as_float(x[4 * i + 3]));
+            }
+          }
+        } else {
+          uint32_t x[32];
+          FKV_TMEM_LD32(tm + C::tOX(ab) + kD + 32 * wq + lb, x);
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(smem_u32(&ms.accfree[ab]));
+          if (valid) {
+            const bool hi = lane & 16;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              *(float4*)(ent + kD + 4 * i) = make_float4(
+                  __uint_as_float(hi ? x[16 + 4 * i] : x[4 * i]), __uint_as_float(hi ? x[17 + 4 * i] : x[4 * i + 1]),
+                  __uint_as_float(hi ? x[18 + 4 * i] : x[4 * i + 2]), __uint_as_float(hi ? x[19 + 4 * i] : x[4 * i + 3]));
+          }
+        }
+        named_bar_sync(bar_id, 128);
+        if (kl == 0) mbar_arrive(smem_u32(&ms.recempty[qbe]));
+        if (tid == 0) EV(27, ie);
+        return;
+      } else if constexpr (C::PVROW) {
         // rows on the TMEM lanes: row c = 32 (wq & 1) + lane sits in lane quarters wq & 1 and (wq & 1) + 2 (the A
         // operand's second atom duplicates the rows); the lazy rescale keeps columns [0, 96) current in the first
         // copy and [96, 192) in the second, so all 8 key warps share the stores as: warp (w, wq) writes its rows'
@@ -1133,9 +1206,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       }
       // PVROW: this thread's per-column partial row sums (its keys, fp32 p) over the item's tiles, pairs of columns;
       // reduced over the keys once at the item end
-      uint64_t lsum2[C::PVROW ? 16 : 1];
+      uint64_t lsum2[C::PVROW ? NCH : 1][C::PVROW ? 16 : 1];
 #pragma unroll
-      for (int q = 0; q < (C::PVROW ? 16 : 1); ++q) lsum2[q] = 0;
+      for (int ch = 0; ch < (C::PVROW ? NCH : 1); ++ch)
+#pragma unroll
+        for (int q = 0; q < (C::PVROW ? 16 : 1); ++q) lsum2[ch][q] = 0;
       // bit ch: chunk ch has a query column that does not see every key of the item (planner, n_tiles >> 16)
       const uint32_t causal_mask = ((uint32_t)R.n_tiles >> (16 + NCH * w)) & ((1u << NCH) - 1);
       // used query columns of each chunk (slot o < n_slots, row < n_rows[o]); unused ones are masked like invisible
@@ -1328,7 +1403,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               }
               if constexpr (C::PVROW) {
 #pragma unroll
-                for (int q = 0; q < 16; ++q) lsum2[q] = mul2(lsum2[q], f2(al[2 * q], al[2 * q + 1]));
+                for (int q = 0; q < 16; ++q) lsum2[ch][q] = mul2(lsum2[ch][q], f2(al[2 * q], al[2 * q + 1]));
               }
             }
             if (resc && j > 0) {
@@ -1337,11 +1412,14 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
                 mbar_wait(smem_u32(&ms.pfree[q2 % C::NPH]), (q2 / C::NPH) & 1);
               tc_fence_after();
               if constexpr (C::PVROW) {
-                // rows on lanes: this lane's row 32 w + lane (quarters w, w + 2), 96 columns each, times alpha_l
-                if ((wq & 1) == w) {
-                  const uint32_t base = tm + C::tOX(ii % C::AB) + 96 * (wq >> 1) + lb;
-#pragma unroll
-                  for (int part = 0; part < 3; ++part) {
+                // rows on lanes, times alpha_l of this lane's row cb + lane. 64 rows: quarters w (columns [0, 96)) and
+                // w + 2 (the duplicate rows, columns [96, 192)); 128 rows: quarter 2 w + ch, all 256 columns
+                const bool mine = kRows == 64 ? (wq & 1) == w : wq == 2 * w + ch;
+                if (mine) {
+                  constexpr int NPART = kRows == 64 ? 3 : C::OXW / 32;
+                  const uint32_t base = tm + C::tOX(ii % C::AB) + (kRows == 64 ? 96 * (wq >> 1) : 0) + lb;
+#pragma unroll 1
+                  for (int part = 0; part < NPART; ++part) {
                     uint32_t r[32];
                     FKV_TMEM_LD32(base + 32 * part, r);
                     tmem_ld_wait();
@@ -1387,7 +1465,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             uf2(x2[q], a, b2);
             const float ea = ex2(a), eb = ex2(b2);
             pk[q] = pack_bf16x2(ea, eb);
-            if constexpr (C::PVROW) lsum2[q] = fadd2(lsum2[q], f2(ea, eb));
+            if constexpr (C::PVROW) lsum2[ch][q] = fadd2(lsum2[ch][q], f2(ea, eb));
           }
           if (ch == 0) {
             if (tid == 0) EV(16, T);
@@ -1434,12 +1512,13 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       // last PV completes (NONE 64-row: deferred past the next item's first tile, the PV pipe runs on) ----
       if (tid == 0) EV(26, ii);
       if constexpr (C::PVROW) {
-        // m and l of row 32 w + kl (the epilogue is deferred past the next item's start, which resets m_run / lw):
-        // the thread partials reduced over the warp's 32 keys (lane l -> column 32 w + l), then over the 4 warps
-        {
+        // m and l of the warpgroup's columns CPW w + kl (the epilogue runs later; m_run / lw are double-buffered):
+        // the thread partials reduced over the warp's 32 keys (lane l -> column cb + l), then over the 4 warps
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
           float v[32];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) uf2(lsum2[q], v[2 * q], v[2 * q + 1]);
+          for (int q = 0; q < 16; ++q) uf2(lsum2[ch][q], v[2 * q], v[2 * q + 1]);
 #pragma unroll
           for (int step = 0; step < 5; ++step) {
             const int off = 16 >> step, half = 16 >> step;
@@ -1451,11 +1530,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
             }
           }
-          lwb[wq * kRows + 32 * w + lane] = v[0];
+          lwb[wq * kRows + CPW * w + 32 * ch + lane] = v[0];
         }
         named_bar_sync(bar_id, 128);
-        if (kl < 32) {
-          const int c = 32 * w + kl, o = c >> 4, r = c & 15;
+        if (kl < CPW) {
+          const int c = CPW * w + kl, o = c >> 4, r = c & 15;
           if (o < I.n_slots && r < R.n_rows[o]) {
             float* ent = p.ws + (int64_t)(R.entry_off[o] + r) * p.entry_stride;
             ent[0] = mrun[c];

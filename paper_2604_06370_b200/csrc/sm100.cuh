@@ -143,8 +143,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef FKV_SPIN_WAIT
   while (!mbar_try_wait(bar, parity)) {
   }
+#else
+  // try_wait with a suspend-time hint: the warp sleeps in hardware until the phase completes (or the hint expires)
+  // instead of spinning on the issue port shared with the softmax warps
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!ok);
+#endif
 }
 // blocking wait that suspends the thread in hardware until the phase completes
 // (suspend-time hint), so waiting warps do not steal issue slots
