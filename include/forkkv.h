@@ -142,8 +142,9 @@ const char* fkv_version(void);
 
 /* Register adapter `adapter_id` (>= 0): B_K, B_V device arrays
  * [L][Hkv_local][r][d] (the kv-head column slices of B), LoRA alpha/r
- * folded in (C-7). Borrowed. Re-registering an id replaces the pointers and
- * invalidates existing plans (E_STALE). */
+ * folded in (C-7). Borrowed; device contexts need 16-byte aligned arrays
+ * (E_INVALID otherwise: vector loads). Re-registering an id replaces the
+ * pointers and invalidates existing plans (E_STALE). */
 fkv_status fkv_register_adapter(fkv_ctx* ctx, int32_t adapter_id, const void* B_K, const void* B_V);
 
 /* ---- control plane (R1-R9) ----------------------------------- */

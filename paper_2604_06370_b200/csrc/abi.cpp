@@ -68,6 +68,8 @@ fkv_status fkv_register_adapter(fkv_ctx* ctx, int32_t adapter_id, const void* B_
   return guard(ctx, [&] {
     if (adapter_id < 0) throw Error(FKV_E_INVALID, "register_adapter: negative id");
     if (ctx->c.device && (!B_K || !B_V)) throw Error(FKV_E_INVALID, "register_adapter: null B_K/B_V");
+    if (ctx->c.device && (((uintptr_t)B_K | (uintptr_t)B_V) & 15))
+      throw Error(FKV_E_INVALID, "register_adapter: B_K/B_V must be 16-byte aligned");
     auto it = ctx->c.adapter_slot.find(adapter_id);
     if (it == ctx->c.adapter_slot.end()) {
       ctx->c.adapter_slot[adapter_id] = (int32_t)ctx->c.adapters.size();

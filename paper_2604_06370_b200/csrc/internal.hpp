@@ -171,6 +171,7 @@ struct Plan {
   std::vector<DevWarp> warps;
   std::vector<DevRow> rows;        // warp rows (16 per warp)
   std::vector<int32_t> out_ptr;    // CSR over output rows (n_rows_q * hq_local + 1)
+  std::vector<int64_t> comb_rows;  // per output row: e0 | e1 << 32, B_v^h address of layer 0 (combine kernel)
   std::vector<int32_t> out_entries;
   std::vector<int64_t> adapter_ptrs;  // [slot][2] device pointers
   std::vector<int32_t> qrow_seq;      // query row -> plan seq index
@@ -184,7 +185,7 @@ struct Plan {
   // device layout (offsets into the uploaded blob)
   std::vector<uint8_t> blob;
   size_t off_seqs = 0, off_base = 0, off_res = 0, off_items = 0, off_warps = 0, off_rows = 0, off_outptr = 0,
-         off_outent = 0, off_adapters = 0, off_qrow = 0,
+         off_outent = 0, off_adapters = 0, off_qrow = 0, off_comb = 0,
          off_sptr = 0, off_sitems = 0, off_tptr = 0, off_trecs = 0, off_irecs = 0, off_ssrc = 0;
   void* dev = nullptr;
   size_t ws_bytes = 0;

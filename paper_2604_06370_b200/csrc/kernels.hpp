@@ -68,6 +68,7 @@ struct AttnParams {
   const DevRow* rows;
   const int32_t* out_ptr;
   const int32_t* out_entries;
+  const longlong2* comb_rows;  // per output row: (e0 | e1 << 32, B_v^h address of layer 0)
   const int64_t* adapters;  // [slot][2]: B_K, B_V device pointers
   const int32_t* qrow_seq;  // query row -> plan seq
   int64_t base_layer_stride;  // elements per layer of base pool

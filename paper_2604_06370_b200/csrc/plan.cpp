@@ -387,6 +387,14 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
     pl.adapter_ptrs[2 * s + 1] = (int64_t)(intptr_t)c.adapters[s].bv;
   }
   // algorithmic bytes per layer: shared base once per segment,
+  // combine rows: entry range and the row's B_v^h (one 16-byte load per output row)
+  pl.comb_rows.assign(2 * n_out, 0);
+  for (int64_t o = 0; o < n_out; ++o) {
+    const int32_t qrow = (int32_t)(o / c.hq_local), qh = (int32_t)(o % c.hq_local), h = qh / c.group;
+    const int32_t slot = pl.seqs[pl.qrow_seq[qrow]].adapter_slot;
+    pl.comb_rows[2 * o] = (int64_t)(uint32_t)pl.out_ptr[o] | ((int64_t)pl.out_ptr[o + 1] << 32);
+    pl.comb_rows[2 * o + 1] = pl.adapter_ptrs[2 * slot + 1] + (int64_t)h * r * d * el;
+  }
   // residual once per (segment, owner), adapters once, Q in + O out.
   std::set<int32_t> used_adapters;
   for (const DevSeq& s : pl.seqs) used_adapters.insert(s.adapter_slot);
@@ -404,6 +412,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   pl.off_outent = put(pl.blob, pl.out_entries);
   pl.off_adapters = put(pl.blob, pl.adapter_ptrs);
   pl.off_qrow = put(pl.blob, pl.qrow_seq);
+  pl.off_comb = put(pl.blob, pl.comb_rows);
   pl.off_sptr = put(pl.blob, pl.sched_ptr);
   pl.off_sitems = put(pl.blob, pl.sched_items);
   pl.off_tptr = put(pl.blob, pl.tile_ptr);
@@ -450,6 +459,7 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.out_entries = (const int32_t*)(base + p.off_outent);
   a.adapters = (const int64_t*)(base + p.off_adapters);
   a.qrow_seq = (const int32_t*)(base + p.off_qrow);
+  a.comb_rows = (const longlong2*)(base + p.off_comb);
   const int64_t P = c.cfg.page_size, d = c.cfg.head_dim, r = c.cfg.rank;
   a.base_layer_stride = c.cfg.n_base_pages * c.hkv_local * P * d;
   a.res_layer_stride = c.cfg.n_res_pages * P * r;

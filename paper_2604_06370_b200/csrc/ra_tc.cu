@@ -337,6 +337,9 @@ __device__ __forceinline__ int perm_d(int n) {
 // d-halves, 2 KB each) and q~ = Q B_k^T (NONE, K-major SW32, 512 B) or B_k^h
 // with permuted columns (DEFERRED, MN-major SW64 quarter blocks, 4 KB).
 __global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_images) {
+  // the main kernel (programmatic dependent launch) may start its prologue and K/V streaming now; it waits for
+  // this grid's completion (griddepcontrol.wait) before it reads the staged images
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int ii = blockIdx.x;
   if (ii >= n_images) return;
   __shared__ __align__(16) float qs[16][kD];
@@ -571,6 +574,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         }
         if (iq < n_my) {  // per-item header, Q rows and q~ / packed B_k (staged images): cp.async by all lanes
           busy = true;
+          if (iq == 0) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the stager's images are complete
           const int qb = iq % C::NQ;
           if (iq < C::NQ || mbar_test(smem_u32(&ms.qempty[qb]), ((iq / C::NQ) - 1) & 1)) {
             EV(9, iq);
@@ -703,6 +707,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         // per-item Q rows and q~ / packed B_k (staged images)
         if (iq < n_my) {
           busy = true;
+          if (iq == 0) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the stager's images are complete
           const int qb = iq % C::NQ;
           if (iq < C::NQ || mbar_test(smem_u32(&ms.qempty[qb]), ((iq / C::NQ) - 1) & 1)) {
             const DevItem it = p.items[p.sched_items[it_begin + iq]];
@@ -1579,8 +1584,19 @@ cudaError_t launch_tc_variant(const AttnParams& p, const void* maps, cudaStream_
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  ra_tc_kernel<kDef, kRowsT><<<p.n_ctas, 384, Cfg<kDef, kRowsT>::SMEM, s>>>(*(const TcMaps*)maps, p);
-  return cudaGetLastError();
+  // programmatic dependent launch: the CTAs start (TMEM, barriers, K / V / residual streaming) while the stager
+  // finishes; the producer's griddepcontrol.wait orders the staged-image reads after it
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_ctas);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = Cfg<kDef, kRowsT>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ra_tc_kernel<kDef, kRowsT>, *(const TcMaps*)maps, p);
 }
 
 cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStream_t s) {
