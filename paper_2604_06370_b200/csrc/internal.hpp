@@ -179,6 +179,7 @@ struct Plan {
   std::vector<int32_t> tile_ptr, tile_recs;      // per-CTA tile records (8 ints each, see kernels.hpp)
   std::vector<uint8_t> item_recs;                // per-item k::ItemRecT
   std::vector<int32_t> stage_src;                // staged image -> source warp slot
+  std::vector<int32_t> stage_desc;               // per image: B_k^h address (2 ints), n_rows, h, Q row index [16]
   int32_t n_ctas = 0;
   size_t stage_off = 0;  // workspace offset of the staged operand images (tcgen05 kernel)
   int64_t n_segments = 0, n_entries = 0, key_tiles = 0, alg_bytes = 0;
@@ -186,7 +187,7 @@ struct Plan {
   std::vector<uint8_t> blob;
   size_t off_seqs = 0, off_base = 0, off_res = 0, off_items = 0, off_warps = 0, off_rows = 0, off_outptr = 0,
          off_outent = 0, off_adapters = 0, off_qrow = 0, off_comb = 0,
-         off_sptr = 0, off_sitems = 0, off_tptr = 0, off_trecs = 0, off_irecs = 0, off_ssrc = 0;
+         off_sptr = 0, off_sitems = 0, off_tptr = 0, off_trecs = 0, off_irecs = 0, off_ssrc = 0, off_sdesc = 0;
   void* dev = nullptr;
   size_t ws_bytes = 0;
 };

@@ -92,6 +92,7 @@ struct AttnParams {
   const void* item_recs;  // per plan item: ItemRecT<tc_rows / 16>
   int32_t tc_rows;        // query rows per CTA of the tcgen05 kernel (64 | 128)
   const int32_t* stage_src;  // staged image i is built from warp slot stage_src[i]; DevItem::pad_[0] = first image
+  const int4* stage_desc;    // per image, 5 x int4: {B_k^h address (layer 0) lo, hi, n_rows, kv head}, Q rows [16]
   int32_t max_pos;
   int32_t tc_prefetch;  // L2 prefetch distance in tiles (tcgen05 producer; 0 = off)
   uint8_t* stage;  // per-warp-slot staged operand images (ws region, kStageBytes each)

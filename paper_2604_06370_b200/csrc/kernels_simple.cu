@@ -393,10 +393,11 @@ cudaError_t launch_synth_fill(void* dst, int32_t dtype, uint64_t seed, int32_t k
   return cudaGetLastError();
 }
 
-// d = 128, r = 16: lane l owns head-dim elements 4l..4l+3 (16-byte partial-entry loads, all of a batch's entries
-// in flight at once), lanes 0..3 own acc_r 4l..4l+3; the late V fusion loads B_v rows as 4-element vectors
+// d = 128, r = 16: lane l owns head-dim elements 4l..4l+3 (16-byte partial-entry loads, a batch of entries in
+// flight at once) and, for l < 16, acc_r[l]; the late V fusion reads B_v rows as 4-element vectors. <= 128
+// registers: all 2048-row C2 warps resident in one wave
 template <typename T>
-__global__ void __launch_bounds__(256) combine128_kernel(AttnParams p) {
+__global__ void __launch_bounds__(256, 2) combine128_kernel(AttnParams p) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= p.n_out_rows) return;
@@ -404,72 +405,52 @@ __global__ void __launch_bounds__(256) combine128_kernel(AttnParams p) {
   const int e0 = (int)(cr.x & 0xffffffffll), e1 = (int)(cr.x >> 32);
   // B_v^h rows (16 x 128) for the late fusion, issued first: they do not depend on the partials
   const T* bv = (const T*)cr.y + (int64_t)p.layer * p.adapter_layer_stride;
-  float4 bvr[16];
+  uint2 bvu[16];  // bf16: 4 elements; f32: elements 4l, 4l+1 (the other two re-read at the end)
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if constexpr (sizeof(T) == 2) {
-      const uint2 u = __ldg((const uint2*)(bv + j * 128 + 4 * lane));
-      bvr[j] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u), __uint_as_float(u.y << 16),
-                           __uint_as_float(u.y & 0xffff0000u));
-    } else {
-      bvr[j] = __ldg((const float4*)(bv + j * 128 + 4 * lane));
-    }
-  }
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), accr = make_float4(0.f, 0.f, 0.f, 0.f);
-  float l = 0.f, Mrun = -INFINITY;
+  for (int j = 0; j < 16; ++j) bvu[j] = __ldg((const uint2*)(bv + j * 128 + 4 * lane));
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float accr = 0.f, l = 0.f, Mrun = -INFINITY;
   for (int eb = e0; eb < e1; eb += 32) {
     const int ne = min(32, e1 - eb);
     const int my_e = lane < ne ? p.out_entries[eb + lane] : 0;
-    // the first 8 entries' accumulators are loaded together with (m, l): they do not depend on the weights
-    float4 v0[8], vr0[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int e = __shfl_sync(0xffffffffu, my_e, k < ne ? k : ne - 1);
-      const float* ent = p.ws + (int64_t)e * p.entry_stride + kEntAcc;
-      v0[k] = *(const float4*)(ent + 4 * lane);
-      vr0[k] = lane < 4 ? *(const float4*)(ent + 128 + 4 * lane) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    float2 ml = make_float2(-INFINITY, 0.f);
-    if (lane < ne) ml = *(const float2*)(p.ws + (int64_t)my_e * p.entry_stride);
-    const bool ok = ml.y > 0.f;
-    float M = ok ? ml.x : -INFINITY;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    M = fmaxf(M, Mrun);
-    if (Mrun != -INFINITY && M != Mrun) {  // more than 32 entries: rescale the earlier batches
-      const float sc = exp2f(Mrun - M);
-      l *= sc;
-      acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
-      accr.x *= sc; accr.y *= sc; accr.z *= sc; accr.w *= sc;
-    }
-    Mrun = M;
-    const float wi = ok ? exp2f(ml.x - M) : 0.f;
-    float lsum = wi * ml.y;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    l += lsum;
+    const float* my = p.ws + (int64_t)my_e * p.entry_stride;
+    const float2 ml = lane < ne ? *(const float2*)my : make_float2(-INFINITY, 0.f);
     for (int i0 = 0; i0 < ne; i0 += 8) {
-      float4 v[8], vr[8];
-      float w[8];
+      float4 v[8];
+      float vr[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {  // all loads of the 8 entries first
-        const int i = i0 + k < ne ? i0 + k : ne - 1;
-        w[k] = i0 + k < ne ? __shfl_sync(0xffffffffu, wi, i) : 0.f;
-        if (i0 == 0) {
-          v[k] = v0[k];
-          vr[k] = vr0[k];
-        } else {
-          const int e = __shfl_sync(0xffffffffu, my_e, i);
-          const float* ent = p.ws + (int64_t)e * p.entry_stride + kEntAcc;
-          v[k] = *(const float4*)(ent + 4 * lane);
-          vr[k] = lane < 4 ? *(const float4*)(ent + 128 + 4 * lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k = 0; k < 8; ++k) {  // the batch's loads first (they do not depend on the weights)
+        const int e = __shfl_sync(0xffffffffu, my_e, i0 + k < ne ? i0 + k : ne - 1);
+        const float* ent = p.ws + (int64_t)e * p.entry_stride + kEntAcc;
+        v[k] = *(const float4*)(ent + 4 * lane);
+        vr[k] = lane < 16 ? ent[128 + lane] : 0.f;
+      }
+      if (i0 == 0) {  // weights of this batch of <= 32 entries: 2^(m_i - M), entries with l > 0 only
+        const bool ok = ml.y > 0.f;
+        float M = ok ? ml.x : -INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        M = fmaxf(M, Mrun);
+        if (Mrun != -INFINITY && M != Mrun) {  // more than 32 entries: rescale the earlier batches
+          const float sc = exp2f(Mrun - M);
+          l *= sc; accr *= sc;
+          acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
         }
+        Mrun = M;
+      }
+      const float wi = ml.y > 0.f ? exp2f(ml.x - Mrun) : 0.f;
+      if (i0 == 0) {
+        float lsum = wi * ml.y;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        l += lsum;
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        if (w[k] != 0.f) {  // an entry with l = 0 may hold non-finite accumulators
-          acc.x += w[k] * v[k].x; acc.y += w[k] * v[k].y; acc.z += w[k] * v[k].z; acc.w += w[k] * v[k].w;
-          accr.x += w[k] * vr[k].x; accr.y += w[k] * vr[k].y; accr.z += w[k] * vr[k].z; accr.w += w[k] * vr[k].w;
+        const float w = i0 + k < ne ? __shfl_sync(0xffffffffu, wi, i0 + k) : 0.f;
+        if (w != 0.f) {  // an entry with l = 0 may hold non-finite accumulators
+          acc.x += w * v[k].x; acc.y += w * v[k].y; acc.z += w * v[k].z; acc.w += w * v[k].w;
+          accr += w * vr[k];
         }
       }
     }
@@ -477,9 +458,16 @@ __global__ void __launch_bounds__(256) combine128_kernel(AttnParams p) {
   // late fusion: O = (acc + acc_r . B_v^h) / l   (Alg1.349-350)
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const float src = (j & 3) == 0 ? accr.x : (j & 3) == 1 ? accr.y : (j & 3) == 2 ? accr.z : accr.w;
-    const float a = __shfl_sync(0xffffffffu, src, j >> 2);
-    acc.x += a * bvr[j].x; acc.y += a * bvr[j].y; acc.z += a * bvr[j].z; acc.w += a * bvr[j].w;
+    const float a = __shfl_sync(0xffffffffu, accr, j);
+    float4 b;
+    if constexpr (sizeof(T) == 2) {
+      b = make_float4(__uint_as_float(bvu[j].x << 16), __uint_as_float(bvu[j].x & 0xffff0000u),
+                      __uint_as_float(bvu[j].y << 16), __uint_as_float(bvu[j].y & 0xffff0000u));
+    } else {
+      const float2 hi = __ldg((const float2*)(bv + j * 128 + 4 * lane + 2));
+      b = make_float4(__uint_as_float(bvu[j].x), __uint_as_float(bvu[j].y), hi.x, hi.y);
+    }
+    acc.x += a * b.x; acc.y += a * b.y; acc.z += a * b.z; acc.w += a * b.w;
   }
   const float inv = 1.f / l;
   T* o = (T*)p.O + (int64_t)warp * 128 + 4 * lane;

@@ -251,10 +251,21 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
         const int64_t nt = (ke - kb + kTileKeys - 1) / kTileKeys;
         pl.key_tiles += nt;
         order_key.push_back({ct.k0, pi, (int64_t)ci});
-        // cost in KB of shared-memory ingest: base K + V tiles, R_k + R_v per slot, + per-item overhead
-        // per-item overhead (header staging, first-tile softmax setup, epilogue) measured at ~4-6 tiles
-        static const int64_t ovh = getenv("FKV_ITEM_OVERHEAD") ? atoll(getenv("FKV_ITEM_OVERHEAD")) : 5;
-        item_cost.push_back((nt + ovh) * (64 + 8 * it.n_warps));
+        if (pl.kernel == 2) {
+          // tcgen05: a tile costs its MMA instructions (S 8 + one per residual group, PV 8; ~115 cycles each, the
+          // binding resource), an item ~22 more (header, first-tile softmax setup, epilogue; B200 timeline)
+          int32_t ng = 0;
+          for (int o = 0; o < it.n_warps; ++o) {
+            const DevWarp& w = pl.warps[it.warp_off + o];
+            ng += o == 0 || w.res_off != pl.warps[it.warp_off + o - 1].res_off ||
+                  w.adapter_slot != pl.warps[it.warp_off + o - 1].adapter_slot;
+          }
+          static const int64_t ovh = getenv("FKV_ITEM_OVERHEAD") ? atoll(getenv("FKV_ITEM_OVERHEAD")) : 22;
+          item_cost.push_back(nt * (16 + ng) + ovh);
+        } else {
+          // cost in KB of shared-memory ingest: base K + V tiles, R_k + R_v per slot, + ~5 tiles per item
+          item_cost.push_back((nt + 5) * (64 + 8 * it.n_warps));
+        }
       }
     }
   }
@@ -387,6 +398,26 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
     pl.adapter_ptrs[2 * s + 1] = (int64_t)(intptr_t)c.adapters[s].bv;
   }
   // algorithmic bytes per layer: shared base once per segment,
+  // stager descriptors: one 80-byte record per image (no pointer chasing in the stage kernel)
+  pl.stage_desc.assign(pl.stage_src.size() * 20, 0);
+  for (size_t i = 0; i < pl.stage_src.size(); ++i) {
+    const DevWarp& w = pl.warps[pl.stage_src[i]];
+    const int32_t h = pl.rows[w.row_off].qh / c.group;
+    const int64_t bk = pl.adapter_ptrs[2 * w.adapter_slot] + (int64_t)h * r * d * el;
+    int32_t* dsc = pl.stage_desc.data() + 20 * i;
+    dsc[0] = (int32_t)(bk & 0xffffffffll);
+    dsc[1] = (int32_t)(bk >> 32);
+    dsc[2] = w.n_rows;
+    dsc[3] = h;
+    for (int j = 0; j < 16; ++j) {
+      if (j < w.n_rows) {
+        const DevRow& rw = pl.rows[w.row_off + j];
+        dsc[4 + j] = (pl.seqs[rw.seq].q_row0 + rw.qi) * c.hq_local + rw.qh;
+      } else {
+        dsc[4 + j] = -1;
+      }
+    }
+  }
   // combine rows: entry range and the row's B_v^h (one 16-byte load per output row)
   pl.comb_rows.assign(2 * n_out, 0);
   for (int64_t o = 0; o < n_out; ++o) {
@@ -419,6 +450,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   pl.off_trecs = put(pl.blob, pl.tile_recs);
   pl.off_irecs = put(pl.blob, pl.item_recs);
   pl.off_ssrc = put(pl.blob, pl.stage_src);
+  pl.off_sdesc = put(pl.blob, pl.stage_desc);
   pl.blob.resize(align256(pl.blob.size()));
   pl.ws_bytes = align256((size_t)pl.n_entries * (size_t)(k::kEntAcc + d + r) * sizeof(float));
   if (pl.kernel == 2) {
@@ -485,6 +517,7 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.item_recs = base + p.off_irecs;
   a.tc_rows = p.tc_rows;
   a.stage_src = (const int32_t*)(base + p.off_ssrc);
+  a.stage_desc = (const int4*)(base + p.off_sdesc);
   a.n_ctas = p.n_ctas;
   a.stage = p.kernel == 2 ? (uint8_t*)ws + p.stage_off : nullptr;
   cudaError_t e = cudaSuccess;

@@ -343,64 +343,49 @@ __global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_image
   const int ii = blockIdx.x;
   if (ii >= n_images) return;
   __shared__ __align__(16) float qs[16][kD];
-  const DevWarp w = p.warps[p.stage_src[ii]];
+  __shared__ int4 dsc[5];  // planner record: B_k^h address, n_rows, kv head, Q row of each of the 16 slot rows
   uint8_t* img = p.stage + (int64_t)ii * kStageBytes;
   const int tid = threadIdx.x;
-  const DevItem* dummy = nullptr;
-  (void)dummy;
-  // kv head of this slot: any row's q head / group (padding rows have seq < 0)
-  int h = 0;
-  {
-    const DevRow r0 = p.rows[w.row_off];
-    h = r0.qh / p.group;
-  }
+  if (tid < 5) dsc[tid] = p.stage_desc[5 * ii + tid];
+  __syncthreads();
+  const int n_rows = dsc[0].z;
+  const int* qrows = (const int*)&dsc[1];
+  const __nv_bfloat16* Bk = (const __nv_bfloat16*)(((uint64_t)(uint32_t)dsc[0].y << 32) | (uint32_t)dsc[0].x) +
+                            (int64_t)p.layer * p.adapter_layer_stride;
+  const bool def = p.rope_mode == FKV_ROPE_DEFERRED;
+  __shared__ __align__(16) float bs[kR][kD + 4];
+  // Q rows and B_k^h in flight together: 2 x 16-byte loads per thread per pass
   for (int c = tid; c < 16 * 16; c += 128) {
     const int row = c >> 4, ch = c & 15;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < w.n_rows) {
-      const DevRow rw = p.rows[w.row_off + row];
-      v = __ldg((const uint4*)((const __nv_bfloat16*)p.Q + ((int64_t)(p.seqs[rw.seq].q_row0 + rw.qi) * p.hq + rw.qh) * kD) +
-                ch);
-    }
+    if (row < n_rows) v = __ldg((const uint4*)((const __nv_bfloat16*)p.Q + (int64_t)qrows[row] * kD) + ch);
+    const int jj = c >> 4, n8 = (c & 15) * 8;  // B_k^h row jj (16 rows x 16 chunks, same index space)
+    const uint4 bv = __ldg((const uint4*)(Bk + jj * kD + (def ? perm_d(n8) : n8)));
     *(uint4*)(img + (ch >> 3) * 2048 + kmajor_off(row, (ch & 7) * 8, 8, 1024, 0)) = v;
-    const __nv_bfloat162* b2 = (const __nv_bfloat162*)&v;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(b2[e]);
-      qs[row][ch * 8 + 2 * e] = f.x;
-      qs[row][ch * 8 + 2 * e + 1] = f.y;
-    }
-  }
-  __syncthreads();
-  const __nv_bfloat16* Bk = (const __nv_bfloat16*)p.adapters[2 * w.adapter_slot] +
-                            (int64_t)p.layer * p.adapter_layer_stride + (int64_t)h * kR * kD;
-  if (p.rope_mode == FKV_ROPE_DEFERRED) {
-    for (int c = tid; c < kR * (kD / 8); c += 128) {
-      const int jj = c >> 4, n8 = (c & 15) * 8;
-      const uint4 v = __ldg((const uint4*)(Bk + jj * kD + perm_d(n8)));
-      *(uint4*)(img + 4096 + mnmajor_off(n8, jj, 4, 1024, 512)) = v;
-    }
-  } else {
-    // q~[row][j] = sum_d Q[row][d] B_k[j][d]: B_k^h (4 KB) through shared memory, 2 outputs per thread
-    __shared__ __align__(16) float bs[kR][kD + 4];
-    for (int c = tid; c < kR * kD / 8; c += 128) {
-      const int jj = c >> 4, d8 = (c & 15) * 8;
-      const uint4 bv = __ldg((const uint4*)(Bk + jj * kD + d8));
-      const __nv_bfloat162* b2 = (const __nv_bfloat162*)&bv;
+    const __nv_bfloat162* q2 = (const __nv_bfloat162*)&v;
+    const __nv_bfloat162* b2 = (const __nv_bfloat162*)&bv;
+    if (def) {
+      *(uint4*)(img + 4096 + mnmajor_off(n8, jj, 4, 1024, 512)) = bv;  // packed B_k image (RoPE partner order)
+    } else {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float2 b = __bfloat1622float2(b2[e]);
-        bs[jj][d8 + 2 * e] = b.x;
-        bs[jj][d8 + 2 * e + 1] = b.y;
+        const float2 f = __bfloat1622float2(q2[e]), b = __bfloat1622float2(b2[e]);
+        qs[row][ch * 8 + 2 * e] = f.x;
+        qs[row][ch * 8 + 2 * e + 1] = f.y;
+        bs[jj][n8 + 2 * e] = b.x;
+        bs[jj][n8 + 2 * e + 1] = b.y;
       }
     }
+  }
+  if (!def) {
+    // q~[row][j] = sum_d Q[row][d] B_k[j][d], 2 outputs per thread
     __syncthreads();
     for (int c = tid; c < 16 * kR; c += 128) {
       const int row = c >> 4, jj = c & 15;
       float acc = 0.f;
 #pragma unroll 8
       for (int dd = 0; dd < kD; ++dd) acc += qs[row][dd] * bs[jj][dd];
-      *(__nv_bfloat16*)(img + 4096 + kmajor_off(row, jj, 2, 256, 0)) = __float2bfloat16_rn(row < w.n_rows ? acc : 0.f);
+      *(__nv_bfloat16*)(img + 4096 + kmajor_off(row, jj, 2, 256, 0)) = __float2bfloat16_rn(row < n_rows ? acc : 0.f);
     }
   }
 }
