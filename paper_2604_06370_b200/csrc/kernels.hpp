@@ -108,6 +108,27 @@ constexpr int kStageBytes = 8192;
 // 128-byte-row TMA box and is an MMA operand as is (tcgen05 kernel, ra_tc.cu).
 __host__ __device__ __forceinline__ int res_col(int row, int j, int swz) { return swz ? (j ^ (((row >> 2) & 1) << 3)) : j; }  // per warp slot: Q image 4 KB + (q~ 512 B | packed B_k 4 KB)
 
+// Programmatic dependent launch (stream-ordered kernels of one layer): the kernel may be scheduled while its
+// predecessor drains; it runs griddepcontrol.wait (full completion + memory of the predecessor) before touching
+// anything the predecessor writes, then lets its own dependent launch (pdl_trigger).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 cudaError_t launch_attention_mma(const AttnParams& p, cudaStream_t s);
 cudaError_t launch_attention_simt(const AttnParams& p, cudaStream_t s);
 cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStream_t s);

@@ -43,6 +43,8 @@ __device__ __forceinline__ void copy_elems(void* dst, const void* src, int64_t n
 
 __global__ void kv_write_kernel(PoolView pv, int32_t layer, Runs<kMaxRuns> runs, int32_t n_runs, const uint8_t* kb,
                                 const uint8_t* vb, const uint8_t* rk, const uint8_t* rv, uint32_t mask) {
+  pdl_wait();
+  pdl_trigger();
   const int run = blockIdx.x;
   if (run >= n_runs) return;
   const WriteRun w = runs.r[run];
@@ -371,9 +373,8 @@ cudaError_t launch_kv_write(const PoolView& pv, int32_t layer, const WriteRun* r
   int maxn = 1;
   for (int i = 0; i < n_runs; ++i) maxn = max(maxn, runs[i].n);
   dim3 grid(n_runs, min(maxn, 16));
-  kv_write_kernel<<<grid, 128, 0, s>>>(pv, layer, rr, n_runs, (const uint8_t*)kb, (const uint8_t*)vb,
-                                       (const uint8_t*)rk, (const uint8_t*)rv, mask);
-  return cudaGetLastError();
+  return launch_pdl(kv_write_kernel, grid, dim3(128), 0, s, pv, layer, rr, n_runs, (const uint8_t*)kb,
+                    (const uint8_t*)vb, (const uint8_t*)rk, (const uint8_t*)rv, mask);
 }
 
 cudaError_t launch_cow_copy(const PoolView& pv, const CopyOp* ops, int32_t n_ops, cudaStream_t s) {
@@ -398,6 +399,8 @@ cudaError_t launch_synth_fill(void* dst, int32_t dtype, uint64_t seed, int32_t k
 // registers: all 2048-row C2 warps resident in one wave
 template <typename T>
 __global__ void __launch_bounds__(256, 2) combine128_kernel(AttnParams p) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= p.n_out_rows) return;
@@ -487,11 +490,8 @@ cudaError_t launch_combine(const AttnParams& p, cudaStream_t s) {
   const int threads = 256;
   const int blocks = (p.n_out_rows * 32 + threads - 1) / threads;
   if (p.d == 128 && p.r == 16 && ((uintptr_t)p.O & 15) == 0 && (p.entry_stride & 3) == 0) {
-    if (p.dtype == FKV_DTYPE_BF16)
-      combine128_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(p);
-    else
-      combine128_kernel<float><<<blocks, threads, 0, s>>>(p);
-    return cudaGetLastError();
+    if (p.dtype == FKV_DTYPE_BF16) return launch_pdl(combine128_kernel<__nv_bfloat16>, dim3(blocks), dim3(threads), 0, s, p);
+    return launch_pdl(combine128_kernel<float>, dim3(blocks), dim3(threads), 0, s, p);
   }
   if (p.dtype == FKV_DTYPE_BF16)
     combine_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(p);

@@ -337,9 +337,10 @@ __device__ __forceinline__ int perm_d(int n) {
 // d-halves, 2 KB each) and q~ = Q B_k^T (NONE, K-major SW32, 512 B) or B_k^h
 // with permuted columns (DEFERRED, MN-major SW64 quarter blocks, 4 KB).
 __global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_images) {
-  // the main kernel (programmatic dependent launch) may start its prologue and K/V streaming now; it waits for
-  // this grid's completion (griddepcontrol.wait) before it reads the staged images
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  // after the predecessor (kv_write: the pool rows) completed, the main kernel may start its prologue and K/V
+  // streaming; it waits for this grid's completion (griddepcontrol.wait) before it reads the staged images
+  pdl_wait();
+  pdl_trigger();
   const int ii = blockIdx.x;
   if (ii >= n_images) return;
   __shared__ __align__(16) float qs[16][kD];
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
   const long long t_start = clock64();
   const int cta = blockIdx.x;
   const bool dbg_on = p.dbg != nullptr && cta == p.dbg_block;
+  pdl_trigger();  // the combine kernel may be scheduled as CTAs drain (it waits for this grid's completion)
   const int it_begin = p.sched_ptr[cta], it_end = p.sched_ptr[cta + 1];
   const int n_my = it_end - it_begin;
   const int P = p.P;
@@ -1597,8 +1599,7 @@ cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStrea
 
 cudaError_t launch_stage(const AttnParams& p, int32_t n_images, cudaStream_t s) {
   if (n_images <= 0) return cudaSuccess;
-  ra_stage_kernel<<<n_images, 128, 0, s>>>(p, n_images);
-  return cudaGetLastError();
+  return launch_pdl(ra_stage_kernel, dim3(n_images), dim3(128), 0, s, p, n_images);
 }
 
 size_t tc_maps_bytes() { return sizeof(TcMaps); }
