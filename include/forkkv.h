@@ -203,7 +203,8 @@ fkv_status fkv_plan_get_info(const fkv_plan* plan, fkv_plan_info* info);
 fkv_status fkv_plan_upload(fkv_ctx* ctx, fkv_plan* plan, void* dev, size_t bytes, void* stream);
 /* ResidualAttention for one layer (Alg.1 + Eq.4):
  *   Q [n_rows_q][Hq_local][d], O same (rows = seqs in plan order, each its
- *   q_len rows), workspace >= info.workspace_bytes (fp32 partials).
+ *   q_len rows), workspace >= info.workspace_bytes (fp32 partials),
+ *   256-byte aligned (E_INVALID otherwise); O 16-byte aligned.
  * sm_scale <= 0 selects 1/sqrt(d) (C-4). Enqueued on `stream`. */
 fkv_status fkv_residual_attention(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
                                   float sm_scale, void* workspace, size_t ws_bytes, void* stream);

@@ -98,8 +98,8 @@ struct AttnParams {
   uint8_t* stage;  // per-warp-slot staged operand images (ws region, kStageBytes each)
   int32_t res_swz;  // residual rows stored in SW32 order (see res_col)
 };
-// partial entry: [m, l, pad, pad, acc[D], acc_r[r]] (acc 16-byte aligned: vector stores / loads)
-constexpr int kEntAcc = 4;
+// partial entry: [m, l, pad x 6, acc[D], acc_r[r]] (acc 32-byte aligned: 256-bit stores, vector loads)
+constexpr int kEntAcc = 8;
 constexpr int kStageBytes = 8192;
 
 // Residual page format (bf16, r = 16): row i of a page holds R[i][j] at column j ^ (8 * ((i >> 2) & 1)), i.e.

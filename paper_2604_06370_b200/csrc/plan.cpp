@@ -475,7 +475,7 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   if (p.generation != c.generation) throw Error(FKV_E_STALE, "attention: plan is stale");
   if (!p.dev) throw Error(FKV_E_INVALID, "attention: plan not uploaded");
   if (layer < 0 || layer >= c.cfg.n_layers || !Q || !O) throw Error(FKV_E_INVALID, "attention: bad layer/Q/O");
-  if (!ws || ws_bytes < p.ws_bytes || ((uintptr_t)ws & 15)) throw Error(FKV_E_INVALID, "attention: workspace too small");
+  if (!ws || ws_bytes < p.ws_bytes || ((uintptr_t)ws & 255)) throw Error(FKV_E_INVALID, "attention: workspace too small or not 256-byte aligned");
   const uint8_t* base = (const uint8_t*)p.dev;
   k::AttnParams a{};
   a.base_k = c.buf.base_k; a.base_v = c.buf.base_v; a.res_k = c.buf.res_k; a.res_v = c.buf.res_v;

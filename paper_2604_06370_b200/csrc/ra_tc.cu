@@ -314,6 +314,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                : "memory");
 }
 
+// 32 consecutive bytes (8 fp32 TMEM words) to global memory in one 256-bit store (sm_100)
+__device__ __forceinline__ void st_global_v8(float* dst, const uint32_t* x) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(x[0]), "r"(x[1]), "r"(x[2]),
+               "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7])
+               : "memory");
+}
+
 // diagnostics: clock64 stamp of pipeline event e for index j (< 256) of CTA dbg_block (fkv_debug_timeline)
 // (EV: the kernel-uniform dbg_on test first, so the stamps cost one predicated branch when off)
 #define EV(e, j)                 \
@@ -1073,10 +1080,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             }
             if (valid) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                *(float4*)(ent + 32 * part + 4 * i) =
-                    make_float4(__uint_as_float(x[4 * i]), __uint_as_float(x[4 * i + 1]), __uint_as_float(x[4 * i + 2]),
-                                __uint_as_float(x[4 * i + 3]));
+              for (int i = 0; i < 4; ++i) st_global_v8(ent + 32 * part + 8 * i, x + 8 * i);
             }
           }
         } else {
@@ -1119,17 +1123,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           for (int k = 0; k < 3; ++k) {
             const int col = 48 * q + 16 * k;  // warp-uniform
             if (col < kD) {
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                *(float4*)(ent + col + 4 * i) =
-                    make_float4(__uint_as_float(x[16 * k + 4 * i]), __uint_as_float(x[16 * k + 4 * i + 1]),
-                                __uint_as_float(x[16 * k + 4 * i + 2]), __uint_as_float(x[16 * k + 4 * i + 3]));
+              st_global_v8(ent + col, x + 16 * k);
+              st_global_v8(ent + col + 8, x + 16 * k + 8);
             } else if ((col - kD) / 16 == o) {
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                *(float4*)(ent + kD + 4 * i) =
-                    make_float4(__uint_as_float(x[16 * k + 4 * i]), __uint_as_float(x[16 * k + 4 * i + 1]),
-                                __uint_as_float(x[16 * k + 4 * i + 2]), __uint_as_float(x[16 * k + 4 * i + 3]));
+              st_global_v8(ent + kD, x + 16 * k);
+              st_global_v8(ent + kD + 8, x + 16 * k + 8);
             }
           }
         }
