@@ -10,4 +10,4 @@ timeout 900 python bench.py --config c4 --steps 2 --warmup 3 --no-e2e > gpurun_o
 timeout 400 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r/bench_c2_reference.json 2> gpurun_out/r/err_ref.txt
 timeout 400 ncu --set full --import-source on --clock-control none -k regex:ra_tc_kernel -s 3 -c 1 -o gpurun_out/r/prof_c2_none python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 400 ncu --set full --import-source on --clock-control none -k regex:ra_tc_kernel -s 3 -c 1 -o gpurun_out/r/prof_c2_deferred python bench.py --mode deferred --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ra_|combine_kernel" -s 96 -c 96 --csv --log-file gpurun_out/r/launches_c2_none.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ra_|combine" -s 96 -c 96 --csv --log-file gpurun_out/r/launches_c2_none.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
