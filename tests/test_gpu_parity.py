@@ -229,3 +229,16 @@ def test_many_splits_combine(mode, monkeypatch):
     assert pl.info.kernel == 2
     assert pl.info.n_items > 8 * 40, pl.info.n_items
     assert err <= TOL["bf16"], err
+
+
+@pytest.mark.parametrize("mode", ["none", "deferred"])
+def test_c2_full_size_sampled(mode):
+    """configs[1] at full size (32K shared prefix, 16 agents x 4 branches = 64 decode sequences, 32 q / 8 kv
+    heads, d 128, r 16, page 128): one layer of exactly the launch configuration bench.py times (same plan,
+    schedule and kernel variant), sampled sequences of every agent group against the fp64 oracle."""
+    scen = recipes.c2()
+    fkv = _ctx(scen, 1, 32, 8, 128, 16, 128, "bf16", mode, theta=500000.0, llama3=True)
+    driver.build(fkv, scen, seed=0)
+    err, pl = _run_and_check(fkv, scen, 0, 0, "bf16", mode, theta=500000.0, llama3=True, seqs=[0, 21, 42, 63])
+    assert pl.info.kernel == 2 and pl.info.n_items > 148
+    assert err <= TOL["bf16"], err
