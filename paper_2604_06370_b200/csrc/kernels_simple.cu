@@ -406,11 +406,9 @@ __global__ void __launch_bounds__(256, 2) combine128_kernel(AttnParams p) {
   if (warp >= p.n_out_rows) return;
   const longlong2 cr = p.comb_rows[warp];
   const int e0 = (int)(cr.x & 0xffffffffll), e1 = (int)(cr.x >> 32);
-  // B_v^h rows (16 x 128) for the late fusion, issued first: they do not depend on the partials
+  // B_v^h rows (16 x 128) for the late fusion: prefetched into L1 now (one 128-byte line per lane), read at the end
   const T* bv = (const T*)cr.y + (int64_t)p.layer * p.adapter_layer_stride;
-  uint2 bvu[16];  // bf16: 4 elements; f32: elements 4l, 4l+1 (the other two re-read at the end)
-#pragma unroll
-  for (int j = 0; j < 16; ++j) bvu[j] = __ldg((const uint2*)(bv + j * 128 + 4 * lane));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)bv + 128 * lane * (int)sizeof(T) / 2));
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   float accr = 0.f, l = 0.f, Mrun = -INFINITY;
   for (int eb = e0; eb < e1; eb += 32) {
@@ -418,11 +416,11 @@ __global__ void __launch_bounds__(256, 2) combine128_kernel(AttnParams p) {
     const int my_e = lane < ne ? p.out_entries[eb + lane] : 0;
     const float* my = p.ws + (int64_t)my_e * p.entry_stride;
     const float2 ml = lane < ne ? *(const float2*)my : make_float2(-INFINITY, 0.f);
-    for (int i0 = 0; i0 < ne; i0 += 8) {
-      float4 v[8];
-      float vr[8];
+    for (int i0 = 0; i0 < ne; i0 += 16) {
+      float4 v[16];
+      float vr[16];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {  // the batch's loads first (they do not depend on the weights)
+      for (int k = 0; k < 16; ++k) {  // the batch's loads first (they do not depend on the weights)
         const int e = __shfl_sync(0xffffffffu, my_e, i0 + k < ne ? i0 + k : ne - 1);
         const float* ent = p.ws + (int64_t)e * p.entry_stride + kEntAcc;
         v[k] = *(const float4*)(ent + 4 * lane);
@@ -449,7 +447,7 @@ __global__ void __launch_bounds__(256, 2) combine128_kernel(AttnParams p) {
         l += lsum;
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < 16; ++k) {
         const float w = i0 + k < ne ? __shfl_sync(0xffffffffu, wi, i0 + k) : 0.f;
         if (w != 0.f) {  // an entry with l = 0 may hold non-finite accumulators
           acc.x += w * v[k].x; acc.y += w * v[k].y; acc.z += w * v[k].z; acc.w += w * v[k].w;
@@ -459,6 +457,9 @@ __global__ void __launch_bounds__(256, 2) combine128_kernel(AttnParams p) {
     }
   }
   // late fusion: O = (acc + acc_r . B_v^h) / l   (Alg1.349-350)
+  uint2 bvu[16];  // bf16: 4 elements; f32: elements 4l, 4l+1 (the other two below)
+#pragma unroll
+  for (int j = 0; j < 16; ++j) bvu[j] = __ldg((const uint2*)(bv + j * 128 + 4 * lane));
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const float a = __shfl_sync(0xffffffffu, accr, j);
