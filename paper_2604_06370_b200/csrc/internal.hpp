@@ -179,6 +179,7 @@ struct Plan {
   std::vector<int32_t> tile_ptr, tile_recs;      // per-CTA tile records (8 ints each, see kernels.hpp)
   std::vector<uint8_t> item_recs;                // per-item k::ItemRecT
   std::vector<int32_t> stage_src;                // staged image -> source warp slot
+  bool l2_evict_first = false;                   // see AttnParams::l2_evict_first
   std::vector<int32_t> stage_desc;               // per image: B_k^h address (2 ints), n_rows, h, Q row index [16]
   int32_t n_ctas = 0;
   size_t stage_off = 0;  // workspace offset of the staged operand images (tcgen05 kernel)

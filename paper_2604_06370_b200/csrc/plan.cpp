@@ -16,6 +16,7 @@
 #include <cstring>
 #include <array>
 #include <map>
+#include <tuple>
 #include <set>
 #include <string>
 #include <unordered_map>
@@ -190,6 +191,15 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
       }
       if (!cta_warps.empty()) ctas.push_back({h, k0, k1, (int32_t)base_off[sg.members[0]], cta_warps});
     }
+  }
+  // L2 policy of the base tiles: evict-first when each (segment, kv head) tile is read by <= 4 row blocks (decode
+  // batches), normal when many row blocks reuse it (prefill chunks, large agent counts); FKV_L2_EVICT=0/1 forces
+  {
+    std::map<std::tuple<int64_t, int32_t, int32_t>, int32_t> readers;  // (segment start, base pages, kv head)
+    int32_t most = 0;
+    for (const Cta& ct : ctas) most = std::max(most, ++readers[std::make_tuple(ct.k0, ct.base_off, ct.kv_head)]);
+    const char* eenv = getenv("FKV_L2_EVICT");
+    pl.l2_evict_first = eenv ? atoi(eenv) != 0 : most <= 4;
   }
   // key split. mma.sync / SIMT: ~2 waves of CTAs over the SMs. tcgen05 (persistent, one CTA per SM):
   // pieces of about half the average per-CTA load, so the greedy schedule below balances.
@@ -516,6 +526,7 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.tile_recs = (const int4*)(base + p.off_trecs);
   a.item_recs = base + p.off_irecs;
   a.tc_rows = p.tc_rows;
+  a.l2_evict_first = p.l2_evict_first ? 1 : 0;
   a.stage_src = (const int32_t*)(base + p.off_ssrc);
   a.stage_desc = (const int4*)(base + p.off_sdesc);
   a.n_ctas = p.n_ctas;

@@ -522,8 +522,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
                 mbar_expect_tx(bar, 32768);
                 // base tiles stream through L2 evict-first: the residual pages (reused by every kv head) and
                 // the other row blocks' hits keep their lines (measured +2.6% on C2)
-                tma_load_3d_hint(sbase + C::OFF_K + k_unit(nk, 0) * 16384, &maps.kb, 0, base_row(kR_), 0, bar,
-                                 l2_policy_evict_first());
+                if (p.l2_evict_first)
+                  tma_load_3d_hint(sbase + C::OFF_K + k_unit(nk, 0) * 16384, &maps.kb, 0, base_row(kR_), 0, bar,
+                                   l2_policy_evict_first());
+                else
+                  tma_load_3d(sbase + C::OFF_K + k_unit(nk, 0) * 16384, &maps.kb, 0, base_row(kR_), 0, bar);
               } else {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -961,7 +964,10 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               EV(7, nv);
               const uint32_t bar = smem_u32(&ms.vfull[slot]);
               mbar_expect_tx(bar, 16384);
-              tma_load_3d_hint(sbase + C::OFF_V + slot * C::VE, &maps.vb, 0, vrow + 64 * h, 0, bar, l2_policy_evict_first());
+              if (p.l2_evict_first)
+                tma_load_3d_hint(sbase + C::OFF_V + slot * C::VE, &maps.vb, 0, vrow + 64 * h, 0, bar, l2_policy_evict_first());
+              else
+                tma_load_3d(sbase + C::OFF_V + slot * C::VE, &maps.vb, 0, vrow + 64 * h, 0, bar);
             }
             const uint32_t dst = sbase + C::OFF_V + slot * C::VE + 16384;
 #pragma unroll
