@@ -224,29 +224,28 @@ __device__ __forceinline__ bool bar_or(uint32_t id, uint32_t n, bool pred) {
   return r != 0;
 }
 
-// ---- packed fp32x2 helpers (FFMA2 / FMUL2 on sm_100) ----
-__device__ __forceinline__ uint64_t f2(float a, float b) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+// ---- packed fp32x2 helpers (FFMA2 / FADD2 / FMUL2 on sm_100): the CUDA builtins, so the register allocator
+// sees the pairs (no inline-asm moves); a pair travels as one 64-bit value
+__device__ __forceinline__ float2 as_f2(uint64_t v) {
+  float2 r;
+  memcpy(&r, &v, 8);
   return r;
 }
+__device__ __forceinline__ uint64_t as_u64(float2 v) {
+  uint64_t r;
+  memcpy(&r, &v, 8);
+  return r;
+}
+__device__ __forceinline__ uint64_t f2(float a, float b) { return as_u64(make_float2(a, b)); }
 __device__ __forceinline__ void uf2(uint64_t v, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  const float2 f = as_f2(v);
+  a = f.x;
+  b = f.y;
 }
-__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) { return as_u64(__fmul2_rn(as_f2(a), as_f2(b))); }
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) { return as_u64(__fadd2_rn(as_f2(a), as_f2(b))); }
 __device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
+  return as_u64(__ffma2_rn(as_f2(a), as_f2(b), as_f2(c)));
 }
 __device__ __forceinline__ uint32_t pack2(uint64_t v) {
   float a, b;
