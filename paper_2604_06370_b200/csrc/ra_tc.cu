@@ -342,7 +342,7 @@ __device__ __forceinline__ int perm_d(int n) {
 // memory images the main kernel bulk-copies: Q rows (K-major SW128, both
 // d-halves, 2 KB each) and q~ = Q B_k^T (NONE, K-major SW32, 512 B) or B_k^h
 // with permuted columns (DEFERRED, MN-major SW64 quarter blocks, 4 KB).
-__global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_images) {
+__global__ void __launch_bounds__(256) ra_stage_kernel(AttnParams p, int n_images) {
   // after the predecessor (kv_write: the pool rows) completed, the main kernel may start its prologue and K/V
   // streaming; it waits for this grid's completion (griddepcontrol.wait) before it reads the staged images
   pdl_wait();
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_image
   const bool def = p.rope_mode == FKV_ROPE_DEFERRED;
   __shared__ __align__(16) float bs[kR][kD + 4];
   // Q rows and B_k^h in flight together: 2 x 16-byte loads per thread per pass
-  for (int c = tid; c < 16 * 16; c += 128) {
+  for (int c = tid; c < 16 * 16; c += 256) {  // one 16-byte Q chunk and one B_k chunk per thread
     const int row = c >> 4, ch = c & 15;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (row < n_rows) v = __ldg((const uint4*)((const __nv_bfloat16*)p.Q + (int64_t)qrows[row] * kD) + ch);
@@ -385,13 +385,20 @@ __global__ void __launch_bounds__(128) ra_stage_kernel(AttnParams p, int n_image
     }
   }
   if (!def) {
-    // q~[row][j] = sum_d Q[row][d] B_k[j][d], 2 outputs per thread
+    // q~[row][j] = sum_d Q[row][d] B_k[j][d], one output per thread (paired FFMA2 over d)
     __syncthreads();
-    for (int c = tid; c < 16 * kR; c += 128) {
-      const int row = c >> 4, jj = c & 15;
-      float acc = 0.f;
+    {
+      const int c = tid, row = c >> 4, jj = c & 15;
+      uint64_t acc2 = 0;
 #pragma unroll 8
-      for (int dd = 0; dd < kD; ++dd) acc += qs[row][dd] * bs[jj][dd];
+      for (int dd = 0; dd < kD; dd += 4) {
+        const float4 qv = *(const float4*)&qs[row][dd], bv4 = *(const float4*)&bs[jj][dd];
+        acc2 = fma2(f2(qv.x, qv.y), f2(bv4.x, bv4.y), acc2);
+        acc2 = fma2(f2(qv.z, qv.w), f2(bv4.z, bv4.w), acc2);
+      }
+      float a0, a1;
+      uf2(acc2, a0, a1);
+      const float acc = a0 + a1;
       *(__nv_bfloat16*)(img + 4096 + kmajor_off(row, jj, 2, 256, 0)) = __float2bfloat16_rn(row < n_rows ? acc : 0.f);
     }
   }
@@ -1605,7 +1612,7 @@ cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStrea
 
 cudaError_t launch_stage(const AttnParams& p, int32_t n_images, cudaStream_t s) {
   if (n_images <= 0) return cudaSuccess;
-  return launch_pdl(ra_stage_kernel, dim3(n_images), dim3(128), 0, s, p, n_images);
+  return launch_pdl(ra_stage_kernel, dim3(n_images), dim3(256), 0, s, p, n_images);
 }
 
 size_t tc_maps_bytes() { return sizeof(TcMaps); }
