@@ -306,7 +306,8 @@ def run_ours(args):
                     fkv.write_kv(layer, batch, starts, ones, host["dkb"], host["dvb"], host["drk"], host["drv"])
                     state["launches"] += 1
                 fkv.residual_attention_host(pl, layer, host["q"][layer], host["o"][layer], host["dq"], host["do"])
-            state["launches"] += 2
+            # tcgen05 path: stager + main kernel + combine; mma.sync / SIMT: main kernel + combine
+            state["launches"] += 3 if pl.info.kernel == 2 else 2
         return pl
 
     for _ in range(args.warmup):
