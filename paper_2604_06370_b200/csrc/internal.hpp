@@ -114,6 +114,8 @@ struct Ctx {
   std::unordered_map<int32_t, int32_t> adapter_slot;
   uint64_t generation = 1;
   bool has_tc_maps = false;
+  bool has_rows_maps = false;
+  std::vector<uint8_t> rows_maps;  // k::RowsMaps (ra_rows.cu)
   std::vector<uint8_t> tc_maps;  // 5 CUtensorMap (base K, base V, R_k, R_v, K d-halves) for the tcgen05 kernel
   std::string last_error;
   size_t elem = 2;
@@ -159,11 +161,17 @@ struct DevRow {         // query row: (seq, query index, local q head)
   int32_t pos;          // absolute position of the query (causal limit)
 };
 
+// a maximal run of page slots [slot0, slot1) over which the member sequences hold the same base pages
+struct PlanSeg {
+  int64_t slot0, slot1;
+  std::vector<int32_t> members;  // plan seq indices
+};
+
 struct Plan {
   uint64_t generation = 0;
   int32_t n_seqs = 0;
   int64_t n_rows_q = 0;  // total query rows (sum q_len)
-  int32_t kernel = 0;    // 0 mma grouped, 1 simt, 2 tcgen05
+  int32_t kernel = 0;    // 0 mma grouped, 1 simt, 2 tcgen05 (keys on lanes, round 1), 3 tcgen05 rows on lanes
   int32_t tc_rows = 64;  // tcgen05: query rows per CTA
   std::vector<DevSeq> seqs;
   std::vector<int32_t> base_pages, res_pages;
@@ -184,6 +192,9 @@ struct Plan {
   int32_t n_ctas = 0;
   size_t stage_off = 0;  // workspace offset of the staged operand images (tcgen05 kernel)
   int64_t n_segments = 0, n_entries = 0, key_tiles = 0, alg_bytes = 0;
+  // rows-on-lanes tcgen05 kernel (kernel 3): k::RItem / RWu / RTile / RRow records (rows.hpp)
+  std::vector<uint8_t> r_items, r_wus, r_tiles, r_rows;
+  size_t off_ritems = 0, off_rwus = 0, off_rtiles = 0, off_rrows = 0;
   // device layout (offsets into the uploaded blob)
   std::vector<uint8_t> blob;
   size_t off_seqs = 0, off_base = 0, off_res = 0, off_items = 0, off_warps = 0, off_rows = 0, off_outptr = 0,
@@ -203,6 +214,10 @@ void write_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int
               const void* kb, const void* vb, const void* rk, const void* rv, uint32_t mask, void* stream);
 void release(Ctx& c, int64_t a);
 std::string dump(const Ctx& c);
+
+// plan_rows.cpp: items / WUs / tiles / rows, partial entries, combine CSR and schedule of kernel 3
+void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const std::vector<const Agent*>& ags,
+                     const std::vector<int64_t>& base_off, const std::vector<int64_t>& res_off, int sms);
 
 // plan.cpp
 Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags);

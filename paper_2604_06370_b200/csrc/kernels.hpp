@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "internal.hpp"
+#include "rows.hpp"
 
 namespace fkv {
 namespace k {
@@ -136,6 +137,7 @@ cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStrea
 cudaError_t launch_stage(const AttnParams& p, int32_t n_warps, cudaStream_t s);
 size_t tc_maps_bytes();
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t s);
+cudaError_t launch_attention_rows(const RowsParams& p, const RowsMaps& maps, cudaStream_t s);
 
 cudaError_t launch_synth_fill(void* dst, int32_t dtype, uint64_t seed, int32_t kind, uint64_t owner, int32_t layer,
                               int64_t pos0, int32_t n_pos, int32_t head0, int32_t n_head, int32_t n_col, float scale,

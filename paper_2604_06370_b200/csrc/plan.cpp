@@ -29,10 +29,7 @@ namespace fkv {
 namespace {
 constexpr int kRowsPerWarp = 16;
 
-struct Seg {
-  int64_t slot0, slot1;
-  std::vector<int32_t> members;  // plan seq indices
-};
+using Seg = PlanSeg;
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -56,7 +53,14 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   const bool tc_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && c.has_tc_maps && (128 % P) == 0 &&
                      P >= 8 && !(flags & (FKV_PLAN_FORCE_SIMT | FKV_PLAN_FORCE_MMA));
   const bool mma_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && !(flags & FKV_PLAN_FORCE_SIMT);
-  pl.kernel = tc_ok ? 2 : (mma_ok ? 0 : 1);
+  // rows-on-lanes tcgen05 kernel (kernel 3, ra_rows.cu): NONE residual-RoPE mode, pages of 16..128 tokens
+  const bool rows_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && c.has_rows_maps && (128 % P) == 0 &&
+                       P >= 16 && c.cfg.rope_mode == FKV_ROPE_NONE && !(flags & (FKV_PLAN_FORCE_SIMT | FKV_PLAN_FORCE_MMA));
+  pl.kernel = rows_ok ? 3 : (tc_ok ? 2 : (mma_ok ? 0 : 1));
+  if (const char* kenv = getenv("FKV_KERNEL")) {
+    const int kk = atoi(kenv);
+    if (kk == 2 && tc_ok) pl.kernel = 2;
+  }
   // tcgen05: 64 query rows per CTA. NONE also has a 128-row variant (FKV_TC_ROWS=128): every MMA instruction then
   // covers N = 128 rows (a tcgen05.mma costs ~120 cycles for any N <= 128, tools/ubench_mma.cu), but its key warps
   // (64 columns each, SIMT row sums, single P^T buffer) are the bottleneck today, so it is not the default;
@@ -129,6 +133,15 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
     }
   }
   pl.n_segments = (int64_t)segs.size();
+  int sms = 148;
+  if (c.device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, c.cfg.device) == cudaSuccess && v > 0) sms = v;
+  }
+  if (pl.kernel == 3) {
+    build_rows_plan(c, pl, segs, ags, base_off, res_off, sms);
+    return plan.release();
+  }
 
   // ---- rows -> owner groups -> warps -> CTAs -> key splits ------------------
   struct Cta {
@@ -203,11 +216,6 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   }
   // key split. mma.sync / SIMT: ~2 waves of CTAs over the SMs. tcgen05 (persistent, one CTA per SM):
   // pieces of about half the average per-CTA load, so the greedy schedule below balances.
-  int sms = 148;
-  if (c.device) {
-    int v = 0;
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, c.cfg.device) == cudaSuccess && v > 0) sms = v;
-  }
   int64_t total_tiles = 0;
   for (const Cta& ct : ctas) total_tiles += (ct.k1 - ct.k0 + kTileKeys - 1) / kTileKeys;
   int64_t split_tiles;
@@ -534,6 +542,33 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.n_ctas = p.n_ctas;
   a.stage = p.kernel == 2 ? (uint8_t*)ws + p.stage_off : nullptr;
   cudaError_t e = cudaSuccess;
+  if (p.kernel == 3) {
+    if (phases & FKV_PHASE_MAIN) {
+      k::RowsParams rp{};
+      rp.base_k = c.buf.base_k; rp.base_v = c.buf.base_v; rp.res_k = c.buf.res_k; rp.res_v = c.buf.res_v;
+      rp.Q = Q; rp.ws = (float*)ws;
+      rp.items = (const k::RItem*)(base + p.off_ritems);
+      rp.wus = (const k::RWu*)(base + p.off_rwus);
+      rp.tiles = (const k::RTile*)(base + p.off_rtiles);
+      rp.rows = (const k::RRow*)(base + p.off_rrows);
+      rp.base_pages = a.base_pages;
+      rp.res_pages = a.res_pages;
+      rp.adapters = a.adapters;
+      rp.sched_ptr = a.sched_ptr;
+      rp.sched_items = a.sched_items;
+      rp.base_rows_layer = (int64_t)layer * c.cfg.n_base_pages * c.hkv_local * P;
+      rp.res_layer_elems = a.res_layer_stride;
+      rp.adapter_layer_elems = a.adapter_layer_stride;
+      rp.layer = layer; rp.hkv = c.hkv_local; rp.P = (int32_t)P; rp.n_ctas = p.n_ctas;
+      rp.entry_stride = a.entry_stride;
+      rp.scale_log2 = a.scale_log2;
+      rp.dbg = a.dbg; rp.dbg_block = a.dbg_block;
+      e = k::launch_attention_rows(rp, *(const k::RowsMaps*)c.rows_maps.data(), (cudaStream_t)stream);
+    }
+    if (e == cudaSuccess && (phases & FKV_PHASE_COMBINE)) e = k::launch_combine(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("attention: ") + cudaGetErrorString(e));
+    return;
+  }
   if ((phases & FKV_PHASE_MAIN) && p.kernel == 2) e = k::launch_stage(a, (int32_t)p.stage_src.size(), (cudaStream_t)stream);
   if (e == cudaSuccess && (phases & FKV_PHASE_MAIN))
     e = p.kernel == 2   ? k::launch_attention_tc(a, c.tc_maps.data(), (cudaStream_t)stream)

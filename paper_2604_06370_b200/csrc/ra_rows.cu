@@ -1,0 +1,623 @@
+// ResidualAttention on 5th-generation tensor cores, query rows on the TMEM lanes (bf16 in / fp32 accumulate,
+// d = 128, r = 16): the hot loop of §8(a) rows a5 (decode) and a7 (chunked prefill), NONE residual-RoPE mode
+// (the north-star split, C-1). One persistent CTA per SM walks a static list of plan items
+// (rows.hpp); every item holds up to 128 query rows (TMEM lane = row) and a sequence of 128-key tiles.
+//
+// Per tile (Alg1.332-346 with the split of Eq.4 applied to K and V):
+//   S       = Q K_base^T                                  8 x tcgen05.mma M=128 N=keys K=16   [SS]
+//   S      += q~_s R_k,s^T   for every residual slot s     1 x MMA per slot, output lanes = the slot's rows
+//             (q~ = Q B_k^T per row, computed once per item on the CUDA cores of the aux warpgroup)
+//   softmax: per row (thread = lane), lazily rescaled online max (threshold 2^8), P (bf16) back into TMEM
+//   O      += P V_base                                    TS MMA (A = P from TMEM), N = 128
+//   A_r    += P [R_v,0 | ... | R_v,n-1]                    TS MMA, N = 16 n (stacked slots; each row keeps its
+//                                                           own slot's 16 columns, Eq.4 late fusion)
+// The combine kernel merges the per-item partials (m, l, O, A_r) and applies O = (acc + acc_r B_v) / l
+// (Alg1.348-350) once per output row.
+//
+// Warp roles (384 threads):
+//   warps 0-3  softmax (thread = row = TMEM lane)
+//   warp  4    MMA issuer (one thread)
+//   warp  5    K_base / V_base loader (TMA tensor boxes)
+//   warp  6    R_k loader (bulk copies of residual pages: the page format is the SW32 K-major operand)
+//   warp  7    R_v loader (16-byte cp.async, 64-key halves of each slot's page)
+//   warps 8-11 aux: q~ of the next item, Q image of the next item (cp.async), epilogue (TMEM -> partial entries)
+//
+// Shared memory: Q image 32 KB (SW128 K-major) | q~ images 2 x 4 KB (SW32 K-major) | ring of kNU 16-KB units
+// (per tile, in MMA consumption order: K d-half 0, K d-half 1, R_k slots 0-3, [R_k slots 4-7] for S; V keys
+// 0-63, R_v keys 0-63, [V keys 64-127, R_v keys 64-127] for PV) | barriers, per-row (m, l) hand-off.
+// TMEM (512 columns): S/P buffer 0 [0,128), S/P buffer 1 [128,256), O [256,384), A_r [384,512).
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+#include "rows.hpp"
+#include "sm100.cuh"
+
+namespace fkv {
+namespace k {
+namespace {
+using namespace sm100;
+
+constexpr int kNU = 11;  // ring units
+constexpr uint32_t kUnit = 16384;
+constexpr uint32_t OFF_Q = 0, OFF_QT = 32768, OFF_RING = 40960;
+constexpr uint32_t OFF_BAR = OFF_RING + kNU * kUnit;
+constexpr uint32_t T_O = 256, T_AR = 384;
+constexpr int kThreads = 384;
+
+struct Bars {
+  uint64_t full[kNU], empty[kNU];
+  uint64_t s_full[2], p_full[2], o_done, o_final, o_free, q_full, q_empty, qt_full[2], ml_full[2];
+  uint32_t tmem_base;
+  uint32_t pad_;
+  float2 ml[2][kRowsLanes];
+};
+constexpr uint32_t kSmemBytes = OFF_BAR + sizeof(Bars);
+static_assert(kSmemBytes <= 232448, "shared memory");
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+// arrive on `bar` once this thread's prior cp.async copies have landed (pending count +1 now, -1 then)
+__device__ __forceinline__ void cp_async_arrive_inc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+// D (+)= A[smem] B[smem]; lanes with a set bit in `dis` keep their D (disable-output-lane)
+__device__ __forceinline__ void mma_ss_m(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc, uint4 dis) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc), "r"(dis.x), "r"(dis.y), "r"(dis.z), "r"(dis.w));
+}
+// D (+)= A[tmem] B[smem], lane-masked
+__device__ __forceinline__ void mma_ts_m(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc, uint4 dis) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(id), "r"(acc), "r"(dis.x), "r"(dis.y), "r"(dis.z), "r"(dis.w));
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// Units of a tile's K side (S) and V side (PV), in ring order.
+__device__ __forceinline__ int n_kside(int n_slots) { return n_slots > 4 ? 4 : 3; }
+__device__ __forceinline__ int n_vside(int n_keys) { return n_keys > 64 ? 4 : 2; }
+
+// Walk the CTA's items in MMA consumption order: S(0), S(1) PV(0), S(2) PV(1), ..., PV(n-1) per item.
+// f(kind, item_idx, item_ord, t, tile_index, last_in_item): kind 0 = K side of tile t, 1 = V side of tile t.
+template <class F>
+__device__ __forceinline__ void walk(const RowsParams& p, F&& f) {
+  const int i0 = p.sched_ptr[blockIdx.x], i1 = p.sched_ptr[blockIdx.x + 1];
+  for (int ii = i0; ii < i1; ++ii) {
+    const RItem it = p.items[p.sched_items[ii]];
+    for (int t = 0; t < it.n_tiles; ++t) {
+      f(0, ii - i0, t, it.tile0 + t, it.n_tiles);
+      if (t > 0) f(1, ii - i0, t - 1, it.tile0 + t - 1, it.n_tiles);
+    }
+    f(1, ii - i0, it.n_tiles - 1, it.tile0 + it.n_tiles - 1, it.n_tiles);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    ra_rows_kernel(const __grid_constant__ RowsParams p, const __grid_constant__ RowsMaps maps) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  Bars& B = *reinterpret_cast<Bars*>(smem + OFF_BAR);
+  const uint32_t sb = smem_u32(smem);
+  if (tid == 0) {
+    for (int i = 0; i < kNU; ++i) {
+      mbar_init(smem_u32(&B.full[i]), 1);
+      mbar_init(smem_u32(&B.empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&B.s_full[i]), 1);
+      mbar_init(smem_u32(&B.p_full[i]), 4);
+      mbar_init(smem_u32(&B.qt_full[i]), 4);
+      mbar_init(smem_u32(&B.ml_full[i]), 4);
+    }
+    mbar_init(smem_u32(&B.o_done), 1);
+    mbar_init(smem_u32(&B.o_final), 1);
+    mbar_init(smem_u32(&B.o_free), 4);
+    mbar_init(smem_u32(&B.q_full), 4);
+    mbar_init(smem_u32(&B.q_empty), 1);
+    fence_mbar_init();
+  }
+  // zero the operand buffers once: stale shared memory must hold finite values (keys beyond a ragged tile
+  // and empty Q rows are multiplied by zero probabilities / never read, but NaN * 0 would poison a row)
+  for (uint32_t i = tid; i < OFF_BAR / 16; i += kThreads) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  fence_async_smem();
+  if (wid == 4) tmem_alloc(smem_u32(&B.tmem_base), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = B.tmem_base;
+  // the kernel is a programmatic dependent launch: the pools (kv_write) and Q are the predecessor's outputs
+  pdl_wait();
+  const int n_my = p.sched_ptr[blockIdx.x + 1] - p.sched_ptr[blockIdx.x];
+  // register budget per warpgroup (setmaxnreg at the top of each role): softmax 232, loaders / MMA 56, aux 216
+  // (x 128 threads = 64512 registers = the CTA allocation of 168 x 384: more would deadlock setmaxnreg.inc)
+
+  if (wid < 4) {
+    // ============================ softmax warpgroup: thread = query row = TMEM lane ============================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    const uint32_t lane_base = (uint32_t)(32 * wid) << 16;
+    const int row = tid;
+    int g = 0;
+    for (int io = 0; io < n_my; ++io) {
+      const RItem it = p.items[p.sched_items[p.sched_ptr[blockIdx.x] + io]];
+      const RRow rr = p.rows[it.row0 + row];
+      float m_run = -INFINITY, l = 0.f;
+      RTile T = p.tiles[it.tile0];
+      for (int t = 0; t < it.n_tiles; ++t, ++g) {
+        const uint32_t lw = __ldg(&p.wus[T.wu].lanes[wid]);
+        const int b = g & 1;
+        RTile Tn;
+        if (t + 1 < it.n_tiles) Tn = p.tiles[it.tile0 + t + 1];
+        mbar_wait(smem_u32(&B.s_full[b]), (g >> 1) & 1);
+        tc_fence_after();
+        if (lw != 0u) {
+          const bool active = (lw >> lane) & 1u;
+          const uint32_t ts = tm + lane_base + 128u * b;
+          uint32_t sr[128];
+          FKV_TMEM_LD32(ts + 0, (sr + 0));
+          FKV_TMEM_LD32(ts + 32, (sr + 32));
+          FKV_TMEM_LD32(ts + 64, (sr + 64));
+          FKV_TMEM_LD32(ts + 96, (sr + 96));
+          tmem_ld_wait();
+          int limit = T.n_keys;
+          if (T.flags & kTileCausal) limit = min(limit, rr.pos - T.key0 + 1);
+          if (__any_sync(0xffffffffu, limit < 128)) {
+#pragma unroll
+            for (int c = 0; c < 128; ++c)
+              if (c >= limit) sr[c] = __float_as_uint(-INFINITY);
+          }
+          float mx;
+          {
+            float m4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float a = __uint_as_float(sr[32 * q]);
+#pragma unroll
+              for (int c = 1; c < 31; c += 2)
+                a = max3(a, __uint_as_float(sr[32 * q + c]), __uint_as_float(sr[32 * q + c + 1]));
+              m4[q] = fmaxf(a, __uint_as_float(sr[32 * q + 31]));
+            }
+            mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * p.scale_log2;
+          }
+          const bool need = active && mx > m_run + 8.f;
+          const bool resc = need && m_run != -INFINITY;
+          const float m_new = need ? mx : m_run;
+          const float alpha = resc ? ex2(m_run - m_new) : 1.f;
+          if (__any_sync(0xffffffffu, resc)) {
+            // O and A_r of this warp's rows were last written by PV of the previous tile
+            mbar_wait(smem_u32(&B.o_done), (g - 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c0 = 0; c0 < 256; c0 += 32) {
+              uint32_t o[32];
+              FKV_TMEM_LD32(tm + lane_base + T_O + c0, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+              FKV_TMEM_ST16(tm + lane_base + T_O + c0, o);
+              FKV_TMEM_ST16(tm + lane_base + T_O + c0 + 16, (o + 16));
+              tmem_st_wait();
+            }
+          }
+          if (active) {
+            m_run = m_new;
+            l *= alpha;
+          }
+          // p = 2^(s * scale_log2 - m): packed fp32x2 FMA, MUFU ex2, bf16 pairs back into the S columns
+          const float2 sl2 = make_float2(p.scale_log2, p.scale_log2);
+          const float2 nm2 = make_float2(-m_run, -m_run);
+          float2 acc2 = make_float2(0.f, 0.f);
+          uint32_t pk[64];
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sl2, nm2);
+            x.x = ex2(x.x);
+            x.y = ex2(x.y);
+            acc2 = __fadd2_rn(acc2, x);
+            pk[c] = pack_bf16x2(x.x, x.y);
+          }
+          FKV_TMEM_ST16(ts + 0, (pk + 0));
+          FKV_TMEM_ST16(ts + 16, (pk + 16));
+          FKV_TMEM_ST16(ts + 32, (pk + 32));
+          FKV_TMEM_ST16(ts + 48, (pk + 48));
+          tmem_st_wait();
+          if (active) l += acc2.x + acc2.y;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&B.p_full[b]));
+        if (t + 1 < it.n_tiles) T = Tn;
+      }
+      B.ml[io & 1][row] = make_float2(m_run, l);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&B.ml_full[io & 1]));
+    }
+  } else if (wid < 8) {
+   asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+   if (wid == 4) {
+    // ==================================== MMA issuer (one thread) ====================================
+    if (lane == 0) {
+      uint32_t u = 0;
+      int g = 0;  // S tiles issued
+      int gp = 0; // PV tiles issued
+      const uint32_t qdesc_lo = (sb + OFF_Q);
+      walk(p, [&](int kind, int io, int t, int ti, int n_tiles) {
+        const RTile T = p.tiles[ti];
+        struct { uint32_t lanes[4]; int32_t n_slots; } W;
+        {
+          const uint4 lw = __ldg(reinterpret_cast<const uint4*>(p.wus[T.wu].lanes));
+          W.lanes[0] = lw.x; W.lanes[1] = lw.y; W.lanes[2] = lw.z; W.lanes[3] = lw.w;
+          W.n_slots = __ldg(&p.wus[T.wu].n_slots);
+        }
+        if (kind == 0) {
+          // ---------------------------------- S = Q K^T + q~ R_k^T ----------------------------------
+          if (t == 0) {
+            mbar_wait(smem_u32(&B.q_full), io & 1);
+            fence_async_smem();
+          }
+          const int ns = (T.n_keys + 15) & ~15;
+          const uint32_t idS = idesc_bf16(128, ns, false, false);
+          const uint32_t dS = tm + 128u * (g & 1);
+          const uint4 none = make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t s_ = u % kNU;
+            mbar_wait(smem_u32(&B.full[s_]), (u / kNU) & 1);
+            tc_fence_after();
+            const uint32_t kb = sb + OFF_RING + s_ * kUnit;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_ss_m(dS, make_desc(qdesc_lo + hh * 16384 + k * 32, 16, 1024, SWZ_128),
+                       make_desc(kb + k * 32, 16, 1024, SWZ_128), idS, (hh | k) != 0, none);
+            mma_commit(smem_u32(&B.empty[s_]));
+            ++u;
+          }
+          if (t == 0) {
+            mbar_wait(smem_u32(&B.qt_full[io & 1]), (io >> 1) & 1);
+            fence_async_smem();
+          }
+          const uint32_t qt = sb + OFF_QT + 4096u * (io & 1);
+          for (int h4 = 0; h4 < W.n_slots; h4 += 4) {
+            const uint32_t s_ = u % kNU;
+            mbar_wait(smem_u32(&B.full[s_]), (u / kNU) & 1);
+            tc_fence_after();
+            const uint32_t rb = sb + OFF_RING + s_ * kUnit;
+            const int n4 = min(4, W.n_slots - h4);
+            for (int s = 0; s < n4; ++s) {
+              const uint4 ml = __ldg(reinterpret_cast<const uint4*>(p.wus[T.wu].slot_lanes[h4 + s]));
+              mma_ss_m(dS, make_desc(qt, 16, 256, SWZ_32), make_desc(rb + 4096u * s, 16, 256, SWZ_32), idS, 1u,
+                       make_uint4(~ml.x, ~ml.y, ~ml.z, ~ml.w));
+            }
+            mma_commit(smem_u32(&B.empty[s_]));
+            ++u;
+          }
+          mma_commit(smem_u32(&B.s_full[g & 1]));
+          if (t == n_tiles - 1) mma_commit(smem_u32(&B.q_empty));
+          ++g;
+        } else {
+          // ---------------------------------- O += P V ; A_r += P R_v ----------------------------------
+          const int b = gp & 1;
+          mbar_wait(smem_u32(&B.p_full[b]), (gp >> 1) & 1);
+          if (t == 0 && io > 0) mbar_wait(smem_u32(&B.o_free), (io - 1) & 1);
+          tc_fence_after();
+          const uint4 dis = make_uint4(~W.lanes[0], ~W.lanes[1], ~W.lanes[2], ~W.lanes[3]);
+          const uint32_t idV = idesc_bf16(128, 128, false, true);
+          const uint32_t idR = idesc_bf16(128, 16 * W.n_slots, false, true);
+          const int nk = (T.n_keys + 15) >> 4;
+          const uint32_t pa = tm + 128u * b;
+          const uint32_t acc0 = (T.flags & kTileFirst) ? 0u : 1u;
+          for (int half = 0; half < (T.n_keys > 64 ? 2 : 1); ++half) {
+            const uint32_t sv = u % kNU, sr_ = (u + 1) % kNU;
+            mbar_wait(smem_u32(&B.full[sv]), (u / kNU) & 1);
+            mbar_wait(smem_u32(&B.full[sr_]), ((u + 1) / kNU) & 1);
+            fence_async_smem();  // R_v arrives through cp.async (generic proxy)
+            tc_fence_after();
+            const uint32_t vb = sb + OFF_RING + sv * kUnit, rvb = sb + OFF_RING + sr_ * kUnit;
+            const int k1 = min(4, nk - 4 * half);
+            for (int k = 0; k < k1; ++k) {
+              const uint32_t acc = (half | k) ? 1u : acc0;
+              const uint32_t a = pa + 8u * (4 * half + k);
+              mma_ts_m(tm + T_O, a, make_desc(vb + 2048u * k, 8192, 1024, SWZ_128), idV, acc, dis);
+              mma_ts_m(tm + T_AR, a, make_desc(rvb + 512u * k, 2048, 256, SWZ_32), idR, acc, dis);
+            }
+            mma_commit(smem_u32(&B.empty[sv]));
+            mma_commit(smem_u32(&B.empty[sr_]));
+            u += 2;
+          }
+          mma_commit(smem_u32(&B.o_done));
+          if (t == n_tiles - 1) mma_commit(smem_u32(&B.o_final));
+          ++gp;
+        }
+      });
+    }
+  } else if (wid == 5) {
+    // ============================ K_base / V_base loader (TMA tensor boxes) ============================
+    if (lane == 0) {
+      uint32_t u = 0;
+      const int P = p.P;
+      const int ppt = 128 / P;  // pages per tile
+      walk(p, [&](int kind, int, int, int ti, int) {
+        const RTile T = p.tiles[ti];
+        const int64_t hrow = (int64_t)T.kv_head * P;
+        if (kind == 0) {
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t s_ = u % kNU;
+            mbar_wait(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
+            const uint32_t dst = sb + OFF_RING + s_ * kUnit;
+            int np = 0;
+            for (int pi = 0; pi < ppt && pi * P < T.n_keys; ++pi) np += p.base_pages[T.base_off + pi] >= 0;
+            mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)np * P * 128);
+            for (int pi = 0; pi < ppt && pi * P < T.n_keys; ++pi) {
+              const int pg = p.base_pages[T.base_off + pi];
+              if (pg < 0) continue;
+              const int64_t r0 = p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow;
+              tma_load_2d(dst + pi * P * 128, &maps.k2d, 64 * hh, (int)r0, smem_u32(&B.full[s_]));
+            }
+            ++u;
+          }
+          u += (uint32_t)n_kside(__ldg(&p.wus[T.wu].n_slots)) - 2u;
+        } else {
+          for (int half = 0; half < (T.n_keys > 64 ? 2 : 1); ++half) {
+            const uint32_t s_ = u % kNU;
+            mbar_wait(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
+            const uint32_t dst = sb + OFF_RING + s_ * kUnit;
+            const int key_lo = 64 * half, key_hi = min(64 * half + 64, T.n_keys);
+            if (P >= 64) {
+              const int pi = key_lo / P;
+              const int pg = p.base_pages[T.base_off + pi];
+              mbar_expect_tx(smem_u32(&B.full[s_]), pg >= 0 ? 16384u : 0u);
+              if (pg >= 0) {
+                const int64_t r0 = p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow + (key_lo % P);
+                tma_load_3d(dst, &maps.v3d, 0, (int)r0, 0, smem_u32(&B.full[s_]));
+              }
+            } else {
+              int np = 0;
+              for (int k = key_lo; k < key_hi; k += P) np += p.base_pages[T.base_off + k / P] >= 0;
+              mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)np * P * 256);
+              for (int k = key_lo; k < key_hi; k += P) {
+                const int pg = p.base_pages[T.base_off + k / P];
+                if (pg < 0) continue;
+                const int64_t r0 = p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow;
+                for (int hh = 0; hh < 2; ++hh)
+                  tma_load_2d(dst + hh * 8192 + (k - key_lo) * 128, &maps.v2d, 64 * hh, (int)r0,
+                              smem_u32(&B.full[s_]));
+              }
+            }
+            u += 2;
+          }
+        }
+      });
+    }
+  } else if (wid == 6) {
+    // ====================== R_k loader: bulk copies of whole residual pages, 4 slots per unit ======================
+    if (lane == 0) {
+      uint32_t u = 0;
+      const int P = p.P;
+      const int ppt = 128 / P;
+      const uint8_t* rk = (const uint8_t*)p.res_k + (size_t)p.layer * p.res_layer_elems * 2;
+      walk(p, [&](int kind, int, int, int ti, int) {
+        const RTile& T = p.tiles[ti];
+        if (kind == 0) {
+          u += 2;
+          const int ns = p.wus[T.wu].n_slots;
+          for (int h4 = 0; h4 < ns; h4 += 4) {
+            const uint32_t s_ = u % kNU;
+            mbar_wait(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
+            const uint32_t dst = sb + OFF_RING + s_ * kUnit;
+            const int n4 = min(4, ns - h4);
+            int np = 0;
+            for (int s = 0; s < n4; ++s)
+              for (int pi = 0; pi < ppt && pi * P < T.n_keys; ++pi) np += p.res_pages[T.res_off[h4 + s] + pi] >= 0;
+            mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)np * P * 32);
+            for (int s = 0; s < n4; ++s)
+              for (int pi = 0; pi < ppt && pi * P < T.n_keys; ++pi) {
+                const int pg = p.res_pages[T.res_off[h4 + s] + pi];
+                if (pg < 0) continue;
+                bulk_g2s(dst + 4096u * s + pi * P * 32, rk + (size_t)pg * P * 32, P * 32, smem_u32(&B.full[s_]));
+              }
+            ++u;
+          }
+        } else {
+          u += (uint32_t)n_vside(T.n_keys);
+        }
+      });
+    }
+  } else if (wid == 7) {
+    // ============ R_v loader: 64-key halves of each slot's pages, 16-byte cp.async by the whole warp ============
+    uint32_t u = 0;
+    const int P = p.P;
+    const uint8_t* rv = (const uint8_t*)p.res_v + (size_t)p.layer * p.res_layer_elems * 2;
+    walk(p, [&](int kind, int, int, int ti, int) {
+      const RTile& T = p.tiles[ti];
+      const int ns = p.wus[T.wu].n_slots;
+      if (kind == 0) {
+        u += (uint32_t)n_kside(ns);
+      } else {
+        for (int half = 0; half < (T.n_keys > 64 ? 2 : 1); ++half) {
+          const uint32_t s_ = (u + 1) % kNU;
+          mbar_wait(smem_u32(&B.empty[s_]), (((u + 1) / kNU) & 1) ^ 1);
+          const uint32_t dst = sb + OFF_RING + s_ * kUnit;
+          // slot s, key k (0..63 of the half): 2 chunks of 16 B at dst + 2048 s + 32 k (page format kept)
+          const int kmax = min(64, T.n_keys - 64 * half);
+          const int nchunk = ns * 128;  // 64 keys x 2 chunks per slot
+          for (int c = lane; c < nchunk; c += 32) {
+            const int s = c >> 7, kk = (c >> 1) & 63, hc = c & 1;
+            if (kk >= kmax) continue;
+            const int key = 64 * half + kk;
+            const int pg = p.res_pages[T.res_off[s] + key / P];
+            if (pg < 0) continue;
+            cp_async16(dst + 2048u * s + 32u * kk + 16u * hc, rv + ((size_t)pg * P + key % P) * 32 + 16 * hc);
+          }
+          cp_async_arrive_inc(smem_u32(&B.full[s_]));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&B.full[s_]));
+          u += 2;
+        }
+      }
+    });
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+   }
+  } else {
+    // ======================= aux warpgroup: q~, Q image, epilogue (thread = row = TMEM lane) =======================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    const int row = tid - 256;
+    const uint32_t lane_base = (uint32_t)(32 * (wid - 8)) << 16;
+    const int i0 = p.sched_ptr[blockIdx.x];
+    const __nv_bfloat16* Qg = (const __nv_bfloat16*)p.Q;
+    // q~ of item `io` into q~ image `buf`
+    auto qtilde = [&](int io) {
+      const RItem it = p.items[p.sched_items[i0 + io]];
+      const RRow rr = p.rows[it.row0 + row];
+      const uint32_t dst = sb + OFF_QT + 4096u * (io & 1) + 32u * row;
+      uint32_t outw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (rr.q_row >= 0) {
+        const int h = (rr.meta >> 8) & 0xff, a = rr.meta >> 16;
+        const uint4* qv = (const uint4*)(Qg + (size_t)rr.q_row * 128);
+        const uint4* bk = (const uint4*)((const __nv_bfloat16*)p.adapters[2 * a] + (size_t)p.layer * p.adapter_layer_elems +
+                                         (size_t)h * 16 * 128);
+        // q~[j] = sum_k Q[k] B_k[j][k], fp32: 8 rows of B_k per pass, one 8-element chunk of Q at a time
+        float qt[16];
+#pragma unroll
+        for (int jh = 0; jh < 2; ++jh) {
+          float2 acc[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = make_float2(0.f, 0.f);
+#pragma unroll 1
+          for (int c = 0; c < 16; ++c) {
+            const uint4 qc = __ldg(qv + c);
+            const uint32_t qw[4] = {qc.x, qc.y, qc.z, qc.w};
+            uint4 bb[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) bb[j] = __ldg(bk + (8 * jh + j) * 16 + c);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t bw[4] = {bb[j].x, bb[j].y, bb[j].z, bb[j].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                acc[j] = __ffma2_rn(make_float2(__uint_as_float(qw[e] << 16), __uint_as_float(qw[e] & 0xffff0000u)),
+                                    make_float2(__uint_as_float(bw[e] << 16), __uint_as_float(bw[e] & 0xffff0000u)),
+                                    acc[j]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) qt[8 * jh + j] = acc[j].x + acc[j].y;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) outw[j] = pack_bf16x2(qt[2 * j], qt[2 * j + 1]);
+      }
+      const uint32_t sw = (uint32_t)((row >> 2) & 1);
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(dst + 16u * sw), "r"(outw[0]), "r"(outw[1]),
+                   "r"(outw[2]), "r"(outw[3]) : "memory");
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(dst + 16u * (sw ^ 1u)), "r"(outw[4]),
+                   "r"(outw[5]), "r"(outw[6]), "r"(outw[7]) : "memory");
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&B.qt_full[io & 1]));
+    };
+    // Q rows of item `io` into the (single) Q image, SW128 K-major [d-half][row][128 B]
+    auto qimage = [&](int io) {
+      const RItem it = p.items[p.sched_items[i0 + io]];
+      const int qr = p.rows[it.row0 + row].q_row;
+      if (qr >= 0) {
+        const uint8_t* src = (const uint8_t*)(Qg + (size_t)qr * 128);
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          cp_async16(sb + OFF_Q + (c >> 3) * 16384u + 128u * row + 16u * ((c & 7) ^ (row & 7)), src + 16 * c);
+      }
+      cp_async_arrive_inc(smem_u32(&B.q_full));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&B.q_full));
+    };
+    if (n_my > 0) {
+      qimage(0);
+      qtilde(0);
+    }
+    for (int io = 0; io < n_my; ++io) {
+      if (io + 1 < n_my) {
+        qtilde(io + 1);  // its image buffer was freed by the last S of item io - 1 (waited below, last iteration)
+        mbar_wait(smem_u32(&B.q_empty), io & 1);
+        qimage(io + 1);
+      }
+      // epilogue of item io
+      const RItem it = p.items[p.sched_items[i0 + io]];
+      const RRow rr = p.rows[it.row0 + row];
+      mbar_wait(smem_u32(&B.ml_full[io & 1]), (io >> 1) & 1);
+      mbar_wait(smem_u32(&B.o_final), io & 1);
+      tc_fence_after();
+      float* e = rr.entry >= 0 ? p.ws + (size_t)rr.entry * p.entry_stride : nullptr;
+      const float2 ml = B.ml[io & 1][row];
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t o[32];
+        FKV_TMEM_LD32(tm + lane_base + T_O + c0, o);
+        tmem_ld_wait();
+        if (e) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *(float4*)(e + kEntAcc + c0 + j) = make_float4(__uint_as_float(o[j]), __uint_as_float(o[j + 1]),
+                                                           __uint_as_float(o[j + 2]), __uint_as_float(o[j + 3]));
+        }
+      }
+      const int slot = rr.meta & 0xff;
+      for (int s = 0; s < kRowsMaxSlots; ++s) {
+        if (!__any_sync(0xffffffffu, rr.q_row >= 0 && slot == s)) continue;
+        uint32_t o[16];
+        FKV_TMEM_LD16(tm + lane_base + T_AR + 16 * s, o);
+        tmem_ld_wait();
+        if (e && slot == s) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *(float4*)(e + kEntAcc + 128 + j) = make_float4(__uint_as_float(o[j]), __uint_as_float(o[j + 1]),
+                                                            __uint_as_float(o[j + 2]), __uint_as_float(o[j + 3]));
+        }
+      }
+      if (e) *(float2*)e = ml;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&B.o_free));
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  }
+  pdl_trigger();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (wid == 4) tmem_dealloc(tm, 512);
+}
+
+}  // namespace
+
+cudaError_t launch_attention_rows(const RowsParams& p, const RowsMaps& maps, cudaStream_t s) {
+  static bool attr[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !attr[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(ra_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr[dev] = true;
+  }
+  if (p.n_ctas <= 0) return cudaSuccess;
+  return launch_pdl(ra_rows_kernel, dim3(p.n_ctas), dim3(kThreads), kSmemBytes, s, p, maps);
+}
+
+}  // namespace k
+}  // namespace fkv

@@ -18,6 +18,12 @@ from workloads import driver, recipes, synth  # noqa: E402
 TOL = {"bf16": 2e-2, "f32": 1e-5}
 
 
+def _tc_kernel(mode):
+    """Default tcgen05 kernel id: 3 = rows on the TMEM lanes (ra_rows.cu, NONE mode), 2 = keys on the TMEM
+    lanes (ra_tc.cu, DEFERRED; FKV_KERNEL=2 forces it for NONE too)."""
+    return 3 if mode == "none" else 2
+
+
 @pytest.fixture(scope="module", autouse=True)
 def _need_gpu():
     if not torch.cuda.is_available():
@@ -66,34 +72,40 @@ def test_device_synth_matches_host_generator():
 
 
 @pytest.mark.parametrize("mode", ["deferred", "none"])
-@pytest.mark.parametrize("kernel", ["tc", "tc128", "mma", "simt"])
+@pytest.mark.parametrize("kernel", ["tc", "tc_keys", "tc128", "mma", "simt"])
 def test_c1_parity(mode, kernel, monkeypatch):
     """configs[0] (C1): 1 layer Llama-3.1-8B shape, r=16, 4 agents forked from a
     2K-token prefix + 128 private + 1 decode token; llama3 RoPE, theta 5e5."""
-    if kernel == "tc128":
+    expect = None
+    if kernel in ("tc128", "tc_keys"):
         if mode == "deferred":
-            pytest.skip("the 128-row variant is NONE only")
-        monkeypatch.setenv("FKV_TC_ROWS", "128")
-        kernel = "tc"
+            pytest.skip("keys-on-lanes variants are the DEFERRED default already")
+        monkeypatch.setenv("FKV_KERNEL", "2")
+        if kernel == "tc128":
+            monkeypatch.setenv("FKV_TC_ROWS", "128")
+        kernel, expect = "tc", 2
     scen = recipes.c1()
     fkv = _ctx(scen, 1, 32, 8, 128, 16, 64, "bf16", mode, theta=500000.0, llama3=True)
     driver.build(fkv, scen, seed=0)
     force = {"tc": 0, "mma": L.PLAN_FORCE_MMA, "simt": L.PLAN_FORCE_SIMT}[kernel]
     err, pl = _run_and_check(fkv, scen, 0, 0, "bf16", mode, flags=L.PLAN_CHECK_WRITTEN | force, theta=500000.0,
                              llama3=True)
-    assert pl.info.kernel == {"tc": 2, "mma": 0, "simt": 1}[kernel]
+    assert pl.info.kernel == (expect or {"tc": _tc_kernel(mode), "mma": 0, "simt": 1}[kernel])
     assert err <= TOL["bf16"], err
 
 
-@pytest.mark.parametrize("mode,rows", [("deferred", 64), ("none", 64), ("none", 128)])
+@pytest.mark.parametrize("mode,variant", [("deferred", 64), ("none", "rows"), ("none", 64), ("none", 128)])
 @pytest.mark.parametrize("P", [16, 32, 64, 128])
-def test_tc_kernel_page_sizes_and_groups(mode, rows, P, monkeypatch):
+def test_tc_kernel_page_sizes_and_groups(mode, variant, P, monkeypatch):
     """tcgen05 kernel: page sizes 16/32/64 (TMA box = one page), owner groups
     with several slots (same-agent branches: 4 branches x g=4 rows = one slot;
     a chunked-prefill owner spanning several slots), key ranges ending inside
     a page, and multi-tile split items; 64-row CTAs and (NONE) the 128-row
     variant (8 slots, row sums reduced on the CUDA cores)."""
-    monkeypatch.setenv("FKV_TC_ROWS", str(rows))
+    if variant != "rows":
+        monkeypatch.setenv("FKV_TC_ROWS", str(variant))
+        if mode == "none":
+            monkeypatch.setenv("FKV_KERNEL", "2")
     ag = [recipes.AgentSpec(100, 100, None, 0, False, 700, decode=False)]
     for i in range(3):
         ag.append(recipes.AgentSpec(1000 + i, i, 100, 700, False, 0, decode=False))
@@ -103,7 +115,7 @@ def test_tc_kernel_page_sizes_and_groups(mode, rows, P, monkeypatch):
     fkv = _ctx(scen, 1, 32, 8, 128, 16, P, "bf16", mode)
     driver.build(fkv, scen, seed=11)
     err, pl = _run_and_check(fkv, scen, 11, 0, "bf16", mode)
-    assert pl.info.kernel == 2
+    assert pl.info.kernel == (3 if variant == "rows" else 2)
     assert err <= TOL["bf16"], err
     scen.q_len = 9   # multi-row chunk per sequence: slots of one owner span several warps
     err, pl = _run_and_check(fkv, scen, 11, 0, "bf16", mode)
@@ -207,7 +219,7 @@ def test_kv_head_shard_parity(mode):
     fkv = _ctx(scen, 1, 32, 8, 128, 16, 128, "bf16", mode, kv_heads=(4, 8))
     driver.build(fkv, scen, seed=21, h0=4)
     err, pl = _run_and_check(fkv, scen, 21, 0, "bf16", mode, h0=4)
-    assert pl.info.kernel == 2
+    assert pl.info.kernel == _tc_kernel(mode)
     assert err <= TOL["bf16"], err
 
 
@@ -226,8 +238,8 @@ def test_many_splits_combine(mode, monkeypatch):
     fkv = _ctx(scen, 1, 32, 8, 128, 16, 128, "bf16", mode)
     driver.build(fkv, scen, seed=5)
     err, pl = _run_and_check(fkv, scen, 5, 0, "bf16", mode)
-    assert pl.info.kernel == 2
-    assert pl.info.n_items > 8 * 40, pl.info.n_items
+    assert pl.info.kernel == _tc_kernel(mode)
+    assert pl.info.n_items > 8 * 39, pl.info.n_items
     assert err <= TOL["bf16"], err
 
 
@@ -240,5 +252,5 @@ def test_c2_full_size_sampled(mode):
     fkv = _ctx(scen, 1, 32, 8, 128, 16, 128, "bf16", mode, theta=500000.0, llama3=True)
     driver.build(fkv, scen, seed=0)
     err, pl = _run_and_check(fkv, scen, 0, 0, "bf16", mode, theta=500000.0, llama3=True, seqs=[0, 21, 42, 63])
-    assert pl.info.kernel == 2 and pl.info.n_items > 148
+    assert pl.info.kernel == _tc_kernel(mode) and pl.info.n_items > 148
     assert err <= TOL["bf16"], err
