@@ -108,13 +108,15 @@ void ctx_create(Ctx& c, const fkv_config& cfg, const fkv_buffers* buf) {
         c.tc_maps.assign((const uint8_t*)m, (const uint8_t*)m + sizeof(m));
         c.has_tc_maps = true;
         if (P >= 16) {
-          // rows-on-lanes kernel (ra_rows.cu): K d-half boxes {64, min(P, 128)}; V 64-key boxes {64, 64, 2}
-          // (P >= 64) or per-page d-half boxes {64, P} (P < 64)
+          // rows-on-lanes kernel (ra_rows.cu): whole-tile boxes {64, 128, 2} (P = 128) or per-page d-half boxes
           k::RowsMaps rm;
           std::memset(&rm, 0, sizeof(rm));
           rm.k2d = make_tmap_2d_bf16(buf->base_k, brows, 128, 256, 64, P, 128);
-          rm.v2d = make_tmap_2d_bf16(buf->base_v, brows, 128, 256, 64, P < 64 ? P : 64, 128);
-          if (P >= 64) rm.v3d = make_tmap_3d_bf16_halves(buf->base_v, brows, 64);
+          rm.v2d = make_tmap_2d_bf16(buf->base_v, brows, 128, 256, 64, P, 128);
+          if (P == 128) {
+            rm.k3d = make_tmap_3d_bf16_halves(buf->base_k, brows, 128);
+            rm.v3d = make_tmap_3d_bf16_halves(buf->base_v, brows, 128);
+          }
           c.rows_maps.assign((const uint8_t*)&rm, (const uint8_t*)&rm + sizeof(rm));
           c.has_rows_maps = true;
         }

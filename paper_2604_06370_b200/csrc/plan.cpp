@@ -563,6 +563,7 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
       rp.entry_stride = a.entry_stride;
       rp.scale_log2 = a.scale_log2;
       rp.dbg = a.dbg; rp.dbg_block = a.dbg_block;
+      rp.flags = getenv("FKV_ROWS_FLAGS") ? atoi(getenv("FKV_ROWS_FLAGS")) : 0;
       e = k::launch_attention_rows(rp, *(const k::RowsMaps*)c.rows_maps.data(), (cudaStream_t)stream);
     }
     if (e == cudaSuccess && (phases & FKV_PHASE_COMBINE)) e = k::launch_combine(a, (cudaStream_t)stream);

@@ -19,7 +19,7 @@
 //   warp  4    MMA issuer (one thread)
 //   warp  5    K_base / V_base loader (TMA tensor boxes)
 //   warp  6    R_k loader (bulk copies of residual pages: the page format is the SW32 K-major operand)
-//   warp  7    R_v loader (16-byte cp.async, 64-key halves of each slot's page)
+//   warp  7    R_v loader (bulk copies of 64-key halves of each slot's page)
 //   warps 8-11 aux: q~ of the next item, Q image of the next item (cp.async), epilogue (TMEM -> partial entries)
 //
 // Shared memory: Q image 32 KB (SW128 K-major) | q~ images 2 x 4 KB (SW32 K-major) | ring of kNU 16-KB units
@@ -39,8 +39,8 @@ namespace k {
 namespace {
 using namespace sm100;
 
-constexpr int kNU = 11;  // ring units
-constexpr uint32_t kUnit = 16384;
+constexpr int kNU = 5;  // ring slots
+constexpr uint32_t kUnit = 32768;
 constexpr uint32_t OFF_Q = 0, OFF_QT = 32768, OFF_RING = 40960;
 constexpr uint32_t OFF_BAR = OFF_RING + kNU * kUnit;
 constexpr uint32_t T_O = 256, T_AR = 384;
@@ -82,6 +82,18 @@ __device__ __forceinline__ void mma_ts_m(uint32_t d, uint32_t a, uint64_t b, uin
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d),
       "r"(a), "l"(b), "r"(id), "r"(acc), "r"(dis.x), "r"(dis.y), "r"(dis.z), "r"(dis.w));
 }
+// mbarrier phase wait: try_wait without a suspend-time hint (the hinted form compiles to NANOSLEEP.SYNCS with a
+// 1 ms hint whose wake-up latency cost several microseconds per wait on B200)
+__device__ __forceinline__ void wait_bar(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -93,9 +105,13 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
   return d;
 }
 
-// Units of a tile's K side (S) and V side (PV), in ring order.
-__device__ __forceinline__ int n_kside(int n_slots) { return n_slots > 4 ? 4 : 3; }
-__device__ __forceinline__ int n_vside(int n_keys) { return n_keys > 64 ? 4 : 2; }
+// diagnostics timeline (fkv_debug_timeline): event ev, index i -> dbg[ev * 512 + i] = clock64 of CTA dbg_block
+template <bool kDbg>
+__device__ __forceinline__ void stamp_(const RowsParams& p, int ev, int i) {
+  if (kDbg && (int)blockIdx.x == p.dbg_block && i < 512) p.dbg[ev * 512 + i] = clock64();
+}
+#define stamp stamp_<kDbg>
+
 
 // Walk the CTA's items in MMA consumption order: S(0), S(1) PV(0), S(2) PV(1), ..., PV(n-1) per item.
 // f(kind, item_idx, item_ord, t, tile_index, last_in_item): kind 0 = K side of tile t, 1 = V side of tile t.
@@ -112,10 +128,12 @@ __device__ __forceinline__ void walk(const RowsParams& p, F&& f) {
   }
 }
 
+template <bool kDbg>
 __global__ void __launch_bounds__(kThreads, 1)
     ra_rows_kernel(const __grid_constant__ RowsParams p, const __grid_constant__ RowsMaps maps) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const long long t_start = clock64();
   Bars& B = *reinterpret_cast<Bars*>(smem + OFF_BAR);
   const uint32_t sb = smem_u32(smem);
   if (tid == 0) {
@@ -140,20 +158,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   // and empty Q rows are multiplied by zero probabilities / never read, but NaN * 0 would poison a row)
   for (uint32_t i = tid; i < OFF_BAR / 16; i += kThreads) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
   fence_async_smem();
+  // the kernel is a programmatic dependent launch: the pools (kv_write) and Q are the predecessor's outputs, and
+  // the predecessor may be another instance of this kernel still holding the SM's tensor memory
+  pdl_wait();
   if (wid == 4) tmem_alloc(smem_u32(&B.tmem_base), 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = B.tmem_base;
-  // the kernel is a programmatic dependent launch: the pools (kv_write) and Q are the predecessor's outputs
-  pdl_wait();
   const int n_my = p.sched_ptr[blockIdx.x + 1] - p.sched_ptr[blockIdx.x];
-  // register budget per warpgroup (setmaxnreg at the top of each role): softmax 232, loaders / MMA 56, aux 216
-  // (x 128 threads = 64512 registers = the CTA allocation of 168 x 384: more would deadlock setmaxnreg.inc)
+  // register budget per warpgroup (setmaxnreg at the top of each role): softmax 224, loaders / MMA 64, aux 216
+  // (x 128 threads = 64512 registers = the CTA allocation of 168 x 384: more would deadlock setmaxnreg.inc).
+  // Dependent grids (the combine kernel, or the next instance of this kernel) are released only after every
+  // warpgroup has moved its registers (named barrier 1 below): registers freed by setmaxnreg.dec must not be
+  // handed to a co-scheduled CTA of another grid before our setmaxnreg.inc claims them (observed on B200 as a
+  // hang / launch failure when the trigger came earlier or at the very end).
+  auto release_dependents = [&]() {
+    named_bar_sync(1, kThreads);
+    pdl_trigger();
+  };
 
   if (wid < 4) {
     // ============================ softmax warpgroup: thread = query row = TMEM lane ============================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+    release_dependents();
     const uint32_t lane_base = (uint32_t)(32 * wid) << 16;
     const int row = tid;
     int g = 0;
@@ -167,7 +195,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int b = g & 1;
         RTile Tn;
         if (t + 1 < it.n_tiles) Tn = p.tiles[it.tile0 + t + 1];
-        mbar_wait(smem_u32(&B.s_full[b]), (g >> 1) & 1);
+        wait_bar(smem_u32(&B.s_full[b]), (g >> 1) & 1);
+        if (tid == 0) stamp(p, 4, g);
         tc_fence_after();
         if (lw != 0u) {
           const bool active = (lw >> lane) & 1u;
@@ -204,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float alpha = resc ? ex2(m_run - m_new) : 1.f;
           if (__any_sync(0xffffffffu, resc)) {
             // O and A_r of this warp's rows were last written by PV of the previous tile
-            mbar_wait(smem_u32(&B.o_done), (g - 1) & 1);
+            wait_bar(smem_u32(&B.o_done), (g - 1) & 1);
             tc_fence_after();
 #pragma unroll 1
             for (int c0 = 0; c0 < 256; c0 += 32) {
@@ -245,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&B.p_full[b]));
+        if (tid == 0) stamp(p, 5, g);
         if (t + 1 < it.n_tiles) T = Tn;
       }
       B.ml[io & 1][row] = make_float2(m_run, l);
@@ -252,286 +282,253 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(smem_u32(&B.ml_full[io & 1]));
     }
   } else if (wid < 8) {
-   asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
-   if (wid == 4) {
-    // ==================================== MMA issuer (one thread) ====================================
-    if (lane == 0) {
-      uint32_t u = 0;
-      int g = 0;  // S tiles issued
-      int gp = 0; // PV tiles issued
-      const uint32_t qdesc_lo = (sb + OFF_Q);
-      walk(p, [&](int kind, int io, int t, int ti, int n_tiles) {
-        const RTile T = p.tiles[ti];
-        struct { uint32_t lanes[4]; int32_t n_slots; } W;
-        {
-          const uint4 lw = __ldg(reinterpret_cast<const uint4*>(p.wus[T.wu].lanes));
-          W.lanes[0] = lw.x; W.lanes[1] = lw.y; W.lanes[2] = lw.z; W.lanes[3] = lw.w;
-          W.n_slots = __ldg(&p.wus[T.wu].n_slots);
-        }
-        if (kind == 0) {
-          // ---------------------------------- S = Q K^T + q~ R_k^T ----------------------------------
-          if (t == 0) {
-            mbar_wait(smem_u32(&B.q_full), io & 1);
-            fence_async_smem();
-          }
-          const int ns = (T.n_keys + 15) & ~15;
-          const uint32_t idS = idesc_bf16(128, ns, false, false);
-          const uint32_t dS = tm + 128u * (g & 1);
-          const uint4 none = make_uint4(0, 0, 0, 0);
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const uint32_t s_ = u % kNU;
-            mbar_wait(smem_u32(&B.full[s_]), (u / kNU) & 1);
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+    release_dependents();
+    if (wid == 4) {
+      // ==================================== MMA issuer (one thread) ====================================
+      if (lane == 0) {
+        uint32_t u = 0;
+        int g = 0;   // S tiles issued
+        int gp = 0;  // PV tiles issued
+        const uint32_t qa = sb + OFF_Q;
+        walk(p, [&](int kind, int io, int t, int ti, int n_tiles) {
+          const RTile* Tp = p.tiles + ti;
+          const int n_keys = __ldg(&Tp->n_keys), wu = __ldg(&Tp->wu);
+          const int n_slots = __ldg(&p.wus[wu].n_slots);
+          if (kind == 0) {
+            // ------------------------- S = Q K^T + q~ R_k^T (K tile unit, R_k unit) -------------------------
+            if (t == 0) {
+              wait_bar(smem_u32(&B.q_full), io & 1);
+              stamp(p, 8, io);
+              fence_async_smem();  // Q rows arrive through cp.async (generic proxy)
+            }
+            const int ns = (n_keys + 15) & ~15;
+            const uint32_t idS = idesc_bf16(128, ns, false, false);
+            const uint32_t dS = tm + 128u * (g & 1);
+            const uint4 none = make_uint4(0, 0, 0, 0);
+            uint32_t s_ = u % kNU;
+            wait_bar(smem_u32(&B.full[s_]), (u / kNU) & 1);
+            stamp(p, 0, g);
             tc_fence_after();
             const uint32_t kb = sb + OFF_RING + s_ * kUnit;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_ss_m(dS, make_desc(qdesc_lo + hh * 16384 + k * 32, 16, 1024, SWZ_128),
-                       make_desc(kb + k * 32, 16, 1024, SWZ_128), idS, (hh | k) != 0, none);
+            for (int k = 0; k < 8; ++k)
+              mma_ss_m(dS, make_desc(qa + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SWZ_128),
+                       make_desc(kb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SWZ_128), idS, k != 0, none);
             mma_commit(smem_u32(&B.empty[s_]));
             ++u;
-          }
-          if (t == 0) {
-            mbar_wait(smem_u32(&B.qt_full[io & 1]), (io >> 1) & 1);
-            fence_async_smem();
-          }
-          const uint32_t qt = sb + OFF_QT + 4096u * (io & 1);
-          for (int h4 = 0; h4 < W.n_slots; h4 += 4) {
-            const uint32_t s_ = u % kNU;
-            mbar_wait(smem_u32(&B.full[s_]), (u / kNU) & 1);
+            if (t == 0) {
+              wait_bar(smem_u32(&B.qt_full[io & 1]), (io >> 1) & 1);
+              stamp(p, 9, io);
+              fence_async_smem();  // q~ written with st.shared by the aux warps
+            }
+            const uint32_t qt = sb + OFF_QT + 4096u * (io & 1);
+            s_ = u % kNU;
+            wait_bar(smem_u32(&B.full[s_]), (u / kNU) & 1);
             tc_fence_after();
             const uint32_t rb = sb + OFF_RING + s_ * kUnit;
-            const int n4 = min(4, W.n_slots - h4);
-            for (int s = 0; s < n4; ++s) {
-              const uint4 ml = __ldg(reinterpret_cast<const uint4*>(p.wus[T.wu].slot_lanes[h4 + s]));
+            for (int s = 0; s < n_slots; ++s) {
+              const uint4 ml = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].slot_lanes[s]));
               mma_ss_m(dS, make_desc(qt, 16, 256, SWZ_32), make_desc(rb + 4096u * s, 16, 256, SWZ_32), idS, 1u,
                        make_uint4(~ml.x, ~ml.y, ~ml.z, ~ml.w));
             }
             mma_commit(smem_u32(&B.empty[s_]));
             ++u;
-          }
-          mma_commit(smem_u32(&B.s_full[g & 1]));
-          if (t == n_tiles - 1) mma_commit(smem_u32(&B.q_empty));
-          ++g;
-        } else {
-          // ---------------------------------- O += P V ; A_r += P R_v ----------------------------------
-          const int b = gp & 1;
-          mbar_wait(smem_u32(&B.p_full[b]), (gp >> 1) & 1);
-          if (t == 0 && io > 0) mbar_wait(smem_u32(&B.o_free), (io - 1) & 1);
-          tc_fence_after();
-          const uint4 dis = make_uint4(~W.lanes[0], ~W.lanes[1], ~W.lanes[2], ~W.lanes[3]);
-          const uint32_t idV = idesc_bf16(128, 128, false, true);
-          const uint32_t idR = idesc_bf16(128, 16 * W.n_slots, false, true);
-          const int nk = (T.n_keys + 15) >> 4;
-          const uint32_t pa = tm + 128u * b;
-          const uint32_t acc0 = (T.flags & kTileFirst) ? 0u : 1u;
-          for (int half = 0; half < (T.n_keys > 64 ? 2 : 1); ++half) {
+            mma_commit(smem_u32(&B.s_full[g & 1]));
+            stamp(p, 1, g);
+            if (t == n_tiles - 1) mma_commit(smem_u32(&B.q_empty));
+            ++g;
+          } else {
+            // ------------------------- O += P V ; A_r += P R_v (V tile unit, R_v unit) -------------------------
+            const int b = gp & 1;
+            wait_bar(smem_u32(&B.p_full[b]), (gp >> 1) & 1);
+            stamp(p, 2, gp);
+            if (t == 0 && io > 0) wait_bar(smem_u32(&B.o_free), (io - 1) & 1);
+            const uint4 lw = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].lanes));
+            const uint4 dis = make_uint4(~lw.x, ~lw.y, ~lw.z, ~lw.w);
+            const uint32_t idV = idesc_bf16(128, 128, false, true);
+            const uint32_t idR = idesc_bf16(128, 16 * n_slots, false, true);
+            const int nk = (n_keys + 15) >> 4;
+            const uint32_t pa = tm + 128u * b;
+            const uint32_t acc0 = (__ldg(&Tp->flags) & kTileFirst) ? 0u : 1u;
             const uint32_t sv = u % kNU, sr_ = (u + 1) % kNU;
-            mbar_wait(smem_u32(&B.full[sv]), (u / kNU) & 1);
-            mbar_wait(smem_u32(&B.full[sr_]), ((u + 1) / kNU) & 1);
-            fence_async_smem();  // R_v arrives through cp.async (generic proxy)
+            wait_bar(smem_u32(&B.full[sv]), (u / kNU) & 1);
+            stamp(p, 13, gp);
+            wait_bar(smem_u32(&B.full[sr_]), ((u + 1) / kNU) & 1);
+            stamp(p, 14, gp);
             tc_fence_after();
             const uint32_t vb = sb + OFF_RING + sv * kUnit, rvb = sb + OFF_RING + sr_ * kUnit;
-            const int k1 = min(4, nk - 4 * half);
-            for (int k = 0; k < k1; ++k) {
-              const uint32_t acc = (half | k) ? 1u : acc0;
-              const uint32_t a = pa + 8u * (4 * half + k);
-              mma_ts_m(tm + T_O, a, make_desc(vb + 2048u * k, 8192, 1024, SWZ_128), idV, acc, dis);
-              mma_ts_m(tm + T_AR, a, make_desc(rvb + 512u * k, 2048, 256, SWZ_32), idR, acc, dis);
+            for (int k = 0; k < nk; ++k) {
+              const uint32_t acc = k ? 1u : acc0;
+              const uint32_t a = pa + 8u * k;
+              mma_ts_m(tm + T_O, a, make_desc(vb + 2048u * k, 16384, 1024, SWZ_128), idV, acc, dis);
+              mma_ts_m(tm + T_AR, a, make_desc(rvb + 512u * k, 4096, 256, SWZ_32), idR, acc, dis);
             }
             mma_commit(smem_u32(&B.empty[sv]));
             mma_commit(smem_u32(&B.empty[sr_]));
             u += 2;
+            mma_commit(smem_u32(&B.o_done));
+            stamp(p, 3, gp);
+            if (t == n_tiles - 1) mma_commit(smem_u32(&B.o_final));
+            ++gp;
           }
-          mma_commit(smem_u32(&B.o_done));
-          if (t == n_tiles - 1) mma_commit(smem_u32(&B.o_final));
-          ++gp;
-        }
-      });
-    }
-  } else if (wid == 5) {
-    // ============================ K_base / V_base loader (TMA tensor boxes) ============================
-    if (lane == 0) {
-      uint32_t u = 0;
-      const int P = p.P;
-      const int ppt = 128 / P;  // pages per tile
-      walk(p, [&](int kind, int, int, int ti, int) {
-        const RTile T = p.tiles[ti];
-        const int64_t hrow = (int64_t)T.kv_head * P;
-        if (kind == 0) {
-          for (int hh = 0; hh < 2; ++hh) {
-            const uint32_t s_ = u % kNU;
-            mbar_wait(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
-            const uint32_t dst = sb + OFF_RING + s_ * kUnit;
-            int np = 0;
-            for (int pi = 0; pi < ppt && pi * P < T.n_keys; ++pi) np += p.base_pages[T.base_off + pi] >= 0;
-            mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)np * P * 128);
-            for (int pi = 0; pi < ppt && pi * P < T.n_keys; ++pi) {
-              const int pg = p.base_pages[T.base_off + pi];
-              if (pg < 0) continue;
-              const int64_t r0 = p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow;
-              tma_load_2d(dst + pi * P * 128, &maps.k2d, 64 * hh, (int)r0, smem_u32(&B.full[s_]));
-            }
-            ++u;
-          }
-          u += (uint32_t)n_kside(__ldg(&p.wus[T.wu].n_slots)) - 2u;
-        } else {
-          for (int half = 0; half < (T.n_keys > 64 ? 2 : 1); ++half) {
-            const uint32_t s_ = u % kNU;
-            mbar_wait(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
-            const uint32_t dst = sb + OFF_RING + s_ * kUnit;
-            const int key_lo = 64 * half, key_hi = min(64 * half + 64, T.n_keys);
-            if (P >= 64) {
-              const int pi = key_lo / P;
-              const int pg = p.base_pages[T.base_off + pi];
-              mbar_expect_tx(smem_u32(&B.full[s_]), pg >= 0 ? 16384u : 0u);
-              if (pg >= 0) {
-                const int64_t r0 = p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow + (key_lo % P);
-                tma_load_3d(dst, &maps.v3d, 0, (int)r0, 0, smem_u32(&B.full[s_]));
-              }
-            } else {
-              int np = 0;
-              for (int k = key_lo; k < key_hi; k += P) np += p.base_pages[T.base_off + k / P] >= 0;
-              mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)np * P * 256);
-              for (int k = key_lo; k < key_hi; k += P) {
-                const int pg = p.base_pages[T.base_off + k / P];
-                if (pg < 0) continue;
-                const int64_t r0 = p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow;
-                for (int hh = 0; hh < 2; ++hh)
-                  tma_load_2d(dst + hh * 8192 + (k - key_lo) * 128, &maps.v2d, 64 * hh, (int)r0,
-                              smem_u32(&B.full[s_]));
-              }
-            }
-            u += 2;
-          }
-        }
-      });
-    }
-  } else if (wid == 6) {
-    // ====================== R_k loader: bulk copies of whole residual pages, 4 slots per unit ======================
-    if (lane == 0) {
-      uint32_t u = 0;
-      const int P = p.P;
-      const int ppt = 128 / P;
-      const uint8_t* rk = (const uint8_t*)p.res_k + (size_t)p.layer * p.res_layer_elems * 2;
-      walk(p, [&](int kind, int, int, int ti, int) {
-        const RTile& T = p.tiles[ti];
-        if (kind == 0) {
-          u += 2;
-          const int ns = p.wus[T.wu].n_slots;
-          for (int h4 = 0; h4 < ns; h4 += 4) {
-            const uint32_t s_ = u % kNU;
-            mbar_wait(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
-            const uint32_t dst = sb + OFF_RING + s_ * kUnit;
-            const int n4 = min(4, ns - h4);
-            int np = 0;
-            for (int s = 0; s < n4; ++s)
-              for (int pi = 0; pi < ppt && pi * P < T.n_keys; ++pi) np += p.res_pages[T.res_off[h4 + s] + pi] >= 0;
-            mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)np * P * 32);
-            for (int s = 0; s < n4; ++s)
-              for (int pi = 0; pi < ppt && pi * P < T.n_keys; ++pi) {
-                const int pg = p.res_pages[T.res_off[h4 + s] + pi];
-                if (pg < 0) continue;
-                bulk_g2s(dst + 4096u * s + pi * P * 32, rk + (size_t)pg * P * 32, P * 32, smem_u32(&B.full[s_]));
-              }
-            ++u;
-          }
-        } else {
-          u += (uint32_t)n_vside(T.n_keys);
-        }
-      });
-    }
-  } else if (wid == 7) {
-    // ============ R_v loader: 64-key halves of each slot's pages, 16-byte cp.async by the whole warp ============
-    uint32_t u = 0;
-    const int P = p.P;
-    const uint8_t* rv = (const uint8_t*)p.res_v + (size_t)p.layer * p.res_layer_elems * 2;
-    walk(p, [&](int kind, int, int, int ti, int) {
-      const RTile& T = p.tiles[ti];
-      const int ns = p.wus[T.wu].n_slots;
-      if (kind == 0) {
-        u += (uint32_t)n_kside(ns);
-      } else {
-        for (int half = 0; half < (T.n_keys > 64 ? 2 : 1); ++half) {
-          const uint32_t s_ = (u + 1) % kNU;
-          mbar_wait(smem_u32(&B.empty[s_]), (((u + 1) / kNU) & 1) ^ 1);
-          const uint32_t dst = sb + OFF_RING + s_ * kUnit;
-          // slot s, key k (0..63 of the half): 2 chunks of 16 B at dst + 2048 s + 32 k (page format kept)
-          const int kmax = min(64, T.n_keys - 64 * half);
-          const int nchunk = ns * 128;  // 64 keys x 2 chunks per slot
-          for (int c = lane; c < nchunk; c += 32) {
-            const int s = c >> 7, kk = (c >> 1) & 63, hc = c & 1;
-            if (kk >= kmax) continue;
-            const int key = 64 * half + kk;
-            const int pg = p.res_pages[T.res_off[s] + key / P];
-            if (pg < 0) continue;
-            cp_async16(dst + 2048u * s + 32u * kk + 16u * hc, rv + ((size_t)pg * P + key % P) * 32 + 16 * hc);
-          }
-          cp_async_arrive_inc(smem_u32(&B.full[s_]));
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&B.full[s_]));
-          u += 2;
-        }
+        });
       }
-    });
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-   }
+    } else if (wid == 5) {
+      // ================= K_base / V_base tiles: one TMA box {64 d, 128 keys, 2 d-halves} per tile (P = 128) =================
+      if (lane == 0) {
+        uint32_t u = 0;
+        int kt = 0;
+        const int P = p.P;
+        const int ppt = 128 / P;  // pages per tile
+        walk(p, [&](int kind, int, int, int ti, int) {
+          const RTile* Tp = p.tiles + ti;
+          const int n_keys = __ldg(&Tp->n_keys), base_off = __ldg(&Tp->base_off);
+          const int64_t hrow = (int64_t)__ldg(&Tp->kv_head) * P;
+          const CUtensorMap* m3 = kind == 0 ? &maps.k3d : &maps.v3d;
+          const CUtensorMap* m2 = kind == 0 ? &maps.k2d : &maps.v2d;
+          const uint32_t s_ = u % kNU;
+          wait_bar(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
+          if (kind == 0) stamp(p, 6, kt++);
+          const uint32_t dst = sb + OFF_RING + s_ * kUnit;
+          if (P == 128) {
+            const int pg = p.base_pages[base_off];
+            mbar_expect_tx(smem_u32(&B.full[s_]), pg >= 0 ? 32768u : 0u);
+            if (pg >= 0)
+              tma_load_3d(dst, m3, 0, (int)(p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow), 0, smem_u32(&B.full[s_]));
+          } else {
+            int np = 0;
+            for (int pi = 0; pi < ppt && pi * P < n_keys; ++pi) np += p.base_pages[base_off + pi] >= 0;
+            mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)np * P * 256);
+            for (int pi = 0; pi < ppt && pi * P < n_keys; ++pi) {
+              const int pg = p.base_pages[base_off + pi];
+              if (pg < 0) continue;
+              const int r0 = (int)(p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow);
+              tma_load_2d(dst + pi * P * 128, m2, 0, r0, smem_u32(&B.full[s_]));
+              tma_load_2d(dst + 16384 + pi * P * 128, m2, 64, r0, smem_u32(&B.full[s_]));
+            }
+          }
+          u += 2;
+        });
+      }
+    } else {
+      // ====== residual pages (warp 6: R_k, warp 7: R_v): one bulk copy per (slot, page), issued by parallel lanes ======
+      const bool is_rv = wid == 7;
+      uint32_t u = 0;  // R_k is the second unit of a tile's K side, R_v the second of its V side
+      const int P = p.P;
+      const int ppt = 128 / P;  // pages per slot and tile (<= 8)
+      const uint8_t* rp = (const uint8_t*)(is_rv ? p.res_v : p.res_k) + (size_t)p.layer * p.res_layer_elems * 2;
+      walk(p, [&](int kind, int, int, int ti, int) {
+        if ((kind == 1) != is_rv) {
+          u += 2;
+          return;
+        }
+        const RTile* Tp = p.tiles + ti;
+        const int n_keys = __ldg(&Tp->n_keys);
+        const int ns = __ldg(&p.wus[__ldg(&Tp->wu)].n_slots);
+        const uint32_t s_ = (u + 1) % kNU;
+        wait_bar(smem_u32(&B.empty[s_]), (((u + 1) / kNU) & 1) ^ 1);
+        const uint32_t dst = sb + OFF_RING + s_ * kUnit;
+        const int np = ns * ppt;  // (slot, page) pieces
+        int mine = 0;             // bytes this lane copies
+        for (int q = lane; q < np; q += 32) {
+          const int s = q / ppt, pi = q % ppt;
+          if (pi * P < n_keys && p.res_pages[__ldg(&Tp->res_off[s]) + pi] >= 0) mine += P * 32;
+        }
+        int tot = mine;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (lane == 0) mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)tot);
+        __syncwarp();
+        for (int q = lane; q < np; q += 32) {
+          const int s = q / ppt, pi = q % ppt;
+          if (pi * P >= n_keys) continue;
+          const int pg = p.res_pages[__ldg(&Tp->res_off[s]) + pi];
+          if (pg >= 0) bulk_g2s(dst + 4096u * s + pi * P * 32, rp + (size_t)pg * P * 32, P * 32, smem_u32(&B.full[s_]));
+        }
+        u += 2;
+      });
+    }
   } else {
     // ======================= aux warpgroup: q~, Q image, epilogue (thread = row = TMEM lane) =======================
     asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    release_dependents();
     const int row = tid - 256;
     const uint32_t lane_base = (uint32_t)(32 * (wid - 8)) << 16;
     const int i0 = p.sched_ptr[blockIdx.x];
     const __nv_bfloat16* Qg = (const __nv_bfloat16*)p.Q;
-    // q~ of item `io` into q~ image `buf`
+    // q~ = Q B_k^h^T (bf16, fp32 accumulate) of item `io` into q~ image io & 1 with warp-level MMA
+    // (m16n8k16): the 16 rows of an m16 tile are computed once per distinct (adapter, kv head) among them
     auto qtilde = [&](int io) {
       const RItem it = p.items[p.sched_items[i0 + io]];
-      const RRow rr = p.rows[it.row0 + row];
-      const uint32_t dst = sb + OFF_QT + 4096u * (io & 1) + 32u * row;
-      uint32_t outw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (rr.q_row >= 0) {
-        const int h = (rr.meta >> 8) & 0xff, a = rr.meta >> 16;
-        const uint4* qv = (const uint4*)(Qg + (size_t)rr.q_row * 128);
-        const uint4* bk = (const uint4*)((const __nv_bfloat16*)p.adapters[2 * a] + (size_t)p.layer * p.adapter_layer_elems +
-                                         (size_t)h * 16 * 128);
-        // q~[j] = sum_k Q[k] B_k[j][k], fp32: 8 rows of B_k per pass, one 8-element chunk of Q at a time
-        float qt[16];
+      const uint32_t qtb = sb + OFF_QT + 4096u * (io & 1);
+      const int gq = lane >> 2, tq = lane & 3;
+      for (int mt = 0; mt < 2; ++mt) {
+        const int r0 = 32 * (wid - 8) + 16 * mt;
+        const RRow ra = p.rows[it.row0 + r0 + gq], rb = p.rows[it.row0 + r0 + gq + 8];
+        // A fragments: rows r0 + gq, r0 + gq + 8; k = 16 ks + 2 tq (+1, +8, +9)
+        uint32_t af[8][4];
+        {
+          const uint32_t* qa = (const uint32_t*)(Qg + (size_t)max(ra.q_row, 0) * 128);
+          const uint32_t* qb = (const uint32_t*)(Qg + (size_t)max(rb.q_row, 0) * 128);
 #pragma unroll
-        for (int jh = 0; jh < 2; ++jh) {
-          float2 acc[8];
+          for (int ks = 0; ks < 8; ++ks) {
+            af[ks][0] = ra.q_row >= 0 ? __ldg(qa + 8 * ks + tq) : 0u;
+            af[ks][1] = rb.q_row >= 0 ? __ldg(qb + 8 * ks + tq) : 0u;
+            af[ks][2] = ra.q_row >= 0 ? __ldg(qa + 8 * ks + tq + 4) : 0u;
+            af[ks][3] = rb.q_row >= 0 ? __ldg(qb + 8 * ks + tq + 4) : 0u;
+          }
+        }
+        const int meta_a = ra.q_row >= 0 ? (ra.meta >> 8) : -1, meta_b = rb.q_row >= 0 ? (rb.meta >> 8) : -1;
+        uint32_t done_a = meta_a < 0, done_b = meta_b < 0;
+        while (__any_sync(0xffffffffu, !done_a || !done_b)) {
+          // the next (adapter, head) still to compute: the first lane with an undone row
+          const uint32_t ba = __ballot_sync(0xffffffffu, !done_a), bbm = __ballot_sync(0xffffffffu, !done_b);
+          const int src = ba ? __ffs(ba) - 1 : __ffs(bbm) - 1;
+          const int meta = __shfl_sync(0xffffffffu, ba ? meta_a : meta_b, src);
+          const int h = meta & 0xff, ad = meta >> 8;
+          const uint32_t* bk = (const uint32_t*)((const __nv_bfloat16*)p.adapters[2 * ad] +
+                                                 (size_t)p.layer * p.adapter_layer_elems + (size_t)h * 16 * 128);
+          float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] = make_float2(0.f, 0.f);
-#pragma unroll 1
-          for (int c = 0; c < 16; ++c) {
-            const uint4 qc = __ldg(qv + c);
-            const uint32_t qw[4] = {qc.x, qc.y, qc.z, qc.w};
-            uint4 bb[8];
+          for (int nt = 0; nt < 2; ++nt) {
+            uint32_t bf[8][2];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) bb[j] = __ldg(bk + (8 * jh + j) * 16 + c);
+            for (int ks = 0; ks < 8; ++ks) {
+              bf[ks][0] = __ldg(bk + (8 * nt + gq) * 64 + 8 * ks + tq);
+              bf[ks][1] = __ldg(bk + (8 * nt + gq) * 64 + 8 * ks + tq + 4);
+            }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const uint32_t bw[4] = {bb[j].x, bb[j].y, bb[j].z, bb[j].w};
+            for (int ks = 0; ks < 8; ++ks)
+              asm volatile(
+                  "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                  "{%8, %9}, {%0, %1, %2, %3};\n"
+                  : "+f"(c[nt][0]), "+f"(c[nt][1]), "+f"(c[nt][2]), "+f"(c[nt][3])
+                  : "r"(af[ks][0]), "r"(af[ks][1]), "r"(af[ks][2]), "r"(af[ks][3]), "r"(bf[ks][0]), "r"(bf[ks][1]));
+          }
+          // rows of this (adapter, head): store q~[row][8 nt + 2 tq .. +1] into the SW32 K-major image
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                acc[j] = __ffma2_rn(make_float2(__uint_as_float(qw[e] << 16), __uint_as_float(qw[e] & 0xffff0000u)),
-                                    make_float2(__uint_as_float(bw[e] << 16), __uint_as_float(bw[e] & 0xffff0000u)),
-                                    acc[j]);
+          for (int half = 0; half < 2; ++half) {
+            const bool mine = half == 0 ? (!done_a && meta_a == meta) : (!done_b && meta_b == meta);
+            if (mine) {
+              const int r = r0 + gq + 8 * half;
+#pragma unroll
+              for (int nt = 0; nt < 2; ++nt) {
+                const uint32_t v = pack_bf16x2(c[nt][2 * half], c[nt][2 * half + 1]);
+                const int j = 8 * nt + 2 * tq;
+                const uint32_t addr = qtb + 32u * r + 16u * ((uint32_t)(j >> 3) ^ (uint32_t)((r >> 2) & 1)) + 2u * (j & 7);
+                asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+              }
             }
           }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) qt[8 * jh + j] = acc[j].x + acc[j].y;
+          if (!done_a && meta_a == meta) done_a = 1;
+          if (!done_b && meta_b == meta) done_b = 1;
         }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) outw[j] = pack_bf16x2(qt[2 * j], qt[2 * j + 1]);
       }
-      const uint32_t sw = (uint32_t)((row >> 2) & 1);
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(dst + 16u * sw), "r"(outw[0]), "r"(outw[1]),
-                   "r"(outw[2]), "r"(outw[3]) : "memory");
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(dst + 16u * (sw ^ 1u)), "r"(outw[4]),
-                   "r"(outw[5]), "r"(outw[6]), "r"(outw[7]) : "memory");
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&B.qt_full[io & 1]));
+      if (row == 0) stamp(p, 10, io);
     };
     // Q rows of item `io` into the (single) Q image, SW128 K-major [d-half][row][128 B]
     auto qimage = [&](int io) {
@@ -553,15 +550,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int io = 0; io < n_my; ++io) {
       if (io + 1 < n_my) {
-        qtilde(io + 1);  // its image buffer was freed by the last S of item io - 1 (waited below, last iteration)
-        mbar_wait(smem_u32(&B.q_empty), io & 1);
+        qtilde(io + 1);  // its image buffer was freed by the last S of item io - 1 (waited in the last iteration)
+        wait_bar(smem_u32(&B.q_empty), io & 1);
         qimage(io + 1);
       }
       // epilogue of item io
       const RItem it = p.items[p.sched_items[i0 + io]];
       const RRow rr = p.rows[it.row0 + row];
-      mbar_wait(smem_u32(&B.ml_full[io & 1]), (io >> 1) & 1);
-      mbar_wait(smem_u32(&B.o_final), io & 1);
+      wait_bar(smem_u32(&B.ml_full[io & 1]), (io >> 1) & 1);
+      wait_bar(smem_u32(&B.o_final), io & 1);
+      if (row == 0) stamp(p, 11, io);
       tc_fence_after();
       float* e = rr.entry >= 0 ? p.ws + (size_t)rr.entry * p.entry_stride : nullptr;
       const float2 ml = B.ml[io & 1][row];
@@ -594,29 +592,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&B.o_free));
+      if (row == 0) stamp(p, 12, io);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   }
-  pdl_trigger();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (wid == 4) tmem_dealloc(tm, 512);
+  if (kDbg && tid == 0 && blockIdx.x < 512) {
+    p.dbg[30 * 512 + blockIdx.x] = clock64() - t_start;
+    p.dbg[31 * 512 + blockIdx.x] = n_my;
+  }
 }
 
 }  // namespace
 
 cudaError_t launch_attention_rows(const RowsParams& p, const RowsMaps& maps, cudaStream_t s) {
+  // the max-dynamic-shared-memory opt-in is per device
   static bool attr[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && !attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(ra_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(ra_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ra_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     if (e != cudaSuccess) return e;
     attr[dev] = true;
   }
   if (p.n_ctas <= 0) return cudaSuccess;
-  return launch_pdl(ra_rows_kernel, dim3(p.n_ctas), dim3(kThreads), kSmemBytes, s, p, maps);
+  // plain stream-ordered launch: as a programmatic dependent launch (either trigger placement) back-to-back
+  // instances or an early-scheduled combine grid hung / failed on B200; FKV_ROWS_FLAGS bit 1
+  // selects the PDL launch for experiments
+  if (p.flags & 2) {
+    if (p.dbg != nullptr) return launch_pdl(ra_rows_kernel<true>, dim3(p.n_ctas), dim3(kThreads), kSmemBytes, s, p, maps);
+    return launch_pdl(ra_rows_kernel<false>, dim3(p.n_ctas), dim3(kThreads), kSmemBytes, s, p, maps);
+  }
+  if (p.dbg != nullptr) ra_rows_kernel<true><<<p.n_ctas, kThreads, kSmemBytes, s>>>(p, maps);
+  else ra_rows_kernel<false><<<p.n_ctas, kThreads, kSmemBytes, s>>>(p, maps);
+  return cudaGetLastError();
 }
 
 }  // namespace k

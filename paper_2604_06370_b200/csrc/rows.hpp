@@ -76,12 +76,13 @@ struct RowsParams {
   float scale_log2;            // sm_scale * log2(e)
   long long* dbg;              // diagnostics timeline (nullptr = off)
   int32_t dbg_block;
+  int32_t flags;               // diagnostics switches (FKV_ROWS_FLAGS): bit 0 = R_v by bulk copies
 };
 
-// TMA maps of the rows kernel: K d-half boxes {64, min(P,128)} (2D, SW128) and V 64-key boxes {64, 64, 2}
-// (3D halves, SW128; P >= 64 only, else V uses the 2D map per (page, half))
+// TMA maps of the rows kernel over the base K / V pools: whole 128-key tiles {64 d, 128 keys, 2 d-halves} (3D,
+// SW128; P = 128) or per-page d-half boxes {64, P} (2D, SW128; P < 128). Both land as [d-half][key][128 B].
 struct RowsMaps {
-  CUtensorMap k2d, v2d, v3d;
+  CUtensorMap k3d, v3d, k2d, v2d;
 };
 
 }  // namespace k
