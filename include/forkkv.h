@@ -162,6 +162,36 @@ fkv_status fkv_fork(fkv_ctx* ctx, int64_t parent, int64_t prefix_len, int64_t ch
  * allocated for them, seqlen = *matched. The caller appends the rest. */
 fkv_status fkv_fork_tokens(fkv_ctx* ctx, int64_t child, int32_t adapter_id, const int32_t* tokens, int64_t n,
                            int64_t* matched);
+/* Fork with a partial hit (P:300 Step 1 + Step 2; "recomputes only the
+ * missing base projection xW ... directly reuses the surviving xA_i", §5.2).
+ * `owner` names the residual lineage (residual radix tree key) whose
+ * surviving xA_i rows the child may reuse; it must hold rows of `adapter_id`
+ * (else E_INVALID). The child maps
+ *   base pages   of the longest full-page prefix of tokens in the base tree,
+ *   residual pages of the longest full-page prefix in the lineage's tree,
+ * each +1, and gets FRESH (unwritten) pages for the rest of
+ * [0, *mapped = max of both): base rows [*base_hit, *mapped) must be
+ * recomputed (xW only: fkv_write_kv with FKV_WRITE_KBASE|FKV_WRITE_VBASE),
+ * residual rows [*res_hit, *mapped) likewise (xA_i only). Tokens
+ * [*mapped, n) are a cold miss: the caller appends them. All mapped pages are
+ * full and are inserted into both trees (one access of each tree's LRU
+ * clock). seqlen = *mapped; the child's residual lineage is `owner`.
+ * Errors: E_INVALID (ids, lineage adapter), E_NEEDS_EVICTION (pools; nothing
+ * changed). Outputs are token counts, multiples of page_size. */
+fkv_status fkv_fork_resume(fkv_ctx* ctx, int64_t child, int32_t adapter_id, int64_t owner, const int32_t* tokens,
+                           int64_t n, int64_t* base_hit, int64_t* res_hit, int64_t* mapped);
+/* Decoupled eviction (§5.2: "independent Least Recently Used (LRU)
+ * states to each radix tree"). Frees n_pages pages of ONE tree
+ * (kind FKV_KIND_BASE = the base tree, FKV_KIND_RES = the residual forest) by
+ * repeatedly removing its least recently used leaf, ties to the older
+ * insertion, among leaves whose page no live agent view holds (a view acts
+ * as the lock). Never touches the other tree, its clock or any agent table.
+ * Atomic: if fewer than n_pages pages are evictable, nothing is evicted and
+ * E_NEEDS_EVICTION is returned (fkv_evictable_pages tells how many are).
+ * *freed (may be NULL) = pages returned to the pool's free set. */
+fkv_status fkv_evict(fkv_ctx* ctx, int32_t kind, int64_t n_pages, int64_t* freed);
+/* Pages fkv_evict(kind, .) could free right now. */
+fkv_status fkv_evictable_pages(fkv_ctx* ctx, int32_t kind, int64_t* n_pages);
 /* Reserve n_new[i] slots for agents[i] (token ids concatenated in
  * token_ids). A first write into a page shared by >1 holder copies it
  * (CoW kernel enqueued on `stream`). Pages that become full are inserted into

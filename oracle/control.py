@@ -10,7 +10,11 @@ fork-with-CoW semantics and the DualRadixTree, written from the paper:
   * fork = Step 1 prefix match / inherit read-only base pages, Step 2
     copy-on-write allocation of exclusive residual pages (P:300 §5.2);
   * no page shared by more than one holder is ever written in place (the
-    "in-place cache update" conflict of P:87 §1 / P:219 §3.3).
+    "in-place cache update" conflict of P:87 §1 / P:219 §3.3);
+  * decoupled eviction: each radix tree has its own LRU state; evicting one
+    tree never touches the other, and a fork over a context whose base pages
+    were evicted while its residual pages survive is a *partial hit* that
+    recomputes only the base rows (§5.2; rules R10-R12).
 
 Where the paper is silent this follows the rule set R1-R9 and readings
 C-9..C-12 listed in DESIGN.md ("Control-plane rules").  The C++ library in
@@ -92,11 +96,16 @@ class Agent:
 
 
 class Node:
-    __slots__ = ("page", "children")
+    """One page-granular radix-tree node: a P-token chunk -> one page.  `last`
+    is the tree's logical clock at the node's last access, `seq` its insertion
+    number in that tree (LRU tie-break: older insertion first)."""
+    __slots__ = ("page", "children", "last", "seq")
 
-    def __init__(self, page: int):
+    def __init__(self, page: int, last: int = 0, seq: int = -1):
         self.page = page
         self.children: Dict[Tuple[int, ...], "Node"] = {}
+        self.last = last
+        self.seq = seq
 
 
 class ControlPlane:
@@ -106,11 +115,21 @@ class ControlPlane:
         self.agents: Dict[int, Agent] = {}
         self.base_root = Node(-1)
         self.res_roots: Dict[int, Node] = {}
+        self.res_adapter: Dict[int, int] = {}   # residual tree owner -> adapter whose xA_i it holds
+        self.clock = [0, 0]                     # independent LRU clocks of the two trees (R10)
+        self.nseq = [0, 0]                      # insertion counters of the two trees
         self.copies: List[Tuple[int, int, int, int]] = []  # (kind, src, dst, rows) CoW log
+
+    def _lineage_ok(self, owner: int, adapter: int) -> bool:
+        """R11: a residual lineage (tree key) holds the xA_i rows of ONE adapter:
+        its surviving tree and every live view of it must use `adapter`."""
+        if self.res_adapter.get(owner, adapter) != adapter:
+            return False
+        return all(ag.adapter == adapter for ag in self.agents.values() if ag.owner == owner)
 
     # ---- R3 -----------------------------------------------------------
     def create_root(self, a: int, adapter: int) -> int:
-        if a in self.agents or a < 0 or adapter < 0:
+        if a in self.agents or a < 0 or adapter < 0 or not self._lineage_ok(a, adapter):
             return E_INVALID
         self.agents[a] = Agent(a, adapter, a)
         return OK
@@ -124,6 +143,8 @@ class ControlPlane:
             return E_INVALID
         share = bool(flags & FORK_SHARE_RESIDUAL)
         if share and adapter != p.adapter:
+            return E_INVALID
+        if not share and not self._lineage_ok(child, adapter):
             return E_INVALID
         k = -(-prefix_len // self.P)
         if not share and len(self.pools[RES].free) < k:
@@ -143,23 +164,38 @@ class ControlPlane:
         return OK
 
     # ---- R7: fork_tokens (Step 1 = longest full-page prefix match) ------
-    def match_prefix(self, tokens: List[int]) -> List[int]:
-        node, pages = self.base_root, []
+    def _match(self, root: Optional[Node], tokens: List[int]) -> List[Node]:
+        """Longest full-page prefix of `tokens` stored under `root` (no touch)."""
+        node, path = root, []
+        if node is None:
+            return path
         for s in range(len(tokens) // self.P):
             ch = node.children.get(tuple(tokens[s * self.P:(s + 1) * self.P]))
             if ch is None:
                 break
-            pages.append(ch.page)
+            path.append(ch)
             node = ch
-        return pages
+        return path
+
+    def _touch(self, kind: int, path: List[Node]) -> None:
+        """R10: one access of a tree = one tick of its own clock for every node on the path."""
+        if path:
+            self.clock[kind] += 1
+            for nd in path:
+                nd.last = self.clock[kind]
+
+    def match_prefix(self, tokens: List[int]) -> List[int]:
+        return [nd.page for nd in self._match(self.base_root, tokens)]
 
     def fork_tokens(self, child: int, adapter: int, tokens: List[int]) -> Tuple[int, int]:
-        if child in self.agents or child < 0 or adapter < 0:
+        if child in self.agents or child < 0 or adapter < 0 or not self._lineage_ok(child, adapter):
             return E_INVALID, 0
-        pages = self.match_prefix(tokens)
+        path = self._match(self.base_root, tokens)
+        pages = [nd.page for nd in path]
         k = len(pages)
         if len(self.pools[RES].free) < k:
             return E_NEEDS_EVICTION, 0
+        self._touch(BASE, path)
         c = Agent(child, adapter, child, k * self.P)
         c.base = list(pages)
         for pg in pages:
@@ -231,22 +267,124 @@ class ControlPlane:
         return OK
 
     def _tree_insert(self, ag: Agent, slot: int) -> None:
-        """R7: page `slot` of agent became full: insert chunks 0..slot."""
+        """R7: page `slot` of agent became full: insert chunks 0..slot (a
+        chunk missing from the tree, e.g. evicted, is (re)inserted with the
+        agent's page).  The walk is one access of each tree (R10)."""
         for kind, table in ((BASE, ag.base), (RES, ag.res)):
             if kind == BASE:
                 node = self.base_root
             else:
-                node = self.res_roots.setdefault(ag.owner, Node(-1))
+                if ag.owner not in self.res_roots:
+                    self.res_roots[ag.owner] = Node(-1)
+                    self.res_adapter[ag.owner] = ag.adapter
+                node = self.res_roots[ag.owner]
+            self.clock[kind] += 1
             for k in range(slot + 1):
                 chunk = tuple(ag.tokens[k * self.P:(k + 1) * self.P])
                 ch = node.children.get(chunk)
                 if ch is None:
                     pg = table[k]
-                    ch = Node(pg)
+                    ch = Node(pg, seq=self.nseq[kind])
+                    self.nseq[kind] += 1
                     node.children[chunk] = ch
                     self.pools[kind].retain(pg)
                     self.pools[kind].in_tree[pg] = True
+                ch.last = self.clock[kind]
                 node = ch
+
+    # ---- R11: fork with partial hit ------------------------------------------
+    def fork_resume(self, child: int, adapter: int, owner: int, tokens: List[int]) -> Tuple[int, Tuple[int, int, int]]:
+        """Fork `child` over `tokens` reusing what survives in BOTH trees
+        (P:300 Step 1 + Step 2, P:304 partial hit).
+
+        base hit  = longest full-page prefix in the base tree (pages mapped);
+        res hit   = longest full-page prefix in the residual tree of `owner`
+                    (the lineage whose xA_i rows it holds; must have been
+                    produced with `adapter`);
+        mapped    = max of the two (tokens).  Base pages [base hit, mapped) and
+        residual pages [res hit, mapped) are fresh (unwritten) pages the
+        engine fills by recomputing only xW resp. xA_i for those rows.
+        All mapped pages are full, so they are inserted into both trees at
+        once (R7).  Returns (status, (base_hit, res_hit, mapped)) in tokens."""
+        if child in self.agents or child < 0 or adapter < 0 or owner < 0:
+            return E_INVALID, (0, 0, 0)
+        if not self._lineage_ok(owner, adapter):
+            return E_INVALID, (0, 0, 0)
+        bpath = self._match(self.base_root, tokens)
+        rpath = self._match(self.res_roots.get(owner), tokens)
+        bm, rm = len(bpath), len(rpath)
+        k = max(bm, rm)
+        if len(self.pools[BASE].free) < k - bm or len(self.pools[RES].free) < k - rm:
+            return E_NEEDS_EVICTION, (0, 0, 0)
+        c = Agent(child, adapter, owner, k * self.P)
+        c.base = [nd.page for nd in bpath]
+        c.res = [nd.page for nd in rpath]
+        for pg in c.base:
+            self.pools[BASE].retain(pg)
+        for pg in c.res:
+            self.pools[RES].retain(pg)
+        c.base += [self.pools[BASE].alloc() for _ in range(k - bm)]
+        c.res += [self.pools[RES].alloc() for _ in range(k - rm)]
+        c.tokens = list(tokens[:k * self.P])
+        self.agents[child] = c
+        if k > 0:
+            self._tree_insert(c, k - 1)
+        return OK, (bm * self.P, rm * self.P, k * self.P)
+
+    # ---- R12: decoupled eviction ----------------------------------------------
+    def _roots(self, kind: int) -> List[Node]:
+        return [self.base_root] if kind == BASE else [self.res_roots[o] for o in sorted(self.res_roots)]
+
+    def evictable_pages(self, kind: int) -> int:
+        """Pages `evict` could free: nodes whose whole subtree holds only
+        tree-only pages (refcount 1), since only unheld leaves go, bottom-up."""
+        pool = self.pools[kind]
+
+        def walk(nd: Node) -> Tuple[int, bool]:
+            tot, clean = 0, True
+            for ch in nd.children.values():
+                t, c = walk(ch)
+                tot += t
+                clean = clean and c
+            if nd.page >= 0:
+                clean = clean and pool.rc[nd.page] == 1
+                tot += 1 if clean else 0
+            return tot, clean
+
+        return sum(walk(r)[0] for r in self._roots(kind))
+
+    def evict(self, kind: int, n_pages: int) -> Tuple[int, int]:
+        """Free `n_pages` pages of ONE tree: repeatedly drop the
+        least recently used leaf (smallest (last, seq)) whose page no live
+        view holds.  The other tree, its clock and every agent table are
+        untouched.  Atomic: if fewer than n_pages can be freed, nothing is
+        evicted and E_NEEDS_EVICTION is returned."""
+        if kind not in (BASE, RES) or n_pages < 1:
+            return E_INVALID, 0
+        if self.evictable_pages(kind) < n_pages:
+            return E_NEEDS_EVICTION, 0
+        pool = self.pools[kind]
+        freed = 0
+        while freed < n_pages:
+            best = None
+            for ri, root in enumerate(self._roots(kind)):
+                stack = [(root, None, None)]
+                while stack:
+                    nd, parent, key = stack.pop()
+                    for ck, ch in nd.children.items():
+                        stack.append((ch, nd, ck))
+                    if nd.page >= 0 and not nd.children and pool.rc[nd.page] == 1:
+                        if best is None or (nd.last, nd.seq) < (best[0].last, best[0].seq):
+                            best = (nd, parent, key)
+            nd, parent, key = best
+            del parent.children[key]
+            pool.release(nd.page)
+            freed += 1
+            if kind == RES:
+                for o in [o for o, r in self.res_roots.items() if not r.children]:
+                    del self.res_roots[o]
+                    del self.res_adapter[o]
+        return OK, freed
 
     # ---- R6 -----------------------------------------------------------
     def release(self, a: int) -> int:
@@ -298,14 +436,15 @@ class ControlPlane:
         def walk(node: Node, depth: int, kind: int):
             for chunk in sorted(node.children):
                 ch = node.children[chunk]
-                out.append(f" {depth} page={ch.page} rc={self.pools[kind].rc[ch.page]} "
-                           f"tok={','.join(map(str, chunk))}")
+                out.append(f" {depth} page={ch.page} rc={self.pools[kind].rc[ch.page]} last={ch.last} "
+                           f"seq={ch.seq} tok={','.join(map(str, chunk))}")
                 walk(ch, depth + 1, kind)
 
-        out.append("base_tree")
+        out.append(f"base_tree clock={self.clock[BASE]} seq={self.nseq[BASE]}")
         walk(self.base_root, 0, BASE)
+        out.append(f"res_forest clock={self.clock[RES]} seq={self.nseq[RES]}")
         for o in sorted(self.res_roots):
-            out.append(f"res_tree owner={o}")
+            out.append(f"res_tree owner={o} adapter={self.res_adapter[o]}")
             walk(self.res_roots[o], 0, RES)
         return "\n".join(out) + "\n"
 

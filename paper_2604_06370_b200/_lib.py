@@ -81,6 +81,9 @@ SIGNATURES = {
     "fkv_create_root": ([_vp, _i64, _i32], _i32),
     "fkv_fork": ([_vp, _i64, _i64, _i64, _i32, _u32], _i32),
     "fkv_fork_tokens": ([_vp, _i64, _i32, _pi32, _i64, _pi64], _i32),
+    "fkv_fork_resume": ([_vp, _i64, _i32, _i64, _pi32, _i64, _pi64, _pi64, _pi64], _i32),
+    "fkv_evict": ([_vp, _i32, _i64, _pi64], _i32),
+    "fkv_evictable_pages": ([_vp, _i32, _pi64], _i32),
     "fkv_append": ([_vp, _i32, _pi64, _pi32, _pi32, _vp], _i32),
     "fkv_write_kv": ([_vp, _i32, _i32, _pi64, _pi64, _pi32, _vp, _vp, _vp, _vp, _u32, _vp], _i32),
     "fkv_release": ([_vp, _i64], _i32),

@@ -185,6 +185,25 @@ class ForkKV:
         self._c(self.lib.fkv_fork_tokens(self.ctx, child, adapter_id, p, len(tokens), ctypes.byref(m)))
         return m.value
 
+    def fork_resume(self, child: int, adapter_id: int, owner: int, tokens: Sequence[int]):
+        """Partial-hit fork: returns (base_hit, res_hit, mapped) in tokens."""
+        a, p = _arr(tokens if len(tokens) else [0], ctypes.c_int32)
+        bh, rh, mp = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        self._c(self.lib.fkv_fork_resume(self.ctx, child, adapter_id, owner, p, len(tokens), ctypes.byref(bh),
+                                         ctypes.byref(rh), ctypes.byref(mp)))
+        return bh.value, rh.value, mp.value
+
+    def evict(self, kind: int, n_pages: int) -> int:
+        """Decoupled eviction of one tree; returns the pages freed."""
+        f = ctypes.c_int64()
+        self._c(self.lib.fkv_evict(self.ctx, kind, n_pages, ctypes.byref(f)))
+        return f.value
+
+    def evictable_pages(self, kind: int) -> int:
+        n = ctypes.c_int64()
+        self._c(self.lib.fkv_evictable_pages(self.ctx, kind, ctypes.byref(n)))
+        return n.value
+
     def append(self, agents: Sequence[int], n_new: Sequence[int], token_ids: Sequence[int], stream=None):
         expected = int(np.sum(n_new)) if len(n_new) else 0
         if len(token_ids) != expected:

@@ -101,6 +101,25 @@ fkv_status fkv_fork_tokens(fkv_ctx* ctx, int64_t child, int32_t adapter_id, cons
   });
 }
 
+fkv_status fkv_fork_resume(fkv_ctx* ctx, int64_t child, int32_t adapter_id, int64_t owner, const int32_t* tokens,
+                           int64_t n, int64_t* base_hit, int64_t* res_hit, int64_t* mapped) {
+  if (!ctx || !base_hit || !res_hit || !mapped) return FKV_E_INVALID;
+  return guard(ctx, [&] { fkv::fork_resume(ctx->c, child, adapter_id, owner, tokens, n, base_hit, res_hit, mapped); });
+}
+
+fkv_status fkv_evict(fkv_ctx* ctx, int32_t kind, int64_t n_pages, int64_t* freed) {
+  if (!ctx) return FKV_E_INVALID;
+  return guard(ctx, [&] {
+    const int64_t f = fkv::evict(ctx->c, kind, n_pages);
+    if (freed) *freed = f;
+  });
+}
+
+fkv_status fkv_evictable_pages(fkv_ctx* ctx, int32_t kind, int64_t* n_pages) {
+  if (!ctx || !n_pages || (kind != FKV_KIND_BASE && kind != FKV_KIND_RES)) return FKV_E_INVALID;
+  return guard(ctx, [&] { *n_pages = fkv::evictable_pages(ctx->c, kind); });
+}
+
 fkv_status fkv_append(fkv_ctx* ctx, int32_t n, const int64_t* agents, const int32_t* n_new,
                       const int32_t* token_ids, void* stream) {
   if (!ctx) return FKV_E_INVALID;

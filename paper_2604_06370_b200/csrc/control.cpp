@@ -30,7 +30,9 @@ void check_cuda(cudaError_t e, const char* what) {
 }
 
 // R7: page `slot` of `ag` became full: walk/insert its chunks 0..slot in the
-// base tree and in the residual tree under ag.owner. New nodes take one ref.
+// base tree and in the residual tree under ag.owner (a missing chunk, e.g. an
+// evicted one, is (re)inserted with the agent's page). New nodes take one ref.
+// The walk is one access of each tree: one tick of its own clock (R10).
 void tree_insert(Ctx& c, Agent& ag, int64_t slot) {
   const int P = c.cfg.page_size;
   for (int kind = 0; kind < 2; ++kind) {
@@ -39,9 +41,13 @@ void tree_insert(Ctx& c, Agent& ag, int64_t slot) {
       node = &c.base_root;
     } else {
       auto& root = c.res_roots[ag.owner];
-      if (!root) root = std::make_unique<TreeNode>();
+      if (!root) {
+        root = std::make_unique<TreeNode>();
+        c.res_adapter[ag.owner] = ag.adapter;
+      }
       node = root.get();
     }
+    const int64_t tick = ++c.clock[kind];
     const auto& table = kind == FKV_KIND_BASE ? ag.base : ag.res;
     for (int64_t k = 0; k <= slot; ++k) {
       std::vector<int32_t> chunk(ag.tokens.begin() + k * P, ag.tokens.begin() + (k + 1) * P);
@@ -49,6 +55,7 @@ void tree_insert(Ctx& c, Agent& ag, int64_t slot) {
       if (it == node->children.end()) {
         auto nd = std::make_unique<TreeNode>();
         nd->page = table[k];
+        nd->seq = c.nseq[kind]++;
         c.pools[kind].retain(table[k]);
         c.pools[kind].in_tree[table[k]] = 1;
         TreeNode* raw = nd.get();
@@ -57,8 +64,34 @@ void tree_insert(Ctx& c, Agent& ag, int64_t slot) {
       } else {
         node = it->second.get();
       }
+      node->last = tick;
     }
   }
+}
+
+// longest full-page prefix of tokens[0, n) stored under `root` (no touch)
+std::vector<TreeNode*> match_path(const TreeNode* root, const int32_t* tokens, int64_t n, int P) {
+  std::vector<TreeNode*> path;
+  const TreeNode* node = root;
+  if (!node) return path;
+  for (int64_t s = 0; s < n / P; ++s) {
+    std::vector<int32_t> chunk(tokens + s * P, tokens + (s + 1) * P);
+    auto it = node->children.find(chunk);
+    if (it == node->children.end()) break;
+    path.push_back(it->second.get());
+    node = it->second.get();
+  }
+  return path;
+}
+
+// R11: a residual lineage (tree key) holds the xA_i rows of ONE adapter: its surviving tree and every live view of
+// it must use `adapter`
+bool lineage_ok(const Ctx& c, int64_t owner, int32_t adapter) {
+  auto it = c.res_adapter.find(owner);
+  if (it != c.res_adapter.end() && it->second != adapter) return false;
+  for (const auto& kv : c.agents)
+    if (kv.second.owner == owner && kv.second.adapter != adapter) return false;
+  return true;
 }
 
 }  // namespace
@@ -128,7 +161,7 @@ void ctx_create(Ctx& c, const fkv_config& cfg, const fkv_buffers* buf) {
 }
 
 void create_root(Ctx& c, int64_t a, int32_t adapter) {
-  if (c.agents.count(a) || a < 0 || adapter < 0) throw Error(FKV_E_INVALID, "create_root: bad agent/adapter");
+  if (c.agents.count(a) || a < 0 || adapter < 0 || !lineage_ok(c, a, adapter)) throw Error(FKV_E_INVALID, "create_root: bad agent/adapter");
   Agent ag;
   ag.id = a; ag.adapter = adapter; ag.owner = a;
   c.agents.emplace(a, std::move(ag));
@@ -141,6 +174,8 @@ void fork(Ctx& c, int64_t parent, int64_t L, int64_t child, int32_t adapter, uin
     throw Error(FKV_E_INVALID, "fork: bad child/adapter/prefix_len");
   const bool share = flags & FKV_FORK_SHARE_RESIDUAL;
   if (share && adapter != p.adapter) throw Error(FKV_E_INVALID, "fork: SHARE_RESIDUAL needs the parent's adapter");
+  if (!share && !lineage_ok(c, child, adapter))
+    throw Error(FKV_E_INVALID, "fork: the child's residual lineage holds another adapter's rows");
   const int P = c.cfg.page_size;
   const int64_t k = (L + P - 1) / P;
   if (!share && c.pools[FKV_KIND_RES].n_free() < k) throw Error(FKV_E_NEEDS_EVICTION, "fork: residual pool exhausted");
@@ -160,20 +195,19 @@ void fork(Ctx& c, int64_t parent, int64_t L, int64_t child, int32_t adapter, uin
 }
 
 int64_t fork_tokens(Ctx& c, int64_t child, int32_t adapter, const int32_t* tokens, int64_t n) {
-  if (c.agents.count(child) || child < 0 || adapter < 0 || n < 0 || (n > 0 && !tokens))
+  if (c.agents.count(child) || child < 0 || adapter < 0 || n < 0 || (n > 0 && !tokens) ||
+      !lineage_ok(c, child, adapter))
     throw Error(FKV_E_INVALID, "fork_tokens: bad child/adapter/tokens");
   const int P = c.cfg.page_size;
+  const std::vector<TreeNode*> path = match_path(&c.base_root, tokens, n, P);
   std::vector<int32_t> pages;
-  const TreeNode* node = &c.base_root;
-  for (int64_t s = 0; s < n / P; ++s) {
-    std::vector<int32_t> chunk(tokens + s * P, tokens + (s + 1) * P);
-    auto it = node->children.find(chunk);
-    if (it == node->children.end()) break;
-    pages.push_back(it->second->page);
-    node = it->second.get();
-  }
+  for (const TreeNode* nd : path) pages.push_back(nd->page);
   const int64_t k = (int64_t)pages.size();
   if (c.pools[FKV_KIND_RES].n_free() < k) throw Error(FKV_E_NEEDS_EVICTION, "fork_tokens: residual pool exhausted");
+  if (!path.empty()) {  // the match is one access of the base tree (R10)
+    const int64_t tick = ++c.clock[FKV_KIND_BASE];
+    for (TreeNode* nd : path) nd->last = tick;
+  }
   Agent ch;
   ch.id = child; ch.adapter = adapter; ch.owner = child; ch.seqlen = k * P;
   ch.base = pages;
@@ -183,6 +217,112 @@ int64_t fork_tokens(Ctx& c, int64_t child, int32_t adapter, const int32_t* token
   c.agents.emplace(child, std::move(ch));
   ++c.generation;
   return k * P;
+}
+
+// R11 (P:300 Step 1 + Step 2, P:304 partial hit): map the surviving base pages AND the surviving residual pages of
+// lineage `owner`; the rows of whichever part is missing are fresh pages the engine recomputes (xW only, or xA_i
+// only). All mapped pages are full and are inserted into both trees at once.
+void fork_resume(Ctx& c, int64_t child, int32_t adapter, int64_t owner, const int32_t* tokens, int64_t n,
+                 int64_t* base_hit, int64_t* res_hit, int64_t* mapped) {
+  if (c.agents.count(child) || child < 0 || adapter < 0 || owner < 0 || n < 0 || (n > 0 && !tokens))
+    throw Error(FKV_E_INVALID, "fork_resume: bad child/adapter/owner/tokens");
+  if (!lineage_ok(c, owner, adapter))
+    throw Error(FKV_E_INVALID, "fork_resume: the residual lineage holds another adapter's rows");
+  const int P = c.cfg.page_size;
+  auto rt = c.res_roots.find(owner);
+  const std::vector<TreeNode*> bpath = match_path(&c.base_root, tokens, n, P);
+  const std::vector<TreeNode*> rpath = match_path(rt == c.res_roots.end() ? nullptr : rt->second.get(), tokens, n, P);
+  const int64_t bm = (int64_t)bpath.size(), rm = (int64_t)rpath.size(), k = std::max(bm, rm);
+  if (c.pools[FKV_KIND_BASE].n_free() < k - bm || c.pools[FKV_KIND_RES].n_free() < k - rm)
+    throw Error(FKV_E_NEEDS_EVICTION, "fork_resume: pool exhausted");
+  Agent ch;
+  ch.id = child; ch.adapter = adapter; ch.owner = owner; ch.seqlen = k * P;
+  for (const TreeNode* nd : bpath) { ch.base.push_back(nd->page); c.pools[FKV_KIND_BASE].retain(nd->page); }
+  for (const TreeNode* nd : rpath) { ch.res.push_back(nd->page); c.pools[FKV_KIND_RES].retain(nd->page); }
+  for (int64_t i = bm; i < k; ++i) ch.base.push_back(c.pools[FKV_KIND_BASE].alloc());
+  for (int64_t i = rm; i < k; ++i) ch.res.push_back(c.pools[FKV_KIND_RES].alloc());
+  ch.tokens.assign(tokens, tokens + k * P);
+  Agent& ref = c.agents.emplace(child, std::move(ch)).first->second;
+  if (k > 0) tree_insert(c, ref, k - 1);
+  ++c.generation;
+  *base_hit = bm * P; *res_hit = rm * P; *mapped = k * P;
+}
+
+namespace {
+// pages of the subtree of `nd` that evict() could free, and whether every page in it is tree-only (refcount 1)
+std::pair<int64_t, bool> evictable_walk(const TreeNode& nd, const PagePool& pool) {
+  int64_t tot = 0;
+  bool clean = true;
+  for (const auto& kv : nd.children) {
+    auto r = evictable_walk(*kv.second, pool);
+    tot += r.first;
+    clean = clean && r.second;
+  }
+  if (nd.page >= 0) {
+    clean = clean && pool.rc[nd.page] == 1;
+    tot += clean ? 1 : 0;
+  }
+  return {tot, clean};
+}
+std::vector<TreeNode*> roots_of(Ctx& c, int32_t kind) {
+  std::vector<TreeNode*> r;
+  if (kind == FKV_KIND_BASE) r.push_back(&c.base_root);
+  else for (auto& kv : c.res_roots) r.push_back(kv.second.get());
+  return r;
+}
+}  // namespace
+
+int64_t evictable_pages(const Ctx& c, int32_t kind) {
+  if (kind == FKV_KIND_BASE) return evictable_walk(c.base_root, c.pools[0]).first;
+  int64_t t = 0;
+  for (const auto& kv : c.res_roots) t += evictable_walk(*kv.second, c.pools[1]).first;
+  return t;
+}
+
+// R12 decoupled eviction (§5.2): free n_pages pages of ONE tree by repeatedly dropping its least
+// recently used leaf (smallest (last, seq)) whose page no live view holds. The other tree, its clock and every
+// agent table are untouched. Atomic: fewer evictable pages than asked -> E_NEEDS_EVICTION, nothing evicted.
+int64_t evict(Ctx& c, int32_t kind, int64_t n_pages) {
+  if ((kind != FKV_KIND_BASE && kind != FKV_KIND_RES) || n_pages < 1) throw Error(FKV_E_INVALID, "evict: bad kind/count");
+  const int64_t avail = evictable_pages(c, kind);
+  if (avail < n_pages)
+    throw Error(FKV_E_NEEDS_EVICTION, "evict: only " + std::to_string(avail) + " evictable pages, " +
+                                          std::to_string(n_pages) + " asked");
+  PagePool& pool = c.pools[kind];
+  int64_t freed = 0;
+  while (freed < n_pages) {
+    TreeNode* best = nullptr;
+    TreeNode* best_parent = nullptr;
+    const std::vector<int32_t>* best_key = nullptr;
+    std::vector<TreeNode*> stack = roots_of(c, kind);
+    while (!stack.empty()) {
+      TreeNode* nd = stack.back();
+      stack.pop_back();
+      for (auto& kv : nd->children) {
+        TreeNode* ch = kv.second.get();
+        if (ch->children.empty() && pool.rc[ch->page] == 1 &&
+            (!best || ch->last < best->last || (ch->last == best->last && ch->seq < best->seq))) {
+          best = ch; best_parent = nd; best_key = &kv.first;
+        }
+        stack.push_back(ch);
+      }
+    }
+    const int32_t pg = best->page;
+    best_parent->children.erase(*best_key);
+    pool.release(pg);
+    ++freed;
+    if (kind == FKV_KIND_RES) {
+      for (auto it = c.res_roots.begin(); it != c.res_roots.end();) {
+        if (it->second->children.empty()) {
+          c.res_adapter.erase(it->first);
+          it = c.res_roots.erase(it);
+        } else {
+          ++it;
+        }
+      }
+    }
+  }
+  return freed;
 }
 
 void append(Ctx& c, int32_t n, const int64_t* agents, const int32_t* n_new, const int32_t* tokens, void* stream) {
@@ -328,7 +468,8 @@ void join(std::ostringstream& o, const std::vector<int32_t>& v) {
 }
 void walk(std::ostringstream& o, const TreeNode& nd, int depth, const PagePool& pool) {
   for (const auto& kv : nd.children) {
-    o << " " << depth << " page=" << kv.second->page << " rc=" << pool.rc[kv.second->page] << " tok=";
+    o << " " << depth << " page=" << kv.second->page << " rc=" << pool.rc[kv.second->page]
+      << " last=" << kv.second->last << " seq=" << kv.second->seq << " tok=";
     join(o, kv.first);
     o << "\n";
     walk(o, *kv.second, depth + 1, pool);
@@ -363,10 +504,11 @@ std::string dump(const Ctx& c) {
       if (p.rc[i] > 0) { o << (first ? "" : " ") << i << ":" << p.rc[i]; first = false; }
     o << "\n";
   }
-  o << "base_tree\n";
+  o << "base_tree clock=" << c.clock[0] << " seq=" << c.nseq[0] << "\n";
   walk(o, c.base_root, 0, c.pools[0]);
+  o << "res_forest clock=" << c.clock[1] << " seq=" << c.nseq[1] << "\n";
   for (const auto& kv : c.res_roots) {
-    o << "res_tree owner=" << kv.first << "\n";
+    o << "res_tree owner=" << kv.first << " adapter=" << c.res_adapter.at(kv.first) << "\n";
     walk(o, *kv.second, 0, c.pools[1]);
   }
   return o.str();

@@ -91,6 +91,8 @@ struct Agent {
 
 struct TreeNode {
   int32_t page = -1;
+  int64_t last = 0;   // the tree's LRU clock at the last access (R10)
+  int64_t seq = -1;   // insertion number in the tree (LRU tie-break)
   std::map<std::vector<int32_t>, std::unique_ptr<TreeNode>> children;
 };
 
@@ -109,6 +111,9 @@ struct Ctx {
   std::unordered_map<int64_t, Agent> agents;
   TreeNode base_root;
   std::map<int64_t, std::unique_ptr<TreeNode>> res_roots;
+  std::map<int64_t, int32_t> res_adapter;  // residual lineage -> adapter whose xA_i rows it holds (R11)
+  int64_t clock[2] = {0, 0};               // independent LRU clocks of the base tree and residual forest (R10)
+  int64_t nseq[2] = {0, 0};                // insertion counters
   std::vector<int32_t> copy_log;  // quads (kind, src, dst, rows)
   std::vector<AdapterSlot> adapters;
   std::unordered_map<int32_t, int32_t> adapter_slot;
@@ -209,6 +214,10 @@ void ctx_create(Ctx& c, const fkv_config& cfg, const fkv_buffers* buf);
 void create_root(Ctx& c, int64_t a, int32_t adapter);
 void fork(Ctx& c, int64_t parent, int64_t L, int64_t child, int32_t adapter, uint32_t flags, void* stream);
 int64_t fork_tokens(Ctx& c, int64_t child, int32_t adapter, const int32_t* tokens, int64_t n);
+void fork_resume(Ctx& c, int64_t child, int32_t adapter, int64_t owner, const int32_t* tokens, int64_t n,
+                 int64_t* base_hit, int64_t* res_hit, int64_t* mapped);
+int64_t evict(Ctx& c, int32_t kind, int64_t n_pages);
+int64_t evictable_pages(const Ctx& c, int32_t kind);
 void append(Ctx& c, int32_t n, const int64_t* agents, const int32_t* n_new, const int32_t* tokens, void* stream);
 void write_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int64_t* start, const int32_t* count,
               const void* kb, const void* vb, const void* rk, const void* rv, uint32_t mask, void* stream);

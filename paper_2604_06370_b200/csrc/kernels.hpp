@@ -1,5 +1,6 @@
 // Launch interface between the host library and the sm_100a kernels.
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -127,7 +128,8 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   la[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = la;
-  cfg.numAttrs = 1;
+  static const bool no_pdl = std::getenv("FKV_NO_PDL") != nullptr;  // diagnostics: plain stream-ordered launches
+  cfg.numAttrs = no_pdl ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

@@ -16,6 +16,14 @@ def _lib_ctx(P, nb, nr, seed=0, L_=2):
                   n_res_pages=nr, dtype="f32", device=None, alloc_order_seed=seed)
 
 
+def _sections(dump):
+    """(agent tables, base pool + tree, residual pool + forest) of a dump."""
+    lines = dump.splitlines()
+    return ("\n".join(l for l in lines if l.startswith("agent ")),
+            "\n".join(l for l in lines if l.startswith("base_")) + dump.split("base_tree")[1].split("res_forest")[0],
+            "\n".join(l for l in lines if l.startswith("res_")) + dump.split("res_forest")[1])
+
+
 def _st(fn, *a):
     try:
         r = fn(*a)
@@ -182,3 +190,70 @@ def test_partitioner():
         assert h1 - h0 == 4 and a1 - a0 == 32
         seen.add((h0, a0))
     assert len(seen) == 8
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_eviction_partial_hit_bit_exact(seed):
+    """R10-R12 (decoupled eviction + partial hit): library vs oracle,
+    bit-exact dumps (LRU clocks, insertion numbers, free-set order), status
+    codes, evicted counts and partial-hit ranges over random scenarios, plus
+    the decoupling property on the library itself (SPEC acceptance #7)."""
+    rnd = random.Random(31000 + seed)
+    P = rnd.choice([2, 4, 8])
+    nb, nr = rnd.randint(12, 40), rnd.randint(12, 48)
+    aseed = rnd.choice([0, 777])
+    o = cp.ControlPlane(P, nb, nr, alloc_order_seed=aseed)
+    m = _lib_ctx(P, nb, nr, seed=aseed)
+    nxt = 0
+    vocab = rnd.choice([2, 3])
+    for step in range(80):
+        live = sorted(o.agents)
+        x = rnd.random()
+        if x < 0.15 or not live:
+            a, ad = nxt, rnd.randrange(3)
+            so, (sm, _) = o.create_root(a, ad), _st(m.create_root, a, ad)
+            nxt += 1
+        elif x < 0.45:
+            ags = rnd.sample(live, rnd.randint(1, min(2, len(live))))
+            ns = [rnd.randint(0, 2 * P) for _ in ags]
+            toks = [rnd.randrange(vocab) for _ in range(sum(ns))]
+            so, (sm, _) = o.append(ags, ns, toks), _st(m.append, ags, ns, toks)
+        elif x < 0.57:
+            a = rnd.choice(live)
+            so, (sm, _) = o.release(a), _st(m.release, a)
+        elif x < 0.72:
+            toks = [rnd.randrange(vocab) for _ in range(rnd.randint(0, 4 * P))]
+            owner = rnd.choice([nxt] + sorted(o.res_roots) + live[:1])
+            ad = o.res_adapter.get(owner, rnd.randrange(3)) if rnd.random() < 0.9 else rnd.randrange(3)
+            so, ro = o.fork_resume(nxt, ad, owner, toks)
+            sm, rm = _st(m.fork_resume, nxt, ad, owner, toks)
+            if so == 0:
+                assert rm == ro, (step, rm, ro)
+            nxt += 1
+        elif x < 0.77:
+            toks = [rnd.randrange(vocab) for _ in range(rnd.randint(0, 3 * P))]
+            ad = rnd.randrange(3)
+            so, mo = o.fork_tokens(nxt, ad, toks)
+            sm, mm = _st(m.fork_tokens, nxt, ad, toks)
+            if so == 0:
+                assert mm == mo
+            nxt += 1
+        else:
+            kind = rnd.choice([cp.BASE, cp.RES])
+            assert m.evictable_pages(kind) == o.evictable_pages(kind)
+            n = rnd.randint(1, 3)
+            before = m.dump()
+            so, fo = o.evict(kind, n)
+            sm, fm = _st(m.evict, kind, n)
+            if so == 0:
+                assert fm == fo == n
+                after = _sections(m.dump())
+                b4 = _sections(before)
+                assert after[0] == b4[0], step                      # agent tables untouched
+                other = 2 if kind == cp.BASE else 1
+                assert after[other] == b4[other], step              # the other tree is bit-identical
+        assert so == sm, (step, so, sm)
+        assert m.dump() == o.dump(), step
+        assert m.take_copy_log() == o.copies, step
+        o.copies.clear()
+        o.check_invariants()
