@@ -177,7 +177,7 @@ def _cpu_baseline(wl, mode, seed, max_seqs, budget_s=20.0):
             break
     # tokens: decode -> 1 per sequence; prefill -> C per sequence (sampled q_sample rows)
     per_token = spent / (done * q_sample) * wl.L
-    return {"value": 1.0 / per_token, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+    return {"value": 1.0 / per_token, "unit": "tokens/s", "cores": threads, "kind": "oracle", "host": _host_cpu_info(),
             "sample": f"{done} of {len(wl.batch)} sequences x {q_sample} query row(s), layer 0 of {wl.L} (full context, "
                       f"fp64, {threads} threads over kv heads), extrapolated x{wl.L} layers; oracle time {spent:.2f}s"}
 
@@ -210,152 +210,296 @@ def run_reference(args):
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": wl.desc, "rope_mode": args.mode},
            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+                            "host": _host_cpu_info(),
                             "sample": f"each step: 1 sequence x {q_sample} query row(s) x layer 0 of {wl.L}, "
                                       f"extrapolated to tokens/s over all layers"},
            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
+def _host_cpu_info():
+    """nproc, the cgroup CPU quota and the CPU model of the host (SURVEY §8(d) oracle timing)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        info["affinity"] = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    try:
+        q, per = open("/sys/fs/cgroup/cpu.max").read().split()
+        info["cgroup_cpu_quota"] = None if q == "max" else round(int(q) / int(per), 2)
+    except Exception:
+        info["cgroup_cpu_quota"] = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu_model"] = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return info
 
-    from paper_2604_06370_b200.api import ForkKV, synth_fill
-    from workloads import driver, synth
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = Workload(args.config, world, rank)
-    scen, batch, C = wl.scen, wl.batch, wl.C
-    P = args.page
-    B = len(batch)
-    h0, h1 = wl.kv
-    nb, nr = scen.pages_needed(P)
-    nb += B + 8
-    nr += B + 8
-    max_pos = max(scen.seqlen(s.id) for s in scen.agents) + args.warmup + args.steps + 8
-    t_setup = time.time()
-    fkv = ForkKV(n_layers=wl.L, n_q_heads=wl.Hq, n_kv_heads=wl.Hkv, head_dim=wl.d, rank=wl.r, page_size=P,
-                 n_base_pages=nb, n_res_pages=nr, dtype="bf16", rope_mode=args.mode, device=local, max_pos=max_pos,
-                 rope_theta=500000.0, llama3=True, kv_heads=(h0, h1))
-    hq = fkv.hq
-    seed = args.seed + (1000 * rank if wl.scaling == "weak" else 0)
-    driver.build(fkv, scen, seed, h0=h0)
-    dev = torch.device("cuda", local)
-    prefill = wl.kind == "prefill"
-    n_q_rows = B * C
-    Q = torch.empty(wl.L, n_q_rows, hq, wl.d, dtype=torch.bfloat16, device=dev)
-    O = torch.empty_like(Q)
-    for layer in range(wl.L):
-        driver.make_queries(fkv, scen, seed, layer, step=1, h0=h0, out=Q[layer])
-    kb = torch.empty(wl.L, B, fkv.hkv, wl.d, dtype=torch.bfloat16, device=dev)
-    vb = torch.empty_like(kb)
-    rk = torch.empty(wl.L, B, wl.r, dtype=torch.bfloat16, device=dev)
-    rv = torch.empty_like(rk)
-    for layer in range(wl.L):
-        synth_fill(kb[layer], seed, synth.KIND_KBASE, 777, layer, 0, head0=h0)
-        synth_fill(vb[layer], seed, synth.KIND_VBASE, 777, layer, 0, head0=h0)
-        synth_fill(rk[layer], seed, synth.KIND_RK, 777, layer, 0)
-        synth_fill(rv[layer], seed, synth.KIND_RV, 777, layer, 0)
-    pl0 = fkv.plan([(a, C) for a in batch], upload=False)
-    plan_buf = torch.empty(max(1 << 24, 2 * pl0.info.device_bytes), dtype=torch.uint8, device=dev)
-    ws_buf = torch.empty(max(64, 2 * pl0.info.workspace_bytes // 4), dtype=torch.float32, device=dev)
-    if prefill:
-        fkv.plan_upload(pl0, dev=plan_buf, ws=ws_buf)
-    torch.cuda.synchronize()
-    t_setup = time.time() - t_setup
-    stream = torch.cuda.current_stream()
-    ones = [1] * B
-    seqlens = {a: fkv.get_table(a)[2] for a in batch}   # host-side bookkeeping (no D2H)
-    state = {"tok": 0, "events": [], "launches": 0, "info": pl0.info}
+KERNEL_NAMES = {0: "mma.sync grouped (baseline)", 1: "simt", 2: "tcgen05 keys-on-lanes (+ stager)",
+                3: "tcgen05 rows-on-lanes"}
 
-    def step(record=False, host=None):
-        if prefill:
-            pl = pl0                      # the chunk's K/V rows are resident; same plan every step
+
+def _launches_per_layer(kernel):
+    """Our kernels per layer: main (+ the stager of kernel 2) + combine."""
+    return 3 if kernel == 2 else 2
+
+
+class Run:
+    """One configured workload on this rank: the control plane, resident pools, Q/O and new-row buffers."""
+
+    def __init__(self, args, wl, mode, world, rank, dev_index):
+        import torch
+        from paper_2604_06370_b200.api import ForkKV, synth_fill
+        from workloads import driver, synth
+        self.args, self.wl, self.mode = args, wl, mode
+        scen, batch, C = wl.scen, wl.batch, wl.C
+        P = args.page
+        B = len(batch)
+        self.B, self.C, self.P = B, C, P
+        self.h0, self.h1 = wl.kv
+        nb, nr = scen.pages_needed(P)
+        nb += B + 8
+        nr += B + 8
+        # every timed / warm-up / e2e decode step appends one token per sequence (DEFERRED needs the RoPE table to
+        # cover them: ADVICE r1)
+        appends = args.warmup + 2 * args.steps + 4
+        max_pos = max(scen.seqlen(s.id) for s in scen.agents) + appends + 16
+        t_setup = time.time()
+        self.fkv = fkv = ForkKV(n_layers=wl.L, n_q_heads=wl.Hq, n_kv_heads=wl.Hkv, head_dim=wl.d, rank=wl.r,
+                                page_size=P, n_base_pages=nb, n_res_pages=nr, dtype="bf16", rope_mode=mode,
+                                device=dev_index, max_pos=max_pos, rope_theta=500000.0, llama3=True,
+                                kv_heads=(self.h0, self.h1))
+        hq = fkv.hq
+        self.hq = hq
+        self.seed = seed = args.seed + (1000 * rank if wl.scaling == "weak" else 0)
+        driver.build(fkv, scen, seed, h0=self.h0)
+        dev = self.dev = torch.device("cuda", dev_index)
+        self.prefill = wl.kind == "prefill"
+        self.n_q_rows = B * C
+        self.Q = torch.empty(wl.L, self.n_q_rows, hq, wl.d, dtype=torch.bfloat16, device=dev)
+        self.O = torch.empty_like(self.Q)
+        for layer in range(wl.L):
+            driver.make_queries(fkv, scen, seed, layer, step=1, h0=self.h0, out=self.Q[layer])
+        self.kb = torch.empty(wl.L, B, fkv.hkv, wl.d, dtype=torch.bfloat16, device=dev)
+        self.vb = torch.empty_like(self.kb)
+        self.rk = torch.empty(wl.L, B, wl.r, dtype=torch.bfloat16, device=dev)
+        self.rv = torch.empty_like(self.rk)
+        for layer in range(wl.L):
+            synth_fill(self.kb[layer], seed, synth.KIND_KBASE, 777, layer, 0, head0=self.h0)
+            synth_fill(self.vb[layer], seed, synth.KIND_VBASE, 777, layer, 0, head0=self.h0)
+            synth_fill(self.rk[layer], seed, synth.KIND_RK, 777, layer, 0)
+            synth_fill(self.rv[layer], seed, synth.KIND_RV, 777, layer, 0)
+        self.pl0 = fkv.plan([(a, C) for a in batch], upload=False)
+        self.plan_buf = torch.empty(max(1 << 24, 2 * self.pl0.info.device_bytes), dtype=torch.uint8, device=dev)
+        self.ws_buf = torch.empty(max(64, 2 * self.pl0.info.workspace_bytes // 4), dtype=torch.float32, device=dev)
+        if self.prefill:
+            fkv.plan_upload(self.pl0, dev=self.plan_buf, ws=self.ws_buf)
+        torch.cuda.synchronize()
+        self.t_setup = time.time() - t_setup
+        self.stream = torch.cuda.current_stream()
+        self.seqlens = {a: fkv.get_table(a)[2] for a in batch}   # host-side bookkeeping (no D2H)
+        self.tok = 0
+        self.events, self.launches, self.alg_bytes, self.info = [], 0, [], self.pl0.info
+        self.pl = self.pl0
+
+    def step(self, record=False, host=None):
+        """One pass of the whole hot path over one batch: (decode) append + plan + upload, then per layer
+        kv_write + main kernel + combine."""
+        import torch
+        fkv, wl, batch = self.fkv, self.wl, self.wl.batch
+        B, ones = self.B, [1] * self.B
+        if self.prefill:
+            pl = self.pl0                     # the chunk's K/V rows are resident; same plan every step
         else:
-            toks = [(state["tok"] + i) % 32000 for i in range(B)]
-            state["tok"] += 1
+            toks = [(self.tok + i) % 32000 for i in range(B)]
+            self.tok += 1
             fkv.append(batch, ones, toks)
             for a in batch:
-                seqlens[a] += 1
+                self.seqlens[a] += 1
             pl = fkv.plan([(a, 1) for a in batch], upload=False)
-            fkv.plan_upload(pl, dev=plan_buf, ws=ws_buf)
-            state["info"] = pl.info
-        starts = [seqlens[a] - 1 for a in batch]
+            fkv.plan_upload(pl, dev=self.plan_buf, ws=self.ws_buf)
+            self.info = pl.info
+        self.pl = pl
+        if record:
+            self.alg_bytes.append(pl.info.alg_bytes)
+        starts = [self.seqlens[a] - 1 for a in batch]
+        Q, O = self.Q, self.O
         for layer in range(wl.L):
             if host is None:
-                if not prefill:
-                    fkv.write_kv(layer, batch, starts, ones, kb[layer], vb[layer], rk[layer], rv[layer])
-                    state["launches"] += 1
+                if not self.prefill:
+                    fkv.write_kv(layer, batch, starts, ones, self.kb[layer], self.vb[layer], self.rk[layer],
+                                 self.rv[layer])
+                    self.launches += 1
                 if record:
                     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
+                    e0.record(self.stream)
                     fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 1)
-                    e1.record(stream)
-                    state["events"].append((e0, e1))
+                    e1.record(self.stream)
+                    self.events.append((e0, e1))
                 else:
                     fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 1)
                 fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 2)
             else:
-                if not prefill:
+                if not self.prefill:
                     host["kv"](layer)
                     fkv.write_kv(layer, batch, starts, ones, host["dkb"], host["dvb"], host["drk"], host["drv"])
-                    state["launches"] += 1
+                    self.launches += 1
                 fkv.residual_attention_host(pl, layer, host["q"][layer], host["o"][layer], host["dq"], host["do"])
-            # tcgen05 path: stager + main kernel + combine; mma.sync / SIMT: main kernel + combine
-            state["launches"] += 3 if pl.info.kernel == 2 else 2
+            self.launches += _launches_per_layer(pl.info.kernel)
         return pl
 
+    def graph_median_ms(self, reps=25):
+        """Main-kernel time of layer 0 as the median over `reps` CUDA-graph replays."""
+        import torch
+        try:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self.fkv.residual_attention_phases(self.pl, 0, self.Q[0], self.O[0], 1)  # warm on the side stream
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=s):
+                    self.fkv.residual_attention_phases(self.pl, 0, self.Q[0], self.O[0], 1)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(reps + 5):
+                e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                g.replay()
+                e1.record(s)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            return statistics.median(ts[5:])
+        except Exception as e:  # capture is a measurement aid, not part of the hot path
+            print(f"graph timing unavailable: {e}", file=sys.stderr)
+            return None
+
+    def free(self):
+        import torch
+        del self.fkv, self.Q, self.O, self.kb, self.vb, self.rk, self.rv, self.plan_buf, self.ws_buf
+        torch.cuda.empty_cache()
+
+
+def _timed(run, args, world, dist_ok, dev_index):
+    """Warm-up, then exactly args.steps steps between barrier + synchronize; returns (ms per step, clocks)."""
+    import torch
+    import torch.distributed as dist
     for _ in range(args.warmup):
-        step()
+        run.step()
     torch.cuda.synchronize()
-    if world > 1:
+    if world > 1 and dist_ok:
         dist.barrier()
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev_index)
     clk.start()
     time.sleep(0.3)
-    state["events"].clear()
-    state["launches"] = 0
+    run.events.clear()
+    run.alg_bytes.clear()
+    run.launches = 0
     t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    t0.record(stream)
+    t0.record(run.stream)
     for _ in range(args.steps):
-        step(record=True)
-    t1.record(stream)
+        run.step(record=True)
+    t1.record(run.stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
-    ms = t0.elapsed_time(t1) / args.steps
-    main_ms = [a.elapsed_time(b) for a, b in state["events"]]
-    launches = state["launches"]
-    info = state["info"]
-    ms_t = torch.tensor([ms], device=dev)
+    return t0.elapsed_time(t1) / args.steps, clocks
+
+
+def _max_over_ranks(x, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.barrier()
-    ms = float(ms_t.item())
-    tokens_per_step = n_q_rows
-    if wl.scaling == "weak":
-        value = tokens_per_step * world / (ms / 1e3)
-    else:  # strong (c4): every rank holds a slice of the same batch; tokens counted once
-        n_tok = torch.tensor([tokens_per_step if h0 == 0 else 0], device=dev)
-        if world > 1:
-            dist.all_reduce(n_tok)
-        value = float(n_tok.item()) / (ms / 1e3)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(x, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t)
+    return float(t.item())
+
+
+def tokens_value(tokens_per_step_rank, ms_max, world, scaling, counts_tokens, sum_fn=None):
+    """Whole-job tokens/s: weak scaling counts every rank's own batch; strong scaling (c4: every rank holds a slice
+    of ONE batch) counts each sequence once (the ranks of head shard 0). `sum_fn` sums over ranks."""
+    sum_fn = sum_fn or (lambda x: x)
+    if scaling == "weak":
+        return tokens_per_step_rank * world / (ms_max / 1e3)
+    return sum_fn(tokens_per_step_rank if counts_tokens else 0) / (ms_max / 1e3)
+
+
+def _roofline(run, wl, ms, hbm, tc_sus, src, config_name, mode):
+    main_ms = [a.elapsed_time(b) for a, b in run.events]
+    avg_main = sum(main_ms) / len(main_ms)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{config_name}_{mode}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    kname = KERNEL_NAMES.get(run.info.kernel, "?")
+    window = "main kernel only" if run.info.kernel == 3 else "stager + main kernel" if run.info.kernel == 2 else \
+        "main kernel"
+    if run.prefill:
+        flops = wl.flops_per_layer(run.fkv.hkv, run.fkv.group)
+        achieved = flops / (avg_main / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tc_sus, "unit": "TFLOP/s", "frac": achieved / tc_sus,
+                "traffic": traffic, "peak_source": f"{src} (sustained bf16)", "alg_flops_per_launch": flops}
+    else:
+        alg = statistics.mean(run.alg_bytes)   # the timed steps' own bytes (each step appends one token)
+        achieved = alg / (avg_main / 1e3) / 1e9
+        layer_ms = ms / wl.L
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "peak_source": src, "alg_bytes_per_launch": alg,
+                "frac_whole_layer": alg / (layer_ms / 1e3) / 1e9 / hbm,
+                "frac_vs_8tbs_spec": achieved / 8000.0}
+    roof.update({"kernel": f"ResidualAttention {kname} (one launch per layer)", "event_window": window,
+                 "avg_launch_ms": avg_main, "share_of_step": sum(main_ms) / len(run.alg_bytes or [1]) / ms})
+    return roof
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_dev = torch.cuda.device_count()
+    if n_dev < 1:
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    dev_index = local % n_dev
+    torch.cuda.set_device(dev_index)
+    if world > 1:
+        # the hot path has no data-path collective (DESIGN §6): ranks exchange only scalars (barrier, max time,
+        # token counts), over gloo so that ranks sharing one GPU work too
+        dist.init_process_group("gloo")
+    wl = Workload(args.config, world, rank)
+    run = Run(args, wl, args.mode, world, rank, dev_index)
+    ms, clocks = _timed(run, args, world, True, dev_index)
+    launches = run.launches
+    ms = _max_over_ranks(ms, world)
+    value = tokens_value(run.n_q_rows, ms, world, wl.scaling, run.h0 == 0, lambda x: _sum_over_ranks(x, world))
+    graph_ms = run.graph_median_ms() if not args.no_graph else None
 
     # ---- e2e: host buffers through the C-ABI ----------------------------------
     e2e = None
     if not args.no_e2e:
-        qh = torch.empty(wl.L, n_q_rows, hq, wl.d, dtype=torch.bfloat16, pin_memory=True)
-        qh.copy_(Q.cpu())
+        L_, hq, d = wl.L, run.hq, wl.d
+        qh = torch.empty(L_, run.n_q_rows, hq, d, dtype=torch.bfloat16, pin_memory=True)
+        qh.copy_(run.Q.cpu())
         oh = torch.empty_like(qh).pin_memory()
-        kvh = [t.cpu().pin_memory() for t in (kb, vb, rk, rv)]
-        dq = torch.empty(n_q_rows, hq, wl.d, dtype=torch.bfloat16, device=dev)
+        kvh = [t.cpu().pin_memory() for t in (run.kb, run.vb, run.rk, run.rv)]
+        dq = torch.empty(run.n_q_rows, hq, d, dtype=torch.bfloat16, device=run.dev)
         do = torch.empty_like(dq)
-        dkv = [torch.empty_like(t[0]) for t in (kb, vb, rk, rv)]
+        dkv = [torch.empty_like(t[0]) for t in (run.kb, run.vb, run.rk, run.rv)]
 
         def kv(layer):
             for dst, src in zip(dkv, kvh):
@@ -364,64 +508,65 @@ def run_ours(args):
         host = {"q": qh, "o": oh, "dq": dq, "do": do, "kv": kv, "dkb": dkv[0], "dvb": dkv[1], "drk": dkv[2],
                 "drv": dkv[3]}
         for _ in range(2):
-            step(host=host)
+            run.step(host=host)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        e0.record(run.stream)
         for _ in range(args.steps):
-            step(host=host)
-        e1.record(stream)
+            run.step(host=host)
+        e1.record(run.stream)
         torch.cuda.synchronize()
-        ems = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
-        if world > 1:
-            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-        h2d = wl.L * (n_q_rows * hq * wl.d * 2 + (0 if prefill else sum(t[0].numel() * 2 for t in (kb, vb, rk, rv))))
-        d2h = wl.L * n_q_rows * hq * wl.d * 2
-        e2e = {"value": value * ms / float(ems.item()), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
+        ems = _max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        h2d = L_ * (run.n_q_rows * hq * d * 2 + (0 if run.prefill else
+                                                 sum(t[0].numel() * 2 for t in (run.kb, run.vb, run.rk, run.rv))))
+        d2h = L_ * run.n_q_rows * hq * d * 2
+        e2e = {"value": value * ms / ems, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
+    hbm, tc, tc_sus, src = _peaks()
+    roof = _roofline(run, wl, ms, hbm, tc_sus, src, args.config, args.mode)
+    if graph_ms:
+        roof["graph_median_launch_ms"] = graph_ms
+        if not run.prefill:
+            roof["frac_graph_median"] = statistics.mean(run.alg_bytes) / (graph_ms / 1e3) / 1e9 / hbm
+    cfg = {"workload": wl.desc, "rope_mode": args.mode, "batch_per_gpu": run.B, "q_rows_per_seq": run.C,
+           "page_size": run.P, "keys_per_seq": max(wl.scen.seqlen(a) for a in wl.batch) + (0 if run.prefill else
+                                                                                         args.warmup),
+           "layers": wl.L, "kv_heads": [run.h0, run.h1], "parallelism": wl.parallelism,
+           "l2": "inputs larger than L2 (each step streams the whole per-layer cache, >>126 MB)",
+           "kernel": KERNEL_NAMES.get(run.info.kernel, "?"), "setup_s": round(run.t_setup, 1)}
+    deferred = None
+    if args.mode == "none" and not args.no_deferred and args.config == "c2" and wl.kind == "decode":
+        # the paper's own semantics (RoPE on the rebuilt residual, Alg1.335) timed in the same invocation
+        run.free()
+        drun = Run(args, wl, "deferred", world, rank, dev_index)
+        dms, dclk = _timed(drun, args, world, True, dev_index)
+        dms = _max_over_ranks(dms, world)
+        droof = _roofline(drun, wl, dms, hbm, tc_sus, src, args.config, "deferred")
+        deferred = {"value": tokens_value(drun.n_q_rows, dms, world, wl.scaling, drun.h0 == 0,
+                                          lambda x: _sum_over_ranks(x, world)),
+                    "unit": "tokens/s", "ms_per_step": dms, "kernel": KERNEL_NAMES.get(drun.info.kernel, "?"),
+                    "roofline_frac": droof["frac"], "avg_launch_ms": droof["avg_launch_ms"], "clocks": dclk,
+                    "gpu_launches": drun.launches}
+        drun.free()
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return
-    hbm, tc, tc_sus, src = _peaks()
-    avg_main = sum(main_ms) / len(main_ms)
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.mode}.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-    if prefill:
-        flops = wl.flops_per_layer(fkv.hkv, fkv.group)
-        achieved = flops / (avg_main / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": tc_sus, "unit": "TFLOP/s", "frac": achieved / tc_sus,
-                "traffic": traffic, "peak_source": f"{src} (sustained bf16)", "alg_flops_per_launch": flops}
-    else:
-        achieved = info.alg_bytes / (avg_main / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_source": src, "alg_bytes_per_launch": info.alg_bytes}
-    roof.update({"kernel": "ResidualAttention main kernel (one launch per layer)", "avg_launch_ms": avg_main,
-                 "share_of_step": sum(main_ms) / args.steps / ms})
     out = {
-        "metric": METRIC_PREFILL if prefill else METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "metric": METRIC_PREFILL if run.prefill else METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": wl.scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": wl.desc, "rope_mode": args.mode, "batch_per_gpu": B, "q_rows_per_seq": C,
-                   "page_size": P, "keys_per_seq": max(scen.seqlen(a) for a in batch) + (0 if prefill else args.warmup),
-                   "layers": wl.L, "kv_heads": [h0, h1], "parallelism": wl.parallelism,
-                   "l2": "inputs larger than L2 (each step streams the whole per-layer cache, >>126 MB)",
-                   "kernel": {0: "mma.sync grouped", 1: "simt", 2: "tcgen05"}.get(info.kernel, "?"),
-                   "setup_s": round(t_setup, 1)},
-        "roofline": roof,
-        "gpu_launches": launches,
-        "clocks": clocks,
+        "config": cfg, "roofline": roof, "gpu_launches": launches, "clocks": clocks,
     }
     if e2e:
         out["e2e"] = e2e
+    if deferred:
+        out["deferred"] = deferred
     if not args.no_cpu_baseline:
-        out["cpu_baseline"] = _cpu_baseline(wl, args.mode, seed, args.cpu_seqs)
+        out["cpu_baseline"] = _cpu_baseline(wl, args.mode, run.seed, args.cpu_seqs)
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
@@ -441,6 +586,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-deferred", action="store_true", help="skip the DEFERRED (paper semantics) sub-result")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph median main-kernel timing")
     ap.add_argument("--cpu-seqs", type=int, default=8)
     ap.add_argument("--page", type=int, default=128, help="tokens per KV page (DESIGN.md C-9)")
     args = ap.parse_args()

@@ -80,10 +80,11 @@ typedef struct fkv_config {
   int32_t n_kv_heads;     /* Hkv (whole model) */
   int32_t head_dim;       /* d: 64 or 128 (bf16 tensor-core path needs 128; SIMT path: even, <=256) */
   int32_t rank;           /* r: LoRA rank of the residual pool; adapters of smaller rank are zero-padded (C-8) */
-  int32_t page_size;      /* P: tokens per page, one of 16, 32, 64 (C-9) */
+  int32_t page_size;      /* P: tokens per page, any divisor of 128 (C-9); the tcgen05 kernels take 16..128,
+                             128 = one key tile per page (bench default) */
   int64_t n_base_pages;   /* pages in the bCache pool */
   int64_t n_res_pages;    /* pages in the rCache pool */
-  int32_t max_pos;        /* rows of the RoPE table */
+  int32_t max_pos;        /* rows of the RoPE table; DEFERRED plans refuse sequences longer than it (E_INVALID) */
   int32_t dtype;          /* FKV_DTYPE_*: element type of pools, adapters, Q and O */
   int32_t rope_mode;      /* FKV_ROPE_* */
   int32_t device;         /* CUDA device ordinal, or -1 for a host-only control plane */
@@ -268,8 +269,10 @@ fkv_status fkv_synth_fill(void* dst, int32_t dtype, uint64_t seed, int32_t kind,
                           int64_t pos0, int32_t n_pos, int32_t head0, int32_t n_head, int32_t n_col, float scale,
                           void* stream);
 /* Head x agent-batch partitioner (§8(e)): choose H kv-head shards and D
- * agent shards with H*D = G, H | n_kv_heads, minimising per-GPU bytes
- * base_bytes/H + res_bytes/D (+ replicated base if D > 1). */
+ * agent shards with H*D = G, H | n_kv_heads, minimising the per-GPU bytes
+ * base_bytes/H + res_bytes/D: a GPU holds the shared base of its H-th of the
+ * kv heads (replicated over the D agent shards) and the head-shared residual
+ * of its D-th of the agents (replicated over the H head shards). */
 fkv_status fkv_partition(int32_t G, int32_t n_kv_heads, int64_t base_bytes, int64_t res_bytes, int32_t* H,
                          int32_t* D);
 /* Shard of `rank` under (H, D): kv heads [*h0, *h1), agents [*a0, *a1) of n_agents. */
@@ -289,6 +292,10 @@ fkv_status fkv_selftest_umma(int32_t test, const void* A, const void* B, float* 
  * int64 [32 events][256 tiles], zeroed by the caller) is non-NULL, CTA
  * `block` stores clock64() stamps of its pipeline events. NULL disables. */
 fkv_status fkv_debug_timeline(fkv_ctx* ctx, void* dbg, int32_t block);
+/* Diagnostics: with the environment variable FKV_HANG_DIAG set, a pipeline wait of the rows kernel that spins
+ * far beyond any legitimate latency records where it waited (in host-mapped memory) and traps; this copies the
+ * report ("" if none) into buf (cap bytes, NUL-terminated). Readable after the resulting launch failure. */
+fkv_status fkv_debug_hang_report(char* buf, int64_t cap);
 
 #ifdef __cplusplus
 }

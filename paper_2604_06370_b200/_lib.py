@@ -104,6 +104,7 @@ SIGNATURES = {
     "fkv_synth_fill": ([_vp, _i32, _u64, _i32, _u64, _i32, _i64, _i32, _i32, _i32, _i32, _f32, _vp], _i32),
     "fkv_selftest_umma": ([_i32, _vp, _vp, _vp, _i32, _i32, _i32, _vp], _i32),
     "fkv_debug_timeline": ([_vp, _vp, _i32], _i32),
+    "fkv_debug_hang_report": ([ctypes.c_char_p, _i64], _i32),
     "fkv_partition": ([_i32, _i32, _i64, _i64, _pi32, _pi32], _i32),
     "fkv_partition_shard": ([_i32, _i32, _i32, _i32, _i64, _pi32, _pi32, _pi64, _pi64], _i32),
 }

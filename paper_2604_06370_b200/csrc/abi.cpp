@@ -1,3 +1,4 @@
+#include <cstdio>
 // extern "C" boundary: argument checks, exception -> status translation.
 #include <cmath>
 #include <cstring>
@@ -216,7 +217,7 @@ fkv_status fkv_plan_get_info(const fkv_plan* plan, fkv_plan_info* info) {
   info->n_rows = p.n_rows_q;
   info->n_segments = p.n_segments;
   info->n_items = (int64_t)p.items.size();
-  info->n_ctas = (int64_t)p.items.size();
+  info->n_ctas = p.kernel >= 2 ? (int64_t)p.n_ctas : (int64_t)p.items.size();  // persistent kernels: p.n_ctas
   info->n_warps = (int64_t)p.warps.size();
   info->n_entries = p.n_entries;
   info->key_tiles = p.key_tiles;
@@ -350,6 +351,13 @@ fkv_status fkv_partition_shard(int32_t rank, int32_t H, int32_t D, int32_t n_kv_
 }
 
 }  // extern "C"
+
+extern "C" fkv_status fkv_debug_hang_report(char* buf, int64_t cap) {
+  if (!buf || cap < 1) return FKV_E_INVALID;
+  const std::string r = fkv::k::hang_report();
+  std::snprintf(buf, (size_t)cap, "%s", r.c_str());
+  return FKV_OK;
+}
 
 extern "C" fkv_status fkv_debug_timeline(fkv_ctx* ctx, void* dbg, int32_t block) {
   if (!ctx || block < 0) return FKV_E_INVALID;

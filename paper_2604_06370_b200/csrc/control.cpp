@@ -397,6 +397,7 @@ void append(Ctx& c, int32_t n, const int64_t* agents, const int32_t* n_new, cons
   }
   ++c.generation;
   if (c.device && !copies.empty()) {
+    DeviceGuard dg(c);
     const auto pv = pool_view(c);
     for (size_t o = 0; o < copies.size(); o += k::kMaxCopies) {
       const int32_t m = (int32_t)std::min<size_t>(k::kMaxCopies, copies.size() - o);
@@ -445,6 +446,7 @@ void write_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int
     }
   }
   if (c.device && !runs.empty()) {
+    DeviceGuard dg(c);
     const auto pv = pool_view(c);
     for (size_t o = 0; o < runs.size(); o += k::kMaxRuns) {
       const int32_t m = (int32_t)std::min<size_t>(k::kMaxRuns, runs.size() - o);

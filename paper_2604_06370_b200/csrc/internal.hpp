@@ -1,6 +1,7 @@
 // Internal structures of the forkkv library (not part of the ABI).
 #pragma once
 #include <cstdint>
+#include <cuda_runtime.h>
 #include <algorithm>
 #include <map>
 #include <memory>
@@ -124,6 +125,8 @@ struct Ctx {
   std::vector<uint8_t> tc_maps;  // 5 CUtensorMap (base K, base V, R_k, R_v, K d-halves) for the tcgen05 kernel
   std::string last_error;
   size_t elem = 2;
+  uint64_t upload_seq = 0;                      // plan uploads so far
+  std::map<const void*, uint64_t> buffer_owner;  // device plan buffer -> upload id of the plan it holds
   void* dbg = nullptr;  // diagnostics buffer (fkv_debug_timeline)
   int32_t dbg_block = 0;
 
@@ -206,7 +209,20 @@ struct Plan {
          off_outent = 0, off_adapters = 0, off_qrow = 0, off_comb = 0,
          off_sptr = 0, off_sitems = 0, off_tptr = 0, off_trecs = 0, off_irecs = 0, off_ssrc = 0, off_sdesc = 0;
   void* dev = nullptr;
+  uint64_t upload_id = 0;  // Ctx::upload_seq at the upload into `dev`
   size_t ws_bytes = 0;
+};
+
+// Makes the ctx's device current for the scope of a library call that launches work (and restores the caller's).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const Ctx& c) {
+    if (c.device && cudaGetDevice(&prev) == cudaSuccess && prev != c.cfg.device) cudaSetDevice(c.cfg.device);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
 };
 
 // control.cpp

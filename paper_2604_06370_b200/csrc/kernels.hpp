@@ -1,6 +1,7 @@
 // Launch interface between the host library and the sm_100a kernels.
 #pragma once
 #include <cstdlib>
+#include <string>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -140,6 +141,9 @@ cudaError_t launch_stage(const AttnParams& p, int32_t n_warps, cudaStream_t s);
 size_t tc_maps_bytes();
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t s);
 cudaError_t launch_attention_rows(const RowsParams& p, const RowsMaps& maps, cudaStream_t s);
+// host-mapped deadlock report of the rows kernel (allocated on first use when FKV_HANG_DIAG is set, else nullptr)
+long long* hang_slot();
+std::string hang_report();
 
 cudaError_t launch_synth_fill(void* dst, int32_t dtype, uint64_t seed, int32_t kind, uint64_t owner, int32_t layer,
                               int64_t pos0, int32_t n_pos, int32_t head0, int32_t n_head, int32_t n_col, float scale,

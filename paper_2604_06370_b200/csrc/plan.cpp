@@ -56,7 +56,10 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
   // rows-on-lanes tcgen05 kernel (kernel 3, ra_rows.cu): NONE residual-RoPE mode, pages of 16..128 tokens
   const bool rows_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && c.has_rows_maps && (128 % P) == 0 &&
                        P >= 16 && c.cfg.rope_mode == FKV_ROPE_NONE && !(flags & (FKV_PLAN_FORCE_SIMT | FKV_PLAN_FORCE_MMA));
-  pl.kernel = rows_ok ? 3 : (tc_ok ? 2 : (mma_ok ? 0 : 1));
+  // the mma.sync kernel (warp-level, pre-Blackwell instruction set) is kept only as a comparison baseline: it runs
+  // when FKV_PLAN_FORCE_MMA asks for it, never by automatic selection (shapes the tcgen05 kernels do not take run
+  // on the SIMT kernel)
+  pl.kernel = rows_ok ? 3 : (tc_ok ? 2 : ((mma_ok && (flags & FKV_PLAN_FORCE_MMA)) ? 0 : 1));
   if (const char* kenv = getenv("FKV_KERNEL")) {
     const int kk = atoi(kenv);
     if (kk == 2 && tc_ok) pl.kernel = 2;
@@ -82,6 +85,10 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
     const Agent& ag = c.agent(seqs[b].agent);
     if (seqs[b].q_len < 1) throw Error(FKV_E_INVALID, "plan: q_len must be >= 1");
     if (seqs[b].q_len > ag.seqlen) throw Error(FKV_E_NO_KEYS, "plan: a query row has no keys");
+    // DEFERRED rotates every key at its absolute position (Alg1.335): the RoPE table must cover the sequence
+    if (c.device && c.cfg.rope_mode == FKV_ROPE_DEFERRED && ag.seqlen > c.cfg.max_pos)
+      throw Error(FKV_E_INVALID, "plan: agent " + std::to_string(ag.id) + " seqlen " + std::to_string(ag.seqlen) +
+                                     " exceeds the RoPE table (max_pos " + std::to_string(c.cfg.max_pos) + ")");
     auto it = c.adapter_slot.find(ag.adapter);
     if (it == c.adapter_slot.end()) throw Error(FKV_E_INVALID, "plan: adapter not registered");
     ags[b] = &ag;
@@ -483,9 +490,12 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
 void upload_plan(Ctx& c, Plan& p, void* dev, size_t bytes, void* stream) {
   if (!c.device) throw Error(FKV_E_INVALID, "plan_upload: host-only ctx");
   if (!dev || bytes < p.blob.size() || ((uintptr_t)dev & 255)) throw Error(FKV_E_INVALID, "plan_upload: bad buffer");
+  DeviceGuard dg(c);
   cudaError_t e = cudaMemcpyAsync(dev, p.blob.data(), p.blob.size(), cudaMemcpyHostToDevice, (cudaStream_t)stream);
   if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("plan_upload: ") + cudaGetErrorString(e));
   p.dev = dev;
+  p.upload_id = ++c.upload_seq;
+  c.buffer_owner[dev] = p.upload_id;  // a buffer belongs to the plan uploaded into it last
 }
 
 void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O, float scale, void* ws,
@@ -494,6 +504,12 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   if (!c.device) throw Error(FKV_E_INVALID, "attention: host-only ctx");
   if (p.generation != c.generation) throw Error(FKV_E_STALE, "attention: plan is stale");
   if (!p.dev) throw Error(FKV_E_INVALID, "attention: plan not uploaded");
+  {
+    auto it = c.buffer_owner.find(p.dev);
+    if (it == c.buffer_owner.end() || it->second != p.upload_id)
+      throw Error(FKV_E_STALE, "attention: another plan was uploaded into this plan's device buffer since");
+  }
+  DeviceGuard dg(c);
   if (layer < 0 || layer >= c.cfg.n_layers || !Q || !O) throw Error(FKV_E_INVALID, "attention: bad layer/Q/O");
   if (!ws || ws_bytes < p.ws_bytes || ((uintptr_t)ws & 255)) throw Error(FKV_E_INVALID, "attention: workspace too small or not 256-byte aligned");
   const uint8_t* base = (const uint8_t*)p.dev;
@@ -564,6 +580,8 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
       rp.scale_log2 = a.scale_log2;
       rp.dbg = a.dbg; rp.dbg_block = a.dbg_block;
       rp.flags = getenv("FKV_ROWS_FLAGS") ? atoi(getenv("FKV_ROWS_FLAGS")) : 0;
+      rp.hang = k::hang_slot();
+      rp.prefetch = getenv("FKV_ROWS_PREFETCH") ? atoi(getenv("FKV_ROWS_PREFETCH")) : 0;
       e = k::launch_attention_rows(rp, *(const k::RowsMaps*)c.rows_maps.data(), (cudaStream_t)stream);
     }
     if (e == cudaSuccess && (phases & FKV_PHASE_COMBINE)) e = k::launch_combine(a, (cudaStream_t)stream);

@@ -29,6 +29,9 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 
 #include "kernels.hpp"
 #include "rows.hpp"
@@ -84,16 +87,31 @@ __device__ __forceinline__ void mma_ts_m(uint32_t d, uint32_t a, uint64_t b, uin
 }
 // mbarrier phase wait: try_wait without a suspend-time hint (the hinted form compiles to NANOSLEEP.SYNCS with a
 // 1 ms hint whose wake-up latency cost several microseconds per wait on B200)
-__device__ __forceinline__ void wait_bar(uint32_t bar, uint32_t parity) {
+// With FKV_HANG_DIAG set, a wait that spins for ~2^27 polls records (block, warp, lane, barrier offset, parity,
+// site) into host-mapped memory (fkv_debug_hang_report) and traps, turning a pipeline deadlock into a located error.
+__device__ __forceinline__ void wait_bar_(uint32_t bar, uint32_t parity, long long* hang, int site) {
   uint32_t ok;
+  uint32_t n = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(ok)
         : "r"(bar), "r"(parity)
         : "memory");
+    if (!ok && ++n == (1u << 27) && hang != nullptr) {
+      extern __shared__ __align__(1024) uint8_t smem[];
+      hang[0] = 1;
+      hang[1] = blockIdx.x;
+      hang[2] = threadIdx.x;
+      hang[3] = (long long)(bar - smem_u32(smem));
+      hang[4] = parity;
+      hang[5] = site;
+      __threadfence_system();
+      __trap();
+    }
   } while (!ok);
 }
+#define wait_bar(bar, parity) wait_bar_((bar), (parity), p.hang, __LINE__)
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -127,6 +145,37 @@ __device__ __forceinline__ void walk(const RowsParams& p, F&& f) {
     f(1, ii - i0, it.n_tiles - 1, it.tile0 + it.n_tiles - 1, it.n_tiles);
   }
 }
+
+// Cursor over the CTA's tiles in processing order, `ahead` tiles in front of the loaders: the L2 prefetch of
+// the pages a loader will need `ahead` tiles later (HBM latency is longer than the shared-memory ring covers).
+struct TileCursor {
+  int ii, i1, t, n, tile0;
+  __device__ void init(const RowsParams& p, int ahead) {
+    ii = p.sched_ptr[blockIdx.x];
+    i1 = p.sched_ptr[blockIdx.x + 1];
+    t = -1;
+    n = 0;
+    tile0 = 0;
+    if (ii < i1) {
+      const RItem it = p.items[p.sched_items[ii]];
+      n = it.n_tiles;
+      tile0 = it.tile0;
+    }
+    for (int k = 0; k < ahead; ++k) next(p);
+  }
+  // advance one tile; returns its index or -1 past the end
+  __device__ int next(const RowsParams& p) {
+    if (ii >= i1) return -1;
+    if (++t >= n) {
+      t = 0;
+      if (++ii >= i1) return -1;
+      const RItem it = p.items[p.sched_items[ii]];
+      n = it.n_tiles;
+      tile0 = it.tile0;
+    }
+    return tile0 + t;
+  }
+};
 
 template <bool kDbg>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -326,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             s_ = u % kNU;
             wait_bar(smem_u32(&B.full[s_]), (u / kNU) & 1);
             tc_fence_after();
+            fence_async_smem();  // R_k pages land through cp.async (generic proxy)
             const uint32_t rb = sb + OFF_RING + s_ * kUnit;
             for (int s = 0; s < n_slots; ++s) {
               const uint4 ml = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].slot_lanes[s]));
@@ -357,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             wait_bar(smem_u32(&B.full[sr_]), ((u + 1) / kNU) & 1);
             stamp(p, 14, gp);
             tc_fence_after();
+            fence_async_smem();  // R_v pages land through cp.async (generic proxy)
             const uint32_t vb = sb + OFF_RING + sv * kUnit, rvb = sb + OFF_RING + sr_ * kUnit;
             for (int k = 0; k < nk; ++k) {
               const uint32_t acc = k ? 1u : acc0;
@@ -381,7 +432,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         int kt = 0;
         const int P = p.P;
         const int ppt = 128 / P;  // pages per tile
+        TileCursor pf;
+        pf.init(p, p.prefetch);
         walk(p, [&](int kind, int, int, int ti, int) {
+          if (kind == 0 && p.prefetch > 0) {
+            // base K and V pages of the tile `prefetch` tiles ahead into L2 (one contiguous P x d run per page)
+            const int tn = pf.next(p);
+            if (tn >= 0) {
+              const RTile* Tq = p.tiles + tn;
+              const int nk = __ldg(&Tq->n_keys), bo = __ldg(&Tq->base_off), hq = __ldg(&Tq->kv_head);
+              for (int pi = 0; pi < ppt && pi * P < nk; ++pi) {
+                const int pg = p.base_pages[bo + pi];
+                if (pg < 0) continue;
+                const size_t off = ((size_t)p.base_rows_layer + (size_t)pg * p.hkv * P + (size_t)hq * P) * 256;
+                bulk_prefetch_l2((const uint8_t*)p.base_k + off, (uint32_t)P * 256);
+                bulk_prefetch_l2((const uint8_t*)p.base_v + off, (uint32_t)P * 256);
+              }
+            }
+          }
           const RTile* Tp = p.tiles + ti;
           const int n_keys = __ldg(&Tp->n_keys), base_off = __ldg(&Tp->base_off);
           const int64_t hrow = (int64_t)__ldg(&Tp->kv_head) * P;
@@ -418,10 +486,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int P = p.P;
       const int ppt = 128 / P;  // pages per slot and tile (<= 8)
       const uint8_t* rp = (const uint8_t*)(is_rv ? p.res_v : p.res_k) + (size_t)p.layer * p.res_layer_elems * 2;
+      TileCursor pf;
+      pf.init(p, p.prefetch);
       walk(p, [&](int kind, int, int, int ti, int) {
         if ((kind == 1) != is_rv) {
           u += 2;
           return;
+        }
+        if (p.prefetch > 0) {
+          // this plane's residual pages of the tile `prefetch` tiles ahead into L2 (lane = (slot, page))
+          const int tn = pf.next(p);
+          if (tn >= 0) {
+            const RTile* Tq = p.tiles + tn;
+            const int nk = __ldg(&Tq->n_keys), nsq = __ldg(&p.wus[__ldg(&Tq->wu)].n_slots);
+            for (int q = lane; q < nsq * ppt; q += 32) {
+              const int s = q / ppt, pi = q % ppt;
+              if (pi * P >= nk) continue;
+              const int pg = p.res_pages[__ldg(&Tq->res_off[s]) + pi];
+              if (pg >= 0) bulk_prefetch_l2(rp + (size_t)pg * P * 32, (uint32_t)P * 32);
+            }
+          }
         }
         const RTile* Tp = p.tiles + ti;
         const int n_keys = __ldg(&Tp->n_keys);
@@ -430,21 +514,40 @@ __global__ void __launch_bounds__(kThreads, 1)
         wait_bar(smem_u32(&B.empty[s_]), (((u + 1) / kNU) & 1) ^ 1);
         const uint32_t dst = sb + OFF_RING + s_ * kUnit;
         const int np = ns * ppt;  // (slot, page) pieces
-        int mine = 0;             // bytes this lane copies
-        for (int q = lane; q < np; q += 32) {
-          const int s = q / ppt, pi = q % ppt;
-          if (pi * P < n_keys && p.res_pages[__ldg(&Tp->res_off[s]) + pi] >= 0) mine += P * 32;
-        }
-        int tot = mine;
+        if (!(p.flags & 1)) {
+          // one bulk copy per (slot, page) piece, issued by parallel lanes
+          int mine = 0;  // bytes this lane copies
+          for (int q = lane; q < np; q += 32) {
+            const int s = q / ppt, pi = q % ppt;
+            if (pi * P < n_keys && p.res_pages[__ldg(&Tp->res_off[s]) + pi] >= 0) mine += P * 32;
+          }
+          int tot = mine;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        if (lane == 0) mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)tot);
-        __syncwarp();
-        for (int q = lane; q < np; q += 32) {
-          const int s = q / ppt, pi = q % ppt;
-          if (pi * P >= n_keys) continue;
-          const int pg = p.res_pages[__ldg(&Tp->res_off[s]) + pi];
-          if (pg >= 0) bulk_g2s(dst + 4096u * s + pi * P * 32, rp + (size_t)pg * P * 32, P * 32, smem_u32(&B.full[s_]));
+          for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+          if (lane == 0) mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)tot);
+          __syncwarp();
+          for (int q = lane; q < np; q += 32) {
+            const int s = q / ppt, pi = q % ppt;
+            if (pi * P >= n_keys) continue;
+            const int pg = p.res_pages[__ldg(&Tp->res_off[s]) + pi];
+            if (pg >= 0)
+              bulk_g2s(dst + 4096u * s + pi * P * 32, rp + (size_t)pg * P * 32, P * 32, smem_u32(&B.full[s_]));
+          }
+        } else {
+          // diagnostics (FKV_ROWS_FLAGS bit 0): 16-byte cp.async by all lanes (LSU path; measured slower: 6.7 K vs
+          // 4.1 K cycles per tile on C2)
+          for (int q = 0; q < np; ++q) {
+            const int s = q / ppt, pi = q % ppt;
+            if (pi * P >= n_keys) continue;
+            const int pg = p.res_pages[__ldg(&Tp->res_off[s]) + pi];
+            if (pg < 0) continue;
+            const uint8_t* src = rp + (size_t)pg * P * 32;
+            const uint32_t d0 = dst + 4096u * s + pi * P * 32;
+            for (int c = lane; c < P * 2; c += 32) cp_async16(d0 + 16u * c, src + 16 * c);
+          }
+          cp_async_arrive_inc(smem_u32(&B.full[s_]));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&B.full[s_]));
         }
         u += 2;
       });
@@ -607,6 +710,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace
+
+long long* hang_slot() {
+  static long long* host = nullptr;
+  static long long* devp = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    if (std::getenv("FKV_HANG_DIAG") &&
+        cudaHostAlloc((void**)&host, 8 * sizeof(long long), cudaHostAllocMapped) == cudaSuccess) {
+      for (int i = 0; i < 8; ++i) host[i] = 0;
+      if (cudaHostGetDevicePointer((void**)&devp, host, 0) != cudaSuccess) devp = nullptr;
+    }
+  }
+  return devp;
+}
+
+// the report (host side of hang_slot): "" if no deadlock was recorded
+std::string hang_report() {
+  hang_slot();
+  static long long* h = nullptr;
+  if (!h) {
+    long long* d = hang_slot();
+    if (!d) return "";
+    cudaHostGetDevicePointer((void**)&h, d, 0);  // unused: the mapped host pointer equals the device one on UVA
+    h = d;
+  }
+  if (h[0] == 0) return "";
+  char buf[256];
+  std::snprintf(buf, sizeof(buf), "rows kernel deadlock: block %lld thread %lld barrier@smem+%lld parity %lld (ra_rows.cu:%lld)",
+                h[1], h[2], h[3], h[4], h[5]);
+  return buf;
+}
 
 cudaError_t launch_attention_rows(const RowsParams& p, const RowsMaps& maps, cudaStream_t s) {
   // the max-dynamic-shared-memory opt-in is per device

@@ -1577,12 +1577,14 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 
 template <bool kDef, int kRowsT>
 cudaError_t launch_tc_variant(const AttnParams& p, const void* maps, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};  // the max-dynamic-shared-memory opt-in is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
     const cudaError_t e = cudaFuncSetAttribute(ra_tc_kernel<kDef, kRowsT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                Cfg<kDef, kRowsT>::SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   // programmatic dependent launch: the CTAs start (TMEM, barriers, K / V / residual streaming) while the stager
   // finishes; the producer's griddepcontrol.wait orders the staged-image reads after it

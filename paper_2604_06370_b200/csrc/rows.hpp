@@ -76,7 +76,9 @@ struct RowsParams {
   float scale_log2;            // sm_scale * log2(e)
   long long* dbg;              // diagnostics timeline (nullptr = off)
   int32_t dbg_block;
-  int32_t flags;               // diagnostics switches (FKV_ROWS_FLAGS): bit 0 = R_v by bulk copies
+  int32_t flags;               // diagnostics switches (FKV_ROWS_FLAGS): bit 0 = residual pages by cp.async instead of bulk copies
+  long long* hang;             // host-mapped deadlock report (FKV_HANG_DIAG; nullptr = off)
+  int32_t prefetch;            // L2 prefetch distance of the loaders in tiles (0 = off; FKV_ROWS_PREFETCH)
 };
 
 // TMA maps of the rows kernel over the base K / V pools: whole 128-key tiles {64 d, 128 keys, 2 d-halves} (3D,

@@ -216,6 +216,10 @@ __device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int c
                "r"(c1), "r"(c2)
                : "memory");
 }
+// L2 prefetch of a contiguous global range (bytes: multiple of 16; no smem destination, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 // non-blocking probe of an mbarrier phase
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   uint32_t ok;
@@ -236,9 +240,10 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
-// named barrier among a subset of warps
+// named barrier among a subset of warps. Non-.aligned form: the warps of a warp-specialized CTA reach it from
+// different code sites (bar.sync = barrier.sync.aligned requires every thread to execute the same instruction)
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+  asm volatile("barrier.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace sm100

@@ -139,18 +139,20 @@ def _random_scenario(rnd, P, max_prefix=300):
     return recipes.Scenario("rand", ag, q_len=q)
 
 
-@pytest.mark.parametrize("seed", range(1, 25))
+@pytest.mark.parametrize("seed", range(1, 121))
 def test_random_suite(seed):
     """Random fork trees (unaligned forks -> CoW tail pages, same-agent
     branches sharing residual pages, chunked-prefill query rows), both RoPE
-    modes, bf16 tensor-core path and fp32 SIMT path, page sizes 16/64."""
+    modes, bf16 tensor-core path and fp32 SIMT path, page sizes 16/64/128,
+    head shapes 8/2, 32/8 (8B) and 64/8 (70B, g = 8)."""
     rnd = random.Random(seed)
     P = rnd.choice([16, 64, 128])
     mode = rnd.choice(["deferred", "none"])
     dtype = "f32" if seed % 4 == 0 else "bf16"
     d = 64 if (dtype == "f32" and seed % 8 == 0) else 128
+    hq, hkv = (8, 2) if dtype == "f32" else rnd.choice([(8, 2), (32, 8), (64, 8)])
     scen = _random_scenario(rnd, P)
-    fkv = _ctx(scen, 2, 8, 2, d, 16, P, dtype, mode)
+    fkv = _ctx(scen, 2, hq, hkv, d, 16, P, dtype, mode)
     driver.build(fkv, scen, seed=seed)
     for layer in (0, 1):
         err, pl = _run_and_check(fkv, scen, seed, layer, dtype, mode, flags=L.PLAN_CHECK_WRITTEN)

@@ -98,3 +98,52 @@ def test_two_rank_shards_partition_the_work(mode):
     if mode == "agents":
         prefix_base = 512 * 8 * 128 * 2 * 2
         assert sum(i[5] for i in infos) > prefix_base * 2 - 1  # base replicated on both ranks
+
+
+def _bench_worker(rank, world, port, q):
+    """bench.py's N>1 host logic over gloo: the Workload each rank builds, the max-over-ranks step time and the
+    whole-job token count (weak: every rank's own batch; strong c4: each sequence once)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        out = {}
+        for cfg in ("c2", "c4"):
+            wl = bench.Workload(cfg, world, rank)
+            ms_rank = 2.0 + rank                       # a slower rank 1
+            ms = bench._max_over_ranks(ms_rank, world)
+            n_rows = len(wl.batch) * wl.C
+            v = bench.tokens_value(n_rows, ms, world, wl.scaling, wl.kv[0] == 0,
+                                   lambda x: bench._sum_over_ranks(x, world))
+            out[cfg] = (wl.scaling, wl.kv, len(wl.batch), ms, v)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_rank_logic_two_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    for cfg in ("c2", "c4"):
+        a, b = res[0][cfg], res[1][cfg]
+        assert a[3] == b[3] == 3.0                     # max over ranks
+        assert a[4] == b[4]                            # every rank derives the same whole-job value
+    # c2 weak scaling: each rank its own 64-sequence batch -> 2 x 64 tokens per step
+    sc, kv, nb, ms, v = res[0]["c2"]
+    assert sc == "weak" and nb == 64 and abs(v - 2 * 64 / (ms / 1e3)) < 1e-6
+    # c4 strong scaling (partitioner H=2? D=?): the shards of ONE 128-agent batch count each sequence once
+    sc, kv0, nb0, ms, v = res[0]["c4"]
+    kv1, nb1 = res[1]["c4"][1], res[1]["c4"][2]
+    assert sc == "strong"
+    counted = (nb0 if kv0[0] == 0 else 0) + (nb1 if kv1[0] == 0 else 0)
+    assert abs(v - counted / (ms / 1e3)) < 1e-6
+    assert counted == 128                              # every agent's decode token exactly once
