@@ -181,6 +181,36 @@ fkv_status fkv_fork_tokens(fkv_ctx* ctx, int64_t child, int32_t adapter_id, cons
  * changed). Outputs are token counts, multiples of page_size. */
 fkv_status fkv_fork_resume(fkv_ctx* ctx, int64_t child, int32_t adapter_id, int64_t owner, const int32_t* tokens,
                            int64_t n, int64_t* base_hit, int64_t* res_hit, int64_t* mapped);
+/* ---- projection producer (§8(f) rows f2, f3) -------------------------------
+ * The step in front of the hot path: it fills the disaggregated pools from a
+ * layer's input activations (Eq.2: bCache = xW, rCache = xA_i;
+ * P:269 §5.1: base K is cached post-RoPE, the residual without RoPE;
+ * P:370 §6 the "LoRA replacement module"; a forked child
+ * recomputes its own residual over the inherited prefix, a partial hit only
+ * the base rows).
+ *
+ * fkv_register_adapter_down: the adapter's down projections A_K, A_V
+ *   [L][hidden][rank] (dtype, row-major, device, borrowed; LoRA alpha/r folded
+ *   into B, C-7). The adapter's B must be registered first (E_INVALID).
+ * fkv_project_kv: for rows [start[i], start[i]+count[i]) of agents[i] (rows
+ *   reserved by fkv_append / a fork), with x [sum count][hidden] (dtype,
+ *   device, rows concatenated in the same order) computes
+ *     K_base = RoPE_t(x W_k), V_base = x W_v     (W [hidden][Hkv_local][d]:
+ *                                                  this ctx's kv-head columns)
+ *     R_k = x A_k, R_v = x A_v                    (the agent's adapter, `layer`)
+ *   (fp32 accumulate; t = the row's absolute position, rotated with the ctx's
+ *   RoPE table, NeoX pairs, C-2) and writes the planes of which_mask
+ *   (FKV_WRITE_KBASE|FKV_WRITE_VBASE and/or FKV_WRITE_RK|FKV_WRITE_RV, each
+ *   pair together) exactly as fkv_write_kv (same permission rules and errors).
+ *   The base GEMM runs on cuBLAS (loaded at run time; E_CUDA if unavailable),
+ *   the rank-r products and the rotation in the library's kernels. workspace:
+ *   device, 256-byte aligned, >= fkv_project_workspace_bytes(n_rows). */
+fkv_status fkv_register_adapter_down(fkv_ctx* ctx, int32_t adapter_id, const void* A_K, const void* A_V,
+                                     int32_t hidden);
+fkv_status fkv_project_workspace_bytes(fkv_ctx* ctx, int64_t n_rows, size_t* bytes);
+fkv_status fkv_project_kv(fkv_ctx* ctx, int32_t layer, int32_t n, const int64_t* agents, const int64_t* start,
+                          const int32_t* count, const void* x, int32_t hidden, const void* W_k, const void* W_v,
+                          uint32_t which_mask, void* workspace, size_t ws_bytes, void* stream);
 /* Decoupled eviction (§5.2: "independent Least Recently Used (LRU)
  * states to each radix tree"). Frees n_pages pages of ONE tree
  * (kind FKV_KIND_BASE = the base tree, FKV_KIND_RES = the residual forest) by

@@ -185,6 +185,29 @@ class ForkKV:
         self._c(self.lib.fkv_fork_tokens(self.ctx, child, adapter_id, p, len(tokens), ctypes.byref(m)))
         return m.value
 
+    def register_adapter_down(self, adapter_id: int, A_K, A_V):
+        """Down projections A_K, A_V [L][hidden][r] of a registered adapter (projection producer, §8(f) f2)."""
+        self.adapters[("A", adapter_id)] = (A_K, A_V)
+        self._c(self.lib.fkv_register_adapter_down(self.ctx, adapter_id, _ptr(A_K), _ptr(A_V), A_K.shape[-2]))
+
+    def project_kv(self, layer: int, agents, start, count, x, W_k=None, W_v=None, mask: int = L.WRITE_ALL,
+                   stream=None, ws=None):
+        """fkv_project_kv: fill rows [start, start+count) of each agent from the layer input x [sum count][hidden]
+        (K_base = RoPE(x W_k), V_base = x W_v, R = x A of the agent's adapter)."""
+        import torch
+        T = int(np.sum(count)) if len(count) else 0
+        need = ctypes.c_size_t()
+        self._c(self.lib.fkv_project_workspace_bytes(self.ctx, T, ctypes.byref(need)))
+        if ws is None or ws.numel() * ws.element_size() < need.value:
+            ws = torch.empty(max(256, need.value), dtype=torch.uint8, device=x.device)
+        aa, pa = _arr(agents, ctypes.c_int64)
+        ss, ps = _arr(start, ctypes.c_int64)
+        cc, pc = _arr(count, ctypes.c_int32)
+        self._c(self.lib.fkv_project_kv(self.ctx, layer, len(agents), pa, ps, pc, _ptr(x), x.shape[-1], _ptr(W_k),
+                                        _ptr(W_v), mask, _ptr(ws), ws.numel() * ws.element_size(),
+                                        _stream_handle(stream)))
+        return ws
+
     def fork_resume(self, child: int, adapter_id: int, owner: int, tokens: Sequence[int]):
         """Partial-hit fork: returns (base_hit, res_hit, mapped) in tokens."""
         a, p = _arr(tokens if len(tokens) else [0], ctypes.c_int32)

@@ -102,6 +102,36 @@ fkv_status fkv_fork_tokens(fkv_ctx* ctx, int64_t child, int32_t adapter_id, cons
   });
 }
 
+fkv_status fkv_register_adapter_down(fkv_ctx* ctx, int32_t adapter_id, const void* A_K, const void* A_V,
+                                     int32_t hidden) {
+  if (!ctx) return FKV_E_INVALID;
+  return guard(ctx, [&] {
+    auto it = ctx->c.adapter_slot.find(adapter_id);
+    if (it == ctx->c.adapter_slot.end())
+      throw Error(FKV_E_INVALID, "register_adapter_down: register the adapter's B first (fkv_register_adapter)");
+    if (hidden < 1 || (ctx->c.device && (!A_K || !A_V)))
+      throw Error(FKV_E_INVALID, "register_adapter_down: null A_K/A_V or hidden < 1");
+    auto& a = ctx->c.adapters[it->second];
+    a.ak = A_K; a.av = A_V; a.hidden = hidden;
+  });
+}
+
+fkv_status fkv_project_workspace_bytes(fkv_ctx* ctx, int64_t n_rows, size_t* bytes) {
+  if (!ctx || !bytes || n_rows < 0) return FKV_E_INVALID;
+  *bytes = fkv::project_workspace_bytes(ctx->c, n_rows);
+  return FKV_OK;
+}
+
+fkv_status fkv_project_kv(fkv_ctx* ctx, int32_t layer, int32_t n, const int64_t* agents, const int64_t* start,
+                          const int32_t* count, const void* x, int32_t hidden, const void* W_k, const void* W_v,
+                          uint32_t which_mask, void* workspace, size_t ws_bytes, void* stream) {
+  if (!ctx) return FKV_E_INVALID;
+  return guard(ctx, [&] {
+    fkv::project_kv(ctx->c, layer, n, agents, start, count, x, hidden, W_k, W_v, which_mask, workspace, ws_bytes,
+                    stream);
+  });
+}
+
 fkv_status fkv_fork_resume(fkv_ctx* ctx, int64_t child, int32_t adapter_id, int64_t owner, const int32_t* tokens,
                            int64_t n, int64_t* base_hit, int64_t* res_hit, int64_t* mapped) {
   if (!ctx || !base_hit || !res_hit || !mapped) return FKV_E_INVALID;

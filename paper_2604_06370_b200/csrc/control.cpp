@@ -456,6 +456,89 @@ void write_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int
   }
 }
 
+// ---- projection producer (§8(f) f2 / f3; Eq.2) -----------------------------------------
+namespace {
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+}  // namespace
+
+size_t project_workspace_bytes(const Ctx& c, int64_t T) {
+  const int64_t n = (int64_t)c.hkv_local * c.cfg.head_dim, r = c.cfg.rank;
+  return al256(T * 4) + al256(T * 16) + 2 * al256(T * n * 4) + al256(T * 2 * r * 4) + 2 * al256(T * n * c.elem) +
+         2 * al256(T * r * c.elem);
+}
+
+void project_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int64_t* start, const int32_t* count,
+                const void* x, int32_t hidden, const void* W_k, const void* W_v, uint32_t mask, void* ws,
+                size_t ws_bytes, void* stream) {
+  if (!c.device) throw Error(FKV_E_INVALID, "project_kv: host-only ctx");
+  if (layer < 0 || layer >= c.cfg.n_layers || hidden < 1 || (mask & ~15u) || mask == 0 || !x || n < 0 ||
+      (n > 0 && (!agents || !start || !count)))
+    throw Error(FKV_E_INVALID, "project_kv: bad layer/hidden/mask/arrays");
+  const bool base = mask & 3u, res = mask & 12u;
+  if ((mask & 3u) && (mask & 3u) != 3u) throw Error(FKV_E_INVALID, "project_kv: base planes are written together");
+  if ((mask & 12u) && (mask & 12u) != 12u) throw Error(FKV_E_INVALID, "project_kv: residual planes are written together");
+  if (base && (!W_k || !W_v)) throw Error(FKV_E_INVALID, "project_kv: W_k / W_v required for the base planes");
+  if (base && (!c.buf.rope_cos || !c.buf.rope_sin))
+    throw Error(FKV_E_INVALID, "project_kv: the RoPE table is required (K_base is cached post-RoPE, P:269)");
+  const int r = c.cfg.rank;
+  if (res && r != 8 && r != 16 && r != 32 && r != 64) throw Error(FKV_E_INVALID, "project_kv: rank must be 8/16/32/64");
+  int64_t T = 0;
+  std::vector<int32_t> pos;
+  std::vector<int64_t> aptr;
+  for (int32_t i = 0; i < n; ++i) {
+    const Agent& ag = c.agent(agents[i]);
+    if (start[i] < 0 || count[i] < 0 || start[i] + count[i] > ag.seqlen)
+      throw Error(FKV_E_INVALID, "project_kv: rows not reserved");
+    if (base && start[i] + count[i] > c.cfg.max_pos) throw Error(FKV_E_INVALID, "project_kv: position beyond RoPE table");
+    const AdapterSlot* as = nullptr;
+    if (res) {
+      auto it = c.adapter_slot.find(ag.adapter);
+      if (it == c.adapter_slot.end() || !c.adapters[it->second].ak)
+        throw Error(FKV_E_INVALID, "project_kv: agent's adapter has no registered down projection (A_k, A_v)");
+      as = &c.adapters[it->second];
+      if (as->hidden != hidden) throw Error(FKV_E_INVALID, "project_kv: hidden size differs from the adapter's A");
+    }
+    for (int32_t j = 0; j < count[i]; ++j) {
+      pos.push_back((int32_t)(start[i] + j));
+      const int64_t off = (int64_t)layer * hidden * r * (int64_t)c.elem;
+      aptr.push_back(as ? (int64_t)(intptr_t)as->ak + off : 0);
+      aptr.push_back(as ? (int64_t)(intptr_t)as->av + off : 0);
+    }
+    T += count[i];
+  }
+  if (T == 0) return;
+  if (!ws || ws_bytes < project_workspace_bytes(c, T) || ((uintptr_t)ws & 255))
+    throw Error(FKV_E_INVALID, "project_kv: workspace too small or not 256-byte aligned");
+  DeviceGuard dg(c);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nn = (int64_t)c.hkv_local * c.cfg.head_dim;
+  uint8_t* w = (uint8_t*)ws;
+  int32_t* dpos = (int32_t*)w;                      w += al256(T * 4);
+  int64_t* daptr = (int64_t*)w;                     w += al256(T * 16);
+  float* yk = (float*)w;                            w += al256(T * nn * 4);
+  float* yv = (float*)w;                            w += al256(T * nn * 4);
+  float* yr = (float*)w;                            w += al256(T * 2 * r * 4);
+  void* skb = w;                                    w += al256(T * nn * c.elem);
+  void* svb = w;                                    w += al256(T * nn * c.elem);
+  void* srk = w;                                    w += al256(T * r * c.elem);
+  void* srv = w;
+  check_cuda(cudaMemcpyAsync(dpos, pos.data(), T * 4, cudaMemcpyHostToDevice, s), "project_kv: upload");
+  check_cuda(cudaMemcpyAsync(daptr, aptr.data(), T * 16, cudaMemcpyHostToDevice, s), "project_kv: upload");
+  std::string err;
+  if (base) {
+    cudaError_t e = k::gemm_rowmajor_f32out(T, nn, hidden, x, W_k, yk, c.cfg.dtype, s, &err);
+    if (e == cudaSuccess) e = k::gemm_rowmajor_f32out(T, nn, hidden, x, W_v, yv, c.cfg.dtype, s, &err);
+    if (e != cudaSuccess) throw Error(FKV_E_CUDA, "project_kv: base GEMM: " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
+  }
+  if (res) check_cuda(k::launch_adapter_proj(x, daptr, (int32_t)T, hidden, r, c.cfg.dtype, yr, s), "project_kv: adapters");
+  check_cuda(k::launch_project_stage(base ? yk : nullptr, yv, res ? yr : nullptr, dpos, (const float*)c.buf.rope_cos,
+                                     (const float*)c.buf.rope_sin, (int32_t)T, c.hkv_local, c.cfg.head_dim, r, 1,
+                                     c.cfg.dtype, skb, svb, srk, srv, s),
+             "project_kv: stage");
+  // the staged rows go through the ordinary row write (permission checks, written bits, page scatter)
+  write_kv(c, layer, n, agents, start, count, skb, svb, srk, srv, mask, stream);
+}
+
 void release(Ctx& c, int64_t a) {
   Agent& ag = c.agent(a);
   for (int32_t pg : ag.base) c.pools[0].release(pg);

@@ -101,6 +101,9 @@ struct AdapterSlot {
   int32_t id;
   const void* bk;
   const void* bv;
+  const void* ak = nullptr;  // down projections A_k, A_v [L][hidden][r] (projection producer; optional)
+  const void* av = nullptr;
+  int32_t hidden = 0;
 };
 
 struct Ctx {
@@ -239,6 +242,10 @@ void write_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int
               const void* kb, const void* vb, const void* rk, const void* rv, uint32_t mask, void* stream);
 void release(Ctx& c, int64_t a);
 std::string dump(const Ctx& c);
+size_t project_workspace_bytes(const Ctx& c, int64_t n_rows);
+void project_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int64_t* start, const int32_t* count,
+                const void* x, int32_t hidden, const void* W_k, const void* W_v, uint32_t mask, void* ws,
+                size_t ws_bytes, void* stream);
 
 // plan_rows.cpp: items / WUs / tiles / rows, partial entries, combine CSR and schedule of kernel 3
 void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const std::vector<const Agent*>& ags,

@@ -143,6 +143,15 @@ cudaError_t launch_combine(const AttnParams& p, cudaStream_t s);
 cudaError_t launch_attention_rows(const RowsParams& p, const RowsMaps& maps, cudaStream_t s);
 // host-mapped deadlock report of the rows kernel (allocated on first use when FKV_HANG_DIAG is set, else nullptr)
 long long* hang_slot();
+// project.cu: the projection producer (§8(f) f2 / f3)
+cudaError_t gemm_rowmajor_f32out(int64_t T, int64_t N, int64_t K, const void* X, const void* W, float* Y, int32_t dtype,
+                                 cudaStream_t s, std::string* err);
+cudaError_t launch_adapter_proj(const void* x, const int64_t* aptr, int32_t n_rows, int32_t hidden, int32_t r,
+                                int32_t dtype, float* out, cudaStream_t s);
+cudaError_t launch_project_stage(const float* yk, const float* yv, const float* yr, const int32_t* pos,
+                                 const float* rope_cos, const float* rope_sin, int32_t n_rows, int32_t hkv, int32_t d,
+                                 int32_t r, int32_t rope, int32_t dtype, void* kb, void* vb, void* rk, void* rv,
+                                 cudaStream_t s);
 std::string hang_report();
 
 cudaError_t launch_synth_fill(void* dst, int32_t dtype, uint64_t seed, int32_t kind, uint64_t owner, int32_t layer,

@@ -259,6 +259,8 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
         t.flags = (k == w.kb ? k::kTileFirst : 0) | (min_pos < k + t.n_keys - 1 ? k::kTileCausal : 0);
         t.wu = wu_idx;
         t.base_off = (int32_t)(w.base_off + k / P);
+        t.base_page = pl.base_pages[t.base_off];
+        t.n_slots = rw.n_slots;
         t.kv_head = w.h;
         for (int s = 0; s < kSlots; ++s)
           t.res_off[s] = s < (int)w.slot_res_off.size() ? (int32_t)(w.slot_res_off[s] + k / P) : 0;

@@ -17,9 +17,8 @@
 // Warp roles (384 threads):
 //   warps 0-3  softmax (thread = row = TMEM lane)
 //   warp  4    MMA issuer (one thread)
-//   warp  5    K_base / V_base loader (TMA tensor boxes)
-//   warp  6    R_k loader (bulk copies of residual pages: the page format is the SW32 K-major operand)
-//   warp  7    R_v loader (bulk copies of 64-key halves of each slot's page)
+//   warp  5    K_base loader (TMA tensor boxes), warp 7 V_base loader
+//   warp  6    R_k and R_v loader (bulk copies of residual pages: the page format is the SW32 operand)
 //   warps 8-11 aux: q~ of the next item, Q image of the next item (cp.async), epilogue (TMEM -> partial entries)
 //
 // Shared memory: Q image 32 KB (SW128 K-major) | q~ images 2 x 4 KB (SW32 K-major) | ring of kNU 16-KB units
@@ -55,6 +54,7 @@ struct Bars {
   uint32_t tmem_base;
   uint32_t pad_;
   float2 ml[2][kRowsLanes];
+  int prog[16];  // diagnostics: per-role progress counters (reported by the deadlock watchdog)
 };
 constexpr uint32_t kSmemBytes = OFF_BAR + sizeof(Bars);
 static_assert(kSmemBytes <= 232448, "shared memory");
@@ -89,6 +89,19 @@ __device__ __forceinline__ void mma_ts_m(uint32_t d, uint32_t a, uint64_t b, uin
 // 1 ms hint whose wake-up latency cost several microseconds per wait on B200)
 // With FKV_HANG_DIAG set, a wait that spins for ~2^27 polls records (block, warp, lane, barrier offset, parity,
 // site) into host-mapped memory (fkv_debug_hang_report) and traps, turning a pipeline deadlock into a located error.
+__device__ __noinline__ void hang_trap(uint32_t bar, uint32_t parity, long long* hang, int site) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  hang[0] = 1;
+  hang[1] = blockIdx.x;
+  hang[2] = threadIdx.x;
+  hang[3] = (long long)(bar - smem_u32(smem));
+  hang[4] = parity;
+  hang[5] = site;
+  const volatile int* pr = reinterpret_cast<const volatile int*>(smem + OFF_BAR + offsetof(Bars, prog));
+  for (int i = 0; i < 16; ++i) hang[8 + i] = pr[i];
+  __threadfence_system();
+  __trap();
+}
 __device__ __forceinline__ void wait_bar_(uint32_t bar, uint32_t parity, long long* hang, int site) {
   uint32_t ok;
   uint32_t n = 0;
@@ -98,17 +111,7 @@ __device__ __forceinline__ void wait_bar_(uint32_t bar, uint32_t parity, long lo
         : "=r"(ok)
         : "r"(bar), "r"(parity)
         : "memory");
-    if (!ok && ++n == (1u << 27) && hang != nullptr) {
-      extern __shared__ __align__(1024) uint8_t smem[];
-      hang[0] = 1;
-      hang[1] = blockIdx.x;
-      hang[2] = threadIdx.x;
-      hang[3] = (long long)(bar - smem_u32(smem));
-      hang[4] = parity;
-      hang[5] = site;
-      __threadfence_system();
-      __trap();
-    }
+    if (__builtin_expect(!ok && ++n == (1u << 27), 0) && hang != nullptr) hang_trap(bar, parity, hang, site);
   } while (!ok);
 }
 #define wait_bar(bar, parity) wait_bar_((bar), (parity), p.hang, __LINE__)
@@ -131,19 +134,41 @@ __device__ __forceinline__ void stamp_(const RowsParams& p, int ev, int i) {
 #define stamp stamp_<kDbg>
 
 
-// Walk the CTA's items in MMA consumption order: S(0), S(1) PV(0), S(2) PV(1), ..., PV(n-1) per item.
-// f(kind, item_idx, item_ord, t, tile_index, last_in_item): kind 0 = K side of tile t, 1 = V side of tile t.
+// Walk the CTA's tiles in MMA consumption order, software-pipelined across item boundaries:
+//   S(0), S(1) PV(0), S(2) PV(1), ..., S(N-1) PV(N-2), PV(N-1)      over the CTA's N tiles (all items, in order)
+// f(kind, item_ord, t, tile_index, n_tiles_of_item, next): kind 0 = K side of tile t of item item_ord, 1 = V side;
+// `next` = the tile index of the same kind's next step (-1 at the end).
+// The units of one kind are then at most 4 apart in the ring sequence (K, R_k, V, R_v per step): with kNU = 5 slots
+// a producer can never find a slot's `empty` barrier two phases behind (parity aliasing), which the per-item
+// order (K units 6 apart across an item boundary) allowed once K and V had producers of their own.
 template <class F>
 __device__ __forceinline__ void walk(const RowsParams& p, F&& f) {
   const int i0 = p.sched_ptr[blockIdx.x], i1 = p.sched_ptr[blockIdx.x + 1];
-  for (int ii = i0; ii < i1; ++ii) {
-    const RItem it = p.items[p.sched_items[ii]];
-    for (int t = 0; t < it.n_tiles; ++t) {
-      f(0, ii - i0, t, it.tile0 + t, it.n_tiles);
-      if (t > 0) f(1, ii - i0, t - 1, it.tile0 + t - 1, it.n_tiles);
-    }
-    f(1, ii - i0, it.n_tiles - 1, it.tile0 + it.n_tiles - 1, it.n_tiles);
+  int pv_io = -1, pv_t = 0, pv_n = 0, pv_t0 = 0;  // the tile whose V side is pending
+  int t0 = 0, n = 0;
+  if (i0 < i1) {
+    const int id = p.sched_items[i0];
+    t0 = __ldg(&p.items[id].tile0);
+    n = __ldg(&p.items[id].n_tiles);
   }
+  for (int ii = i0; ii < i1; ++ii) {
+    int nt0 = -1, nn = 0;
+    if (ii + 1 < i1) {
+      const int id = p.sched_items[ii + 1];
+      nt0 = __ldg(&p.items[id].tile0);
+      nn = __ldg(&p.items[id].n_tiles);
+    }
+    for (int t = 0; t < n; ++t) {
+      // next flat tile of the CTA (both kinds step through the same sequence)
+      const int tn = t + 1 < n ? t0 + t + 1 : nt0;
+      f(0, ii - i0, t, t0 + t, n, tn);
+      if (pv_io >= 0) f(1, pv_io, pv_t, pv_t0 + pv_t, pv_n, t0 + t);
+      pv_io = ii - i0; pv_t = t; pv_n = n; pv_t0 = t0;
+    }
+    t0 = nt0;
+    n = nn;
+  }
+  if (pv_io >= 0) f(1, pv_io, pv_t, pv_t0 + pv_t, pv_n, -1);
 }
 
 // Cursor over the CTA's tiles in processing order, `ahead` tiles in front of the loaders: the L2 prefetch of
@@ -216,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tm = B.tmem_base;
   const int n_my = p.sched_ptr[blockIdx.x + 1] - p.sched_ptr[blockIdx.x];
-  // register budget per warpgroup (setmaxnreg at the top of each role): softmax 224, loaders / MMA 64, aux 216
+  // register budget per warpgroup (setmaxnreg at the top of each role): softmax 224, loaders / MMA 96, aux 184
   // (x 128 threads = 64512 registers = the CTA allocation of 168 x 384: more would deadlock setmaxnreg.inc).
   // Dependent grids (the combine kernel, or the next instance of this kernel) are released only after every
   // warpgroup has moved its registers (named barrier 1 below): registers freed by setmaxnreg.dec must not be
@@ -244,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int b = g & 1;
         RTile Tn;
         if (t + 1 < it.n_tiles) Tn = p.tiles[it.tile0 + t + 1];
+        if (lane == 0) B.prog[wid] = g;
         wait_bar(smem_u32(&B.s_full[b]), (g >> 1) & 1);
         if (tid == 0) stamp(p, 4, g);
         tc_fence_after();
@@ -331,21 +357,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(smem_u32(&B.ml_full[io & 1]));
     }
   } else if (wid < 8) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
     release_dependents();
     if (wid == 4) {
       // ==================================== MMA issuer (one thread) ====================================
+      // Tile fields come from the tile record (n_keys, flags, n_slots, WU) read at the top of each step, before
+      // the barrier waits, so their latency overlaps the waits; the S step keeps the WU's output-lane mask for
+      // its PV step.
       if (lane == 0) {
         uint32_t u = 0;
         int g = 0;   // S tiles issued
         int gp = 0;  // PV tiles issued
         const uint32_t qa = sb + OFF_Q;
-        walk(p, [&](int kind, int io, int t, int ti, int n_tiles) {
+        uint4 pv_l0 = make_uint4(0, 0, 0, 0), pv_l1 = pv_l0;  // WU lanes of the S tiles by parity (registers)
+        walk(p, [&](int kind, int io, int t, int ti, int n_tiles, int) {
           const RTile* Tp = p.tiles + ti;
-          const int n_keys = __ldg(&Tp->n_keys), wu = __ldg(&Tp->wu);
-          const int n_slots = __ldg(&p.wus[wu].n_slots);
+          const int n_keys = __ldg(&Tp->n_keys), wu = __ldg(&Tp->wu), n_slots = __ldg(&Tp->n_slots);
           if (kind == 0) {
             // ------------------------- S = Q K^T + q~ R_k^T (K tile unit, R_k unit) -------------------------
+            uint4 ml[kRowsMaxSlots];
+#pragma unroll
+            for (int sl = 0; sl < kRowsMaxSlots; ++sl)
+              ml[sl] = sl < n_slots ? __ldg(reinterpret_cast<const uint4*>(p.wus[wu].slot_lanes[sl]))
+                                    : make_uint4(0, 0, 0, 0);
+            {
+              const uint4 l = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].lanes));
+              if (g & 1) pv_l1 = l;
+              else pv_l0 = l;
+            }
             if (t == 0) {
               wait_bar(smem_u32(&B.q_full), io & 1);
               stamp(p, 8, io);
@@ -356,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t dS = tm + 128u * (g & 1);
             const uint4 none = make_uint4(0, 0, 0, 0);
             uint32_t s_ = u % kNU;
+            B.prog[4] = (int)u;
             wait_bar(smem_u32(&B.full[s_]), (u / kNU) & 1);
             stamp(p, 0, g);
             tc_fence_after();
@@ -375,13 +415,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             s_ = u % kNU;
             wait_bar(smem_u32(&B.full[s_]), (u / kNU) & 1);
             tc_fence_after();
-            fence_async_smem();  // R_k pages land through cp.async (generic proxy)
+            fence_async_smem();  // residual pages may land through cp.async (generic proxy)
             const uint32_t rb = sb + OFF_RING + s_ * kUnit;
-            for (int s = 0; s < n_slots; ++s) {
-              const uint4 ml = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].slot_lanes[s]));
-              mma_ss_m(dS, make_desc(qt, 16, 256, SWZ_32), make_desc(rb + 4096u * s, 16, 256, SWZ_32), idS, 1u,
-                       make_uint4(~ml.x, ~ml.y, ~ml.z, ~ml.w));
-            }
+#pragma unroll
+            for (int sl = 0; sl < kRowsMaxSlots; ++sl)
+              if (sl < n_slots)
+                mma_ss_m(dS, make_desc(qt, 16, 256, SWZ_32), make_desc(rb + 4096u * sl, 16, 256, SWZ_32), idS, 1u,
+                         make_uint4(~ml[sl].x, ~ml[sl].y, ~ml[sl].z, ~ml[sl].w));
             mma_commit(smem_u32(&B.empty[s_]));
             ++u;
             mma_commit(smem_u32(&B.s_full[g & 1]));
@@ -391,23 +431,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             // ------------------------- O += P V ; A_r += P R_v (V tile unit, R_v unit) -------------------------
             const int b = gp & 1;
+            const uint32_t acc0 = (__ldg(&Tp->flags) & kTileFirst) ? 0u : 1u;
+            const uint4 lw = b ? pv_l1 : pv_l0;
             wait_bar(smem_u32(&B.p_full[b]), (gp >> 1) & 1);
             stamp(p, 2, gp);
             if (t == 0 && io > 0) wait_bar(smem_u32(&B.o_free), (io - 1) & 1);
-            const uint4 lw = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].lanes));
             const uint4 dis = make_uint4(~lw.x, ~lw.y, ~lw.z, ~lw.w);
             const uint32_t idV = idesc_bf16(128, 128, false, true);
             const uint32_t idR = idesc_bf16(128, 16 * n_slots, false, true);
             const int nk = (n_keys + 15) >> 4;
             const uint32_t pa = tm + 128u * b;
-            const uint32_t acc0 = (__ldg(&Tp->flags) & kTileFirst) ? 0u : 1u;
             const uint32_t sv = u % kNU, sr_ = (u + 1) % kNU;
+            B.prog[4] = (int)u + 1000000;
             wait_bar(smem_u32(&B.full[sv]), (u / kNU) & 1);
             stamp(p, 13, gp);
             wait_bar(smem_u32(&B.full[sr_]), ((u + 1) / kNU) & 1);
             stamp(p, 14, gp);
             tc_fence_after();
-            fence_async_smem();  // R_v pages land through cp.async (generic proxy)
+            fence_async_smem();  // residual pages may land through cp.async (generic proxy)
             const uint32_t vb = sb + OFF_RING + sv * kUnit, rvb = sb + OFF_RING + sr_ * kUnit;
             for (int k = 0; k < nk; ++k) {
               const uint32_t acc = k ? 1u : acc0;
@@ -425,101 +466,122 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         });
       }
-    } else if (wid == 5) {
-      // ================= K_base / V_base tiles: one TMA box {64 d, 128 keys, 2 d-halves} per tile (P = 128) =================
+    } else if (wid == 5 || wid == 7) {
+      // ======= K_base (warp 5) / V_base (warp 7) tiles: one TMA box {64 d, 128 keys, 2 d-halves} per tile (P = 128) =======
+      // (one issuing thread streams ~45 B/clk at most, tools/ub_fill.cu: K and V get a thread each). The next tile's
+      // record is read one step ahead (its latency overlaps this step's wait for a free ring slot).
       if (lane == 0) {
+        const int my_kind = wid == 5 ? 0 : 1;
         uint32_t u = 0;
         int kt = 0;
         const int P = p.P;
         const int ppt = 128 / P;  // pages per tile
-        TileCursor pf;
-        pf.init(p, p.prefetch);
-        walk(p, [&](int kind, int, int, int ti, int) {
-          if (kind == 0 && p.prefetch > 0) {
-            // base K and V pages of the tile `prefetch` tiles ahead into L2 (one contiguous P x d run per page)
-            const int tn = pf.next(p);
-            if (tn >= 0) {
-              const RTile* Tq = p.tiles + tn;
-              const int nk = __ldg(&Tq->n_keys), bo = __ldg(&Tq->base_off), hq = __ldg(&Tq->kv_head);
-              for (int pi = 0; pi < ppt && pi * P < nk; ++pi) {
-                const int pg = p.base_pages[bo + pi];
-                if (pg < 0) continue;
-                const size_t off = ((size_t)p.base_rows_layer + (size_t)pg * p.hkv * P + (size_t)hq * P) * 256;
-                bulk_prefetch_l2((const uint8_t*)p.base_k + off, (uint32_t)P * 256);
-                bulk_prefetch_l2((const uint8_t*)p.base_v + off, (uint32_t)P * 256);
-              }
-            }
+        const CUtensorMap* m3 = my_kind == 0 ? &maps.k3d : &maps.v3d;
+        const CUtensorMap* m2 = my_kind == 0 ? &maps.k2d : &maps.v2d;
+        int c_pg = -1, c_h = 0, c_nk = 0, c_bo = 0;
+        bool have = false;
+        walk(p, [&](int kind, int, int, int ti, int, int tn) {
+          if (kind != my_kind) {
+            u += 2;
+            return;
           }
-          const RTile* Tp = p.tiles + ti;
-          const int n_keys = __ldg(&Tp->n_keys), base_off = __ldg(&Tp->base_off);
-          const int64_t hrow = (int64_t)__ldg(&Tp->kv_head) * P;
-          const CUtensorMap* m3 = kind == 0 ? &maps.k3d : &maps.v3d;
-          const CUtensorMap* m2 = kind == 0 ? &maps.k2d : &maps.v2d;
+          if (!have) {
+            const RTile* T0 = p.tiles + ti;
+            c_pg = __ldg(&T0->base_page); c_h = __ldg(&T0->kv_head); c_nk = __ldg(&T0->n_keys);
+            c_bo = __ldg(&T0->base_off);
+          }
+          int n_pg = -1, n_h = 0, n_nk = 0, n_bo = 0;
+          if (tn >= 0) {
+            const RTile* Tn = p.tiles + tn;
+            n_pg = __ldg(&Tn->base_page); n_h = __ldg(&Tn->kv_head); n_nk = __ldg(&Tn->n_keys);
+            n_bo = __ldg(&Tn->base_off);
+          }
+          const int64_t hrow = (int64_t)c_h * P;
           const uint32_t s_ = u % kNU;
+          B.prog[wid] = (int)u;
           wait_bar(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
-          if (kind == 0) stamp(p, 6, kt++);
+          if (my_kind == 0) stamp(p, 6, kt++);
           const uint32_t dst = sb + OFF_RING + s_ * kUnit;
           if (P == 128) {
-            const int pg = p.base_pages[base_off];
-            mbar_expect_tx(smem_u32(&B.full[s_]), pg >= 0 ? 32768u : 0u);
-            if (pg >= 0)
-              tma_load_3d(dst, m3, 0, (int)(p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow), 0, smem_u32(&B.full[s_]));
+            mbar_expect_tx(smem_u32(&B.full[s_]), c_pg >= 0 ? 32768u : 0u);
+            if (c_pg >= 0)
+              tma_load_3d(dst, m3, 0, (int)(p.base_rows_layer + (int64_t)c_pg * p.hkv * P + hrow), 0,
+                          smem_u32(&B.full[s_]));
           } else {
             int np = 0;
-            for (int pi = 0; pi < ppt && pi * P < n_keys; ++pi) np += p.base_pages[base_off + pi] >= 0;
+            for (int pi = 0; pi < ppt && pi * P < c_nk; ++pi) np += p.base_pages[c_bo + pi] >= 0;
             mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)np * P * 256);
-            for (int pi = 0; pi < ppt && pi * P < n_keys; ++pi) {
-              const int pg = p.base_pages[base_off + pi];
+            for (int pi = 0; pi < ppt && pi * P < c_nk; ++pi) {
+              const int pg = p.base_pages[c_bo + pi];
               if (pg < 0) continue;
               const int r0 = (int)(p.base_rows_layer + (int64_t)pg * p.hkv * P + hrow);
               tma_load_2d(dst + pi * P * 128, m2, 0, r0, smem_u32(&B.full[s_]));
               tma_load_2d(dst + 16384 + pi * P * 128, m2, 64, r0, smem_u32(&B.full[s_]));
             }
           }
+          B.prog[wid + 4] = (int)u;
           u += 2;
+          c_pg = n_pg; c_h = n_h; c_nk = n_nk; c_bo = n_bo;
+          have = true;
         });
       }
     } else {
-      // ====== residual pages (warp 6: R_k, warp 7: R_v): one bulk copy per (slot, page), issued by parallel lanes ======
-      const bool is_rv = wid == 7;
-      uint32_t u = 0;  // R_k is the second unit of a tile's K side, R_v the second of its V side
+      // ====== residual pages (warp 6: R_k and R_v): one bulk copy per (slot, page), lanes in parallel ======
+      // lane s owns slot s (P = 128: one page per slot and tile; records read one step ahead). R_k of tile k+1
+      // and R_v of tile k alternate in the walk; both use the same residual pages (the two planes share the page
+      // table), so the R_k step keeps its page for the tile's R_v step.
+      uint32_t u = 0;
       const int P = p.P;
       const int ppt = 128 / P;  // pages per slot and tile (<= 8)
-      const uint8_t* rp = (const uint8_t*)(is_rv ? p.res_v : p.res_k) + (size_t)p.layer * p.res_layer_elems * 2;
-      TileCursor pf;
-      pf.init(p, p.prefetch);
-      walk(p, [&](int kind, int, int, int ti, int) {
-        if ((kind == 1) != is_rv) {
-          u += 2;
-          return;
+      const uint8_t* rpk = (const uint8_t*)p.res_k + (size_t)p.layer * p.res_layer_elems * 2;
+      const uint8_t* rpv = (const uint8_t*)p.res_v + (size_t)p.layer * p.res_layer_elems * 2;
+      int c_pg = -1, c_nk = 0, c_ns = 0;      // the next R_k step's tile (prefetched)
+      int v0_pg = -1, v0_nk = 0, v0_ns = 0, v1_pg = -1, v1_nk = 0, v1_ns = 0;  // pending R_v tiles (by parity)
+      int kstep = 0, vstep = 0;
+      bool have = false;
+      auto rec = [&](int ti, int& pg, int& nk, int& ns) {
+        const RTile* T0 = p.tiles + ti;
+        nk = __ldg(&T0->n_keys);
+        ns = __ldg(&T0->n_slots);
+        pg = (P == 128 && lane < ns) ? p.res_pages[__ldg(&T0->res_off[lane])] : -1;
+      };
+      walk(p, [&](int kind, int, int, int ti, int, int tn) {
+        const bool is_rv = kind == 1;
+        int pg, nk, ns;
+        if (!is_rv) {
+          if (!have) rec(ti, c_pg, c_nk, c_ns);
+          pg = c_pg; nk = c_nk; ns = c_ns;
+          if (kstep & 1) { v1_pg = pg; v1_nk = nk; v1_ns = ns; }
+          else { v0_pg = pg; v0_nk = nk; v0_ns = ns; }
+          ++kstep;
+          if (tn >= 0) rec(tn, c_pg, c_nk, c_ns);
+          have = true;
+        } else {
+          if (vstep & 1) { pg = v1_pg; nk = v1_nk; ns = v1_ns; }
+          else { pg = v0_pg; nk = v0_nk; ns = v0_ns; }
+          ++vstep;
         }
-        if (p.prefetch > 0) {
-          // this plane's residual pages of the tile `prefetch` tiles ahead into L2 (lane = (slot, page))
-          const int tn = pf.next(p);
-          if (tn >= 0) {
-            const RTile* Tq = p.tiles + tn;
-            const int nk = __ldg(&Tq->n_keys), nsq = __ldg(&p.wus[__ldg(&Tq->wu)].n_slots);
-            for (int q = lane; q < nsq * ppt; q += 32) {
-              const int s = q / ppt, pi = q % ppt;
-              if (pi * P >= nk) continue;
-              const int pg = p.res_pages[__ldg(&Tq->res_off[s]) + pi];
-              if (pg >= 0) bulk_prefetch_l2(rp + (size_t)pg * P * 32, (uint32_t)P * 32);
-            }
-          }
-        }
+        const uint8_t* rp = is_rv ? rpv : rpk;
         const RTile* Tp = p.tiles + ti;
-        const int n_keys = __ldg(&Tp->n_keys);
-        const int ns = __ldg(&p.wus[__ldg(&Tp->wu)].n_slots);
         const uint32_t s_ = (u + 1) % kNU;
+        if (lane == 0) B.prog[6] = (int)u + 1;
         wait_bar(smem_u32(&B.empty[s_]), (((u + 1) / kNU) & 1) ^ 1);
         const uint32_t dst = sb + OFF_RING + s_ * kUnit;
-        const int np = ns * ppt;  // (slot, page) pieces
-        if (!(p.flags & 1)) {
-          // one bulk copy per (slot, page) piece, issued by parallel lanes
-          int mine = 0;  // bytes this lane copies
+        if (P == 128) {
+          const int mine = pg >= 0 ? 4096 : 0;
+          int tot = mine;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+          if (lane == 0) mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)tot);
+          __syncwarp();
+          if (pg >= 0) bulk_g2s(dst + 4096u * lane, rp + (size_t)pg * 4096, 4096, smem_u32(&B.full[s_]));
+        } else {
+          // pages of 16..64 tokens: (slot, page) pieces over the lanes (tile fields re-read: not prefetched)
+          const int np = ns * ppt;
+          int mine = 0;
           for (int q = lane; q < np; q += 32) {
-            const int s = q / ppt, pi = q % ppt;
-            if (pi * P < n_keys && p.res_pages[__ldg(&Tp->res_off[s]) + pi] >= 0) mine += P * 32;
+            const int sl = q / ppt, pi = q % ppt;
+            if (pi * P < nk && p.res_pages[__ldg(&Tp->res_off[sl]) + pi] >= 0) mine += P * 32;
           }
           int tot = mine;
 #pragma unroll
@@ -527,34 +589,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)tot);
           __syncwarp();
           for (int q = lane; q < np; q += 32) {
-            const int s = q / ppt, pi = q % ppt;
-            if (pi * P >= n_keys) continue;
-            const int pg = p.res_pages[__ldg(&Tp->res_off[s]) + pi];
-            if (pg >= 0)
-              bulk_g2s(dst + 4096u * s + pi * P * 32, rp + (size_t)pg * P * 32, P * 32, smem_u32(&B.full[s_]));
+            const int sl = q / ppt, pi = q % ppt;
+            if (pi * P >= nk) continue;
+            const int pgq = p.res_pages[__ldg(&Tp->res_off[sl]) + pi];
+            if (pgq >= 0)
+              bulk_g2s(dst + 4096u * sl + pi * P * 32, rp + (size_t)pgq * P * 32, P * 32, smem_u32(&B.full[s_]));
           }
-        } else {
-          // diagnostics (FKV_ROWS_FLAGS bit 0): 16-byte cp.async by all lanes (LSU path; measured slower: 6.7 K vs
-          // 4.1 K cycles per tile on C2)
-          for (int q = 0; q < np; ++q) {
-            const int s = q / ppt, pi = q % ppt;
-            if (pi * P >= n_keys) continue;
-            const int pg = p.res_pages[__ldg(&Tp->res_off[s]) + pi];
-            if (pg < 0) continue;
-            const uint8_t* src = rp + (size_t)pg * P * 32;
-            const uint32_t d0 = dst + 4096u * s + pi * P * 32;
-            for (int c = lane; c < P * 2; c += 32) cp_async16(d0 + 16u * c, src + 16 * c);
-          }
-          cp_async_arrive_inc(smem_u32(&B.full[s_]));
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&B.full[s_]));
         }
+        if (lane == 0) B.prog[10] = (int)u + 1;
         u += 2;
       });
     }
   } else {
     // ======================= aux warpgroup: q~, Q image, epilogue (thread = row = TMEM lane) =======================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 184;\n" ::: "memory");
     release_dependents();
     const int row = tid - 256;
     const uint32_t lane_base = (uint32_t)(32 * (wid - 8)) << 16;
@@ -658,6 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         qimage(io + 1);
       }
       // epilogue of item io
+      if (row == 0) B.prog[8] = io;
       const RItem it = p.items[p.sched_items[i0 + io]];
       const RRow rr = p.rows[it.row0 + row];
       wait_bar(smem_u32(&B.ml_full[io & 1]), (io >> 1) & 1);
@@ -718,8 +767,8 @@ long long* hang_slot() {
   if (!tried) {
     tried = true;
     if (std::getenv("FKV_HANG_DIAG") &&
-        cudaHostAlloc((void**)&host, 8 * sizeof(long long), cudaHostAllocMapped) == cudaSuccess) {
-      for (int i = 0; i < 8; ++i) host[i] = 0;
+        cudaHostAlloc((void**)&host, 32 * sizeof(long long), cudaHostAllocMapped) == cudaSuccess) {
+      for (int i = 0; i < 32; ++i) host[i] = 0;
       if (cudaHostGetDevicePointer((void**)&devp, host, 0) != cudaSuccess) devp = nullptr;
     }
   }
@@ -737,9 +786,14 @@ std::string hang_report() {
     h = d;
   }
   if (h[0] == 0) return "";
-  char buf[256];
-  std::snprintf(buf, sizeof(buf), "rows kernel deadlock: block %lld thread %lld barrier@smem+%lld parity %lld (ra_rows.cu:%lld)",
-                h[1], h[2], h[3], h[4], h[5]);
+  char buf[512];
+  int n = std::snprintf(buf, sizeof(buf),
+                        "rows kernel deadlock: block %lld thread %lld barrier@smem+%lld parity %lld (ra_rows.cu:%lld); "
+                        "progress softmax g %lld %lld %lld %lld | mma u %lld | K wait %lld issued %lld | res wait %lld "
+                        "issued %lld | V wait %lld issued %lld | aux io %lld",
+                        h[1], h[2], h[3], h[4], h[5], h[8], h[9], h[10], h[11], h[12], h[13], h[17], h[14], h[18], h[15],
+                        h[19], h[16]);
+  (void)n;
   return buf;
 }
 

@@ -40,7 +40,8 @@ struct RTile {         // 64 bytes
   int32_t base_off;    // base_pages[base_off + i], i < 128 / P (page ids, -1 = none)
   int32_t kv_head;     // local kv head
   int32_t res_off[8];  // res_pages[res_off[s] + i] for slot s
-  int32_t pad_[2];
+  int32_t n_slots;     // residual slots of the tile's WU (copy of RWu::n_slots: one dependent load less)
+  int32_t base_page;   // base_pages[base_off] (the tile's only page when P = 128), -1 = none
 };
 static_assert(sizeof(RTile) == 64, "RTile");
 constexpr int32_t kTileFirst = 1, kTileCausal = 2;

@@ -37,6 +37,14 @@ KIND_BK = 5
 KIND_BV = 6
 KIND_Q = 7
 KIND_TOKEN = 8
+# projection producer inputs (§8(f) f2/f3): layer input x [T][hidden] (owner = writer agent, pos = token position,
+# head = column >> 8, col = column & 255), the model's K / V projections W [hidden][Hkv][d] (owner 0, pos = hidden
+# row) and the adapters' down projections A [hidden][r] (owner = adapter id, pos = hidden row)
+KIND_X = 9
+KIND_WK = 10
+KIND_WV = 11
+KIND_AK = 12
+KIND_AV = 13
 
 # Scales (powers of two so fp32 scaling is exact). Q is 4x so that logits
 # have std ~1.3 at d=128; B is 1/8 so the residual K is ~25-30% of base K
@@ -49,6 +57,11 @@ SCALE = {
     KIND_BK: 0.125,
     KIND_BV: 0.125,
     KIND_Q: 4.0,
+    KIND_X: 1.0,
+    KIND_WK: 0.03125,   # x W has std ~0.67 at hidden 4096
+    KIND_WV: 0.03125,
+    KIND_AK: 0.03125,
+    KIND_AV: 0.03125,
 }
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
