@@ -366,13 +366,14 @@ class Run:
                     self.fkv.residual_attention_phases(self.pl, 0, self.Q[0], self.O[0], 1)
             torch.cuda.synchronize()
             ts = []
-            for _ in range(reps + 5):
-                e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(s)
-                g.replay()
-                e1.record(s)
-                torch.cuda.synchronize()
-                ts.append(e0.elapsed_time(e1))
+            with torch.cuda.stream(s):                    # replay() launches on the current stream
+                for _ in range(reps + 5):
+                    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(s)
+                    g.replay()
+                    e1.record(s)
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1))
             return statistics.median(ts[5:])
         except Exception as e:  # capture is a measurement aid, not part of the hot path
             print(f"graph timing unavailable: {e}", file=sys.stderr)

@@ -181,6 +181,30 @@ fkv_status fkv_fork_tokens(fkv_ctx* ctx, int64_t child, int32_t adapter_id, cons
  * changed). Outputs are token counts, multiples of page_size. */
 fkv_status fkv_fork_resume(fkv_ctx* ctx, int64_t child, int32_t adapter_id, int64_t owner, const int32_t* tokens,
                            int64_t n, int64_t* base_hit, int64_t* res_hit, int64_t* mapped);
+/* ---- sequence split across GPUs (§8(f) row f4) ------------------------------
+ * A very long shared prefix with few agents does not partition by agent or
+ * head; its keys do. Softmax is invariant to blocking (P-6): each GPU
+ * attends over its own key range and the partial outputs are merged by their
+ * log-sum-exp; the late V fusion (Eq.4) is linear, so the merge is exact.
+ * fkv_plan_create_range: as fkv_plan_create, restricted to the keys
+ *   [key_begin, key_end) (page-aligned; key_end = INT64_MAX for "to the end");
+ *   rows that see no key of the range produce O = 0 and lse = -inf.
+ * fkv_residual_attention_lse: fkv_residual_attention that also writes
+ *   lse [sum q_len][Hq_local] (fp32, natural log of sum_t exp(scale q.k_t)).
+ * fkv_merge_lse: O = sum_p exp(lse_p - L) O_p, L = log sum_p exp(lse_p), for
+ *   O_parts [n_parts][n_rows][head_dim] (dtype) and lse_parts [n_parts][n_rows]
+ *   (device; e.g. gathered over NCCL); lse_out (nullable) receives L. Rows
+ *   with every lse_p = -inf give O = 0. No ctx: a pure device routine. */
+/* Key range [*key_begin, *key_end) of `rank` among G: page-aligned, ~equal page counts over [0, max_seqlen), the
+ * last range open-ended (INT64_MAX). */
+fkv_status fkv_partition_keys(int64_t max_seqlen, int32_t G, int32_t page_size, int32_t rank, int64_t* key_begin,
+                              int64_t* key_end);
+fkv_status fkv_plan_create_range(fkv_ctx* ctx, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t key_begin,
+                                 int64_t key_end, fkv_plan** plan);
+fkv_status fkv_residual_attention_lse(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
+                                      float* lse, float sm_scale, void* workspace, size_t ws_bytes, void* stream);
+fkv_status fkv_merge_lse(int32_t n_parts, int64_t n_rows, int32_t head_dim, int32_t dtype, const void* O_parts,
+                         const float* lse_parts, void* O, float* lse_out, void* stream);
 /* ---- projection producer (§8(f) rows f2, f3) -------------------------------
  * The step in front of the hot path: it fills the disaggregated pools from a
  * layer's input activations (Eq.2: bCache = xW, rCache = xA_i;

@@ -81,6 +81,10 @@ SIGNATURES = {
     "fkv_create_root": ([_vp, _i64, _i32], _i32),
     "fkv_fork": ([_vp, _i64, _i64, _i64, _i32, _u32], _i32),
     "fkv_fork_tokens": ([_vp, _i64, _i32, _pi32, _i64, _pi64], _i32),
+    "fkv_partition_keys": ([_i64, _i32, _i32, _i32, _pi64, _pi64], _i32),
+    "fkv_plan_create_range": ([_vp, _i32, _vp, _u32, _i64, _i64, ctypes.POINTER(_vp)], _i32),
+    "fkv_residual_attention_lse": ([_vp, _vp, _i32, _vp, _vp, _vp, _f32, _vp, ctypes.c_size_t, _vp], _i32),
+    "fkv_merge_lse": ([_i32, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp], _i32),
     "fkv_register_adapter_down": ([_vp, _i32, _vp, _vp, _i32], _i32),
     "fkv_project_workspace_bytes": ([_vp, _i64, ctypes.POINTER(ctypes.c_size_t)], _i32),
     "fkv_project_kv": ([_vp, _i32, _i32, _pi64, _pi64, _pi32, _vp, _i32, _vp, _vp, _u32, _vp, ctypes.c_size_t, _vp],

@@ -72,6 +72,29 @@ def synth_fill(dst, seed: int, kind: int, owner: int, layer: int, pos0: int, hea
                                          scale, _stream_handle(stream)))
 
 
+def merge_lse(O_parts, lse_parts, O=None, lse_out=None, stream=None):
+    """fkv_merge_lse: O_parts [G][rows...][d], lse_parts [G][rows...] (device) -> merged O (and lse)."""
+    import torch
+    G = O_parts.shape[0]
+    d = O_parts.shape[-1]
+    n_rows = lse_parts[0].numel()
+    if O is None:
+        O = torch.empty(O_parts.shape[1:], dtype=O_parts.dtype, device=O_parts.device)
+    lib = L.load()
+    dt = L.DTYPE_BF16 if O_parts.dtype == torch.bfloat16 else L.DTYPE_F32
+    _check(lib, None, lib.fkv_merge_lse(G, n_rows, d, dt, _ptr(O_parts), _ptr(lse_parts), _ptr(O), _ptr(lse_out),
+                                         _stream_handle(stream)))
+    return O
+
+
+def partition_keys(max_seqlen: int, G: int, page_size: int, rank: int) -> Tuple[int, Optional[int]]:
+    """Key range (begin, end) of `rank` for the cross-GPU sequence split (end None = open-ended)."""
+    lib = L.load()
+    kb, ke = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib, None, lib.fkv_partition_keys(max_seqlen, G, page_size, rank, ctypes.byref(kb), ctypes.byref(ke)))
+    return kb.value, (None if ke.value == (1 << 63) - 1 else ke.value)
+
+
 def partition(G: int, n_kv_heads: int, base_bytes: int, res_bytes: int) -> Tuple[int, int]:
     lib = L.load()
     H, D = ctypes.c_int32(), ctypes.c_int32()
@@ -287,11 +310,18 @@ class ForkKV:
         return [tuple(buf[4 * i:4 * i + 4].tolist()) for i in range(n.value)]
 
     # ---- hot path -------------------------------------------------------------
-    def plan(self, seqs: Iterable[Tuple[int, int]], flags: int = 0, upload: bool = True, stream=None) -> Plan:
+    def plan(self, seqs: Iterable[Tuple[int, int]], flags: int = 0, upload: bool = True, stream=None,
+             key_range: Optional[Tuple[int, int]] = None) -> Plan:
+        """fkv_plan_create, or fkv_plan_create_range when key_range = (begin, end) (end None = to the end)."""
         seqs = list(seqs)
         arr = (L.fkv_seq * len(seqs))(*[L.fkv_seq(a, q, 0) for a, q in seqs])
         h = ctypes.c_void_p()
-        self._c(self.lib.fkv_plan_create(self.ctx, len(seqs), arr, flags, ctypes.byref(h)))
+        if key_range is None:
+            self._c(self.lib.fkv_plan_create(self.ctx, len(seqs), arr, flags, ctypes.byref(h)))
+        else:
+            kb, ke = key_range
+            self._c(self.lib.fkv_plan_create_range(self.ctx, len(seqs), arr, flags, kb,
+                                                   (1 << 63) - 1 if ke is None else ke, ctypes.byref(h)))
         info = L.fkv_plan_info()
         self._c(self.lib.fkv_plan_get_info(h, ctypes.byref(info)))
         pl = Plan(self, h, info)
@@ -316,6 +346,17 @@ class ForkKV:
         self._c(self.lib.fkv_residual_attention(self.ctx, pl.handle, layer, _ptr(Q), _ptr(O), sm_scale,
                                                 _ptr(pl.ws), pl.ws.numel() * 4, _stream_handle(stream)))
         return O
+
+    def residual_attention_lse(self, pl: Plan, layer: int, Q, O=None, lse=None, sm_scale: float = 0.0, stream=None):
+        """Attention plus the per-row log-sum-exp [rows][Hq_local] (fp32), for the cross-GPU LSE merge (§8(f) f4)."""
+        import torch
+        if O is None:
+            O = torch.empty_like(Q)
+        if lse is None:
+            lse = torch.empty(Q.shape[0], Q.shape[1], dtype=torch.float32, device=Q.device)
+        self._c(self.lib.fkv_residual_attention_lse(self.ctx, pl.handle, layer, _ptr(Q), _ptr(O), _ptr(lse), sm_scale,
+                                                    _ptr(pl.ws), pl.ws.numel() * 4, _stream_handle(stream)))
+        return O, lse
 
     def residual_attention_phases(self, pl: Plan, layer: int, Q, O, phases: int, sm_scale: float = 0.0,
                                   stream=None):

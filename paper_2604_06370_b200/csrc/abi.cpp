@@ -240,6 +240,47 @@ fkv_status fkv_plan_create(fkv_ctx* ctx, int32_t n, const fkv_seq* seqs, uint32_
   return FKV_OK;
 }
 
+fkv_status fkv_plan_create_range(fkv_ctx* ctx, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t key_begin,
+                                 int64_t key_end, fkv_plan** out) {
+  if (!ctx || !out) return FKV_E_INVALID;
+  *out = nullptr;
+  fkv::Plan* p = nullptr;
+  fkv_status st = guard(ctx, [&] { p = fkv::make_plan(ctx->c, n, seqs, flags, key_begin, key_end); });
+  if (st != FKV_OK) return st;
+  *out = new fkv_plan{p};
+  return FKV_OK;
+}
+
+fkv_status fkv_residual_attention_lse(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
+                                      float* lse, float sm_scale, void* workspace, size_t ws_bytes, void* stream) {
+  if (!ctx || !plan || !lse) return FKV_E_INVALID;
+  return guard(ctx, [&] {
+    fkv::run_attention(ctx->c, *plan->p, layer, Q, O, sm_scale, workspace, ws_bytes, stream, 3u, lse);
+  });
+}
+
+fkv_status fkv_merge_lse(int32_t n_parts, int64_t n_rows, int32_t head_dim, int32_t dtype, const void* O_parts,
+                         const float* lse_parts, void* O, float* lse_out, void* stream) {
+  if (n_parts < 1 || n_rows < 0 || head_dim < 1 || !O_parts || !lse_parts || !O ||
+      (dtype != FKV_DTYPE_BF16 && dtype != FKV_DTYPE_F32))
+    return FKV_E_INVALID;
+  const cudaError_t e = fkv::k::launch_merge_lse(n_parts, n_rows, head_dim, O_parts, lse_parts, O, lse_out, dtype,
+                                                 (cudaStream_t)stream);
+  return e == cudaSuccess ? FKV_OK : FKV_E_CUDA;
+}
+
+fkv_status fkv_partition_keys(int64_t max_seqlen, int32_t G, int32_t page_size, int32_t rank, int64_t* key_begin,
+                              int64_t* key_end) {
+  if (G < 1 || rank < 0 || rank >= G || page_size < 1 || max_seqlen < 0 || !key_begin || !key_end)
+    return FKV_E_INVALID;
+  // G page-aligned ranges of ~equal page count over [0, max_seqlen); the last one open-ended
+  const int64_t pages = (max_seqlen + page_size - 1) / page_size;
+  const int64_t lo = pages * rank / G, hi = pages * (rank + 1) / G;
+  *key_begin = lo * page_size;
+  *key_end = rank == G - 1 ? INT64_MAX : hi * page_size;
+  return FKV_OK;
+}
+
 fkv_status fkv_plan_get_info(const fkv_plan* plan, fkv_plan_info* info) {
   if (!plan || !info) return FKV_E_INVALID;
   const fkv::Plan& p = *plan->p;

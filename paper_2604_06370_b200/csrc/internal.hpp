@@ -201,6 +201,7 @@ struct Plan {
   bool l2_evict_first = false;                   // see AttnParams::l2_evict_first
   std::vector<int32_t> stage_desc;               // per image: B_k^h address (2 ints), n_rows, h, Q row index [16]
   int32_t n_ctas = 0;
+  bool key_range = false;  // range plan (§8(f) f4): output rows may see no key of [key_begin, key_end)
   size_t stage_off = 0;  // workspace offset of the staged operand images (tcgen05 kernel)
   int64_t n_segments = 0, n_entries = 0, key_tiles = 0, alg_bytes = 0;
   // rows-on-lanes tcgen05 kernel (kernel 3): k::RItem / RWu / RTile / RRow records (rows.hpp)
@@ -252,9 +253,10 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
                      const std::vector<int64_t>& base_off, const std::vector<int64_t>& res_off, int sms);
 
 // plan.cpp
-Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags);
+Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t key_begin = 0,
+                int64_t key_end = INT64_MAX);
 void upload_plan(Ctx& c, Plan& p, void* dev, size_t bytes, void* stream);
 void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O, float scale, void* ws,
-                   size_t ws_bytes, void* stream, uint32_t phases = 3u);
+                   size_t ws_bytes, void* stream, uint32_t phases = 3u, float* lse = nullptr);
 
 }  // namespace fkv

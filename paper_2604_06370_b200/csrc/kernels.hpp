@@ -54,6 +54,7 @@ static_assert(sizeof(ItemRecT<4>) == 176 && sizeof(ItemRecT<8>) == 336, "ItemRec
 constexpr int kTileRecInts = 16;  // tile record: t0, k1, meta, base page, residual page of slots 0..7, pad
 
 struct AttnParams {
+  float* lse;              // optional per output row log-sum-exp of the scaled logits (natural log; -inf = no keys)
   const void* base_k;
   const void* base_v;
   const void* res_k;
@@ -140,6 +141,9 @@ cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStrea
 cudaError_t launch_stage(const AttnParams& p, int32_t n_warps, cudaStream_t s);
 size_t tc_maps_bytes();
 cudaError_t launch_combine(const AttnParams& p, cudaStream_t s);
+// O = sum_p exp(lse_p - L) O_p, L = log sum_p exp(lse_p): merge of attention outputs over disjoint key ranges
+cudaError_t launch_merge_lse(int32_t n_parts, int64_t n_rows, int32_t d, const void* O_parts, const float* lse_parts,
+                             void* O, float* lse_out, int32_t dtype, cudaStream_t s);
 cudaError_t launch_attention_rows(const RowsParams& p, const RowsMaps& maps, cudaStream_t s);
 // host-mapped deadlock report of the rows kernel (allocated on first use when FKV_HANG_DIAG is set, else nullptr)
 long long* hang_slot();

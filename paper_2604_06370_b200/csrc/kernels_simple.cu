@@ -210,7 +210,9 @@ __global__ void combine_kernel(AttnParams p) {
     for (int c = 0; c < kMaxD; ++c)
       if (lane + 32 * c < d) acc[c] += a * ldf<T>(bv, (int64_t)j * d + lane + 32 * c);
   }
-  const float inv = 1.f / l;
+  // a row with no keys in this plan's key range (range plans, §8(f) f4): O = 0, lse = -inf
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  if (p.lse && lane == 0) p.lse[warp] = l > 0.f ? (Mrun + log2f(l)) * 0.69314718055994531f : -INFINITY;
   T* o = (T*)p.O + (int64_t)warp * d;
 #pragma unroll
   for (int c = 0; c < kMaxD; ++c) {
@@ -473,7 +475,8 @@ __global__ void __launch_bounds__(256, 2) combine128_kernel(AttnParams p) {
     }
     acc.x += a * b.x; acc.y += a * b.y; acc.z += a * b.z; acc.w += a * b.w;
   }
-  const float inv = 1.f / l;
+  const float inv = l > 0.f ? 1.f / l : 0.f;   // no keys in a range plan's key range: O = 0, lse = -inf
+  if (p.lse && lane == 0) p.lse[warp] = l > 0.f ? (Mrun + log2f(l)) * 0.69314718055994531f : -INFINITY;
   T* o = (T*)p.O + (int64_t)warp * 128 + 4 * lane;
   if constexpr (sizeof(T) == 2) {
     __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
@@ -498,6 +501,47 @@ cudaError_t launch_combine(const AttnParams& p, cudaStream_t s) {
     combine_kernel<__nv_bfloat16><<<blocks, threads, 0, s>>>(p);
   else
     combine_kernel<float><<<blocks, threads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// LSE merge of G partial attention outputs of the same rows over disjoint key ranges (blocking invariance of
+// softmax; the late V fusion is linear so each part's fused O merges exactly): warp per row, lanes over d
+template <typename T>
+__global__ void merge_lse_kernel(int32_t G, int64_t n_rows, int32_t d, const T* __restrict__ Op,
+                                 const float* __restrict__ lp, T* __restrict__ O, float* __restrict__ lse_out) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  float M = -INFINITY;
+  for (int g = 0; g < G; ++g) M = fmaxf(M, lp[(int64_t)g * n_rows + row]);
+  float den = 0.f;
+  for (int g = 0; g < G; ++g) {
+    const float v = lp[(int64_t)g * n_rows + row];
+    den += v == -INFINITY ? 0.f : __expf(v - M);
+  }
+  for (int e = lane; e < d; e += 32) {
+    float acc = 0.f;
+    for (int g = 0; g < G; ++g) {
+      const float v = lp[(int64_t)g * n_rows + row];
+      if (v != -INFINITY) acc += __expf(v - M) * ldf<T>(Op, ((int64_t)g * n_rows + row) * d + e);
+    }
+    const float o = den > 0.f ? acc / den : 0.f;
+    if constexpr (sizeof(T) == 2) O[row * d + e] = __float2bfloat16_rn(o);
+    else O[row * d + e] = o;
+  }
+  if (lse_out && lane == 0) lse_out[row] = den > 0.f ? M + __logf(den) : -INFINITY;
+}
+
+cudaError_t launch_merge_lse(int32_t n_parts, int64_t n_rows, int32_t d, const void* O_parts, const float* lse_parts,
+                             void* O, float* lse_out, int32_t dtype, cudaStream_t s) {
+  if (n_rows <= 0) return cudaSuccess;
+  const int64_t blocks = (n_rows * 32 + 255) / 256;
+  if (dtype == FKV_DTYPE_BF16)
+    merge_lse_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, s>>>(n_parts, n_rows, d, (const __nv_bfloat16*)O_parts,
+                                                                     lse_parts, (__nv_bfloat16*)O, lse_out);
+  else
+    merge_lse_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(n_parts, n_rows, d, (const float*)O_parts, lse_parts,
+                                                             (float*)O, lse_out);
   return cudaGetLastError();
 }
 

@@ -42,7 +42,7 @@ size_t put(std::vector<uint8_t>& blob, const std::vector<T>& v) {
 }
 }  // namespace
 
-Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
+Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t key_begin, int64_t key_end) {
   if (n < 1 || !seqs) throw Error(FKV_E_INVALID, "plan: empty batch");
   const int P = c.cfg.page_size;
   const int g = c.group;
@@ -138,6 +138,21 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
       // push in reverse so segments come out in ascending page-id order
       for (auto it = groups.rbegin(); it != groups.rend(); ++it) stack.push_back({it->second, s});
     }
+  }
+  // range plan (§8(f) f4, sequence split across GPUs): only the keys of [key_begin, key_end), page-aligned
+  if (key_begin != 0 || key_end != INT64_MAX) {
+    const int P_ = c.cfg.page_size;
+    if (key_begin < 0 || key_end <= key_begin || key_begin % P_ || (key_end != INT64_MAX && key_end % P_))
+      throw Error(FKV_E_INVALID, "plan: key range must be page-aligned and non-empty");
+    pl.key_range = true;
+    const int64_t s0 = key_begin / P_, s1 = key_end == INT64_MAX ? INT64_MAX : key_end / P_;
+    std::vector<Seg> kept;
+    for (Seg sg : segs) {
+      sg.slot0 = std::max<int64_t>(sg.slot0, s0);
+      sg.slot1 = std::min<int64_t>(sg.slot1, s1);
+      if (sg.slot1 > sg.slot0) kept.push_back(std::move(sg));
+    }
+    segs.swap(kept);
   }
   pl.n_segments = (int64_t)segs.size();
   int sms = 148;
@@ -417,7 +432,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags) {
       pl.out_entries[fill[o]++] = w.entry_off + j;
     }
   for (int64_t o = 0; o < n_out; ++o)
-    if (pl.out_ptr[o + 1] == pl.out_ptr[o]) throw Error(FKV_E_NO_KEYS, "plan: an output row has no keys");
+    if (!pl.key_range && pl.out_ptr[o + 1] == pl.out_ptr[o]) throw Error(FKV_E_NO_KEYS, "plan: an output row has no keys");
   // adapters
   pl.adapter_ptrs.resize(c.adapters.size() * 2);
   for (size_t s = 0; s < c.adapters.size(); ++s) {
@@ -499,7 +514,7 @@ void upload_plan(Ctx& c, Plan& p, void* dev, size_t bytes, void* stream) {
 }
 
 void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O, float scale, void* ws,
-                   size_t ws_bytes, void* stream, uint32_t phases) {
+                   size_t ws_bytes, void* stream, uint32_t phases, float* lse) {
   if (phases == 0 || (phases & ~3u)) throw Error(FKV_E_INVALID, "attention: bad phases");
   if (!c.device) throw Error(FKV_E_INVALID, "attention: host-only ctx");
   if (p.generation != c.generation) throw Error(FKV_E_STALE, "attention: plan is stale");
@@ -514,6 +529,7 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   if (!ws || ws_bytes < p.ws_bytes || ((uintptr_t)ws & 255)) throw Error(FKV_E_INVALID, "attention: workspace too small or not 256-byte aligned");
   const uint8_t* base = (const uint8_t*)p.dev;
   k::AttnParams a{};
+  a.lse = lse;
   a.base_k = c.buf.base_k; a.base_v = c.buf.base_v; a.res_k = c.buf.res_k; a.res_v = c.buf.res_v;
   a.rope_cos = c.buf.rope_cos; a.rope_sin = c.buf.rope_sin;
   a.Q = Q; a.O = O; a.ws = (float*)ws;
@@ -581,7 +597,7 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
       rp.dbg = a.dbg; rp.dbg_block = a.dbg_block;
       rp.flags = getenv("FKV_ROWS_FLAGS") ? atoi(getenv("FKV_ROWS_FLAGS")) : 0;
       rp.hang = k::hang_slot();
-      rp.prefetch = getenv("FKV_ROWS_PREFETCH") ? atoi(getenv("FKV_ROWS_PREFETCH")) : 0;
+      rp.prefetch = getenv("FKV_ROWS_PREFETCH") ? atoi(getenv("FKV_ROWS_PREFETCH")) : 3;
       e = k::launch_attention_rows(rp, *(const k::RowsMaps*)c.rows_maps.data(), (cudaStream_t)stream);
     }
     if (e == cudaSuccess && (phases & FKV_PHASE_COMBINE)) e = k::launch_combine(a, (cudaStream_t)stream);

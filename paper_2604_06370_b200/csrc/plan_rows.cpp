@@ -314,7 +314,8 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
     for (size_t e = 0; e < entry_qrow.size(); ++e) pl.out_entries[fill[entry_qrow[e]]++] = (int32_t)e;
   }
   for (int64_t o = 0; o < n_out; ++o)
-    if (pl.out_ptr[o + 1] == pl.out_ptr[o]) throw Error(FKV_E_NO_KEYS, "plan: an output row has no keys");
+    if (!pl.key_range && pl.out_ptr[o + 1] == pl.out_ptr[o])
+      throw Error(FKV_E_NO_KEYS, "plan: an output row has no keys");
   pl.adapter_ptrs.resize(c.adapters.size() * 2);
   for (size_t s = 0; s < c.adapters.size(); ++s) {
     pl.adapter_ptrs[2 * s] = (int64_t)(intptr_t)c.adapters[s].bk;

@@ -470,8 +470,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ======= K_base (warp 5) / V_base (warp 7) tiles: one TMA box {64 d, 128 keys, 2 d-halves} per tile (P = 128) =======
       // (one issuing thread streams ~45 B/clk at most, tools/ub_fill.cu: K and V get a thread each). The next tile's
       // record is read one step ahead (its latency overlaps this step's wait for a free ring slot).
-      if (lane == 0) {
+      {
+        // lane 0 issues the TMA boxes; the whole warp runs the walk so that its 32 lanes can prefetch the page of
+        // the tile `p.prefetch` steps ahead into L2 (prefetch.global.L2 over the LSU path: the TMA engine's
+        // delivery rate is its outstanding bytes over the load latency, and L2 hits halve that latency)
         const int my_kind = wid == 5 ? 0 : 1;
+        TileCursor pf;
+        if (p.prefetch > 0) pf.init(p, p.prefetch);
+        const uint8_t* plane = (const uint8_t*)(my_kind == 0 ? p.base_k : p.base_v);
         uint32_t u = 0;
         int kt = 0;
         const int P = p.P;
@@ -496,13 +502,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             n_pg = __ldg(&Tn->base_page); n_h = __ldg(&Tn->kv_head); n_nk = __ldg(&Tn->n_keys);
             n_bo = __ldg(&Tn->base_off);
           }
+          if (p.prefetch > 0 && P == 128) {
+            const int tf = pf.next(p);
+            if (tf >= 0) {
+              const RTile* Tf = p.tiles + tf;
+              const int fpg = __ldg(&Tf->base_page), fh = __ldg(&Tf->kv_head);
+              if (fpg >= 0) {
+                const uint8_t* src =
+                    plane + ((size_t)p.base_rows_layer + (size_t)fpg * p.hkv * P + (size_t)fh * P) * 256;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 128 * (lane + 32 * j)));
+              }
+            }
+          }
           const int64_t hrow = (int64_t)c_h * P;
           const uint32_t s_ = u % kNU;
-          B.prog[wid] = (int)u;
+          if (lane == 0) B.prog[wid] = (int)u;
           wait_bar(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
-          if (my_kind == 0) stamp(p, 6, kt++);
+          if (my_kind == 0 && lane == 0) stamp(p, 6, kt++);
           const uint32_t dst = sb + OFF_RING + s_ * kUnit;
-          if (P == 128) {
+          if (lane != 0) {
+            // lanes 1..31 only prefetch
+          } else if (P == 128) {
             mbar_expect_tx(smem_u32(&B.full[s_]), c_pg >= 0 ? 32768u : 0u);
             if (c_pg >= 0)
               tma_load_3d(dst, m3, 0, (int)(p.base_rows_layer + (int64_t)c_pg * p.hkv * P + hrow), 0,
@@ -519,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_2d(dst + 16384 + pi * P * 128, m2, 64, r0, smem_u32(&B.full[s_]));
             }
           }
-          B.prog[wid + 4] = (int)u;
+          if (lane == 0) B.prog[wid + 4] = (int)u;
           u += 2;
           c_pg = n_pg; c_h = n_h; c_nk = n_nk; c_bo = n_bo;
           have = true;
@@ -545,9 +567,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         ns = __ldg(&T0->n_slots);
         pg = (P == 128 && lane < ns) ? p.res_pages[__ldg(&T0->res_off[lane])] : -1;
       };
+      TileCursor pf;
+      if (p.prefetch > 0) pf.init(p, p.prefetch);
       walk(p, [&](int kind, int, int, int ti, int, int tn) {
         const bool is_rv = kind == 1;
         int pg, nk, ns;
+        if (!is_rv && p.prefetch > 0 && P == 128) {
+          // residual pages (both planes) of the tile `prefetch` steps ahead into L2: lane = (slot, plane, quarter)
+          const int tf = pf.next(p);
+          if (tf >= 0) {
+            const RTile* Tf = p.tiles + tf;
+            const int sl = lane >> 2, pl = (lane >> 1) & 1, hf = lane & 1;
+            if (sl < __ldg(&Tf->n_slots)) {
+              const int fpg = p.res_pages[__ldg(&Tf->res_off[sl])];
+              if (fpg >= 0) {
+                const uint8_t* src = (pl ? rpv : rpk) + (size_t)fpg * 4096 + 2048 * hf;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 128 * j));
+              }
+            }
+          }
+        }
         if (!is_rv) {
           if (!have) rec(ti, c_pg, c_nk, c_ns);
           pg = c_pg; nk = c_nk; ns = c_ns;

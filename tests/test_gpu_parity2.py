@@ -213,3 +213,34 @@ def test_deferred_plan_refuses_sequences_past_rope_table():
     with pytest.raises(L.FkvError) as e:
         fkv.plan([(0, 1)])
     assert e.value.code == L.E_INVALID
+
+
+# ---- §8(f) f4: key-range plans + LSE merge (the cross-GPU sequence split, on one GPU) -------------------------
+
+@pytest.mark.parametrize("mode", ["none", "deferred"])
+@pytest.mark.parametrize("G", [2, 3])
+def test_sequence_split_range_plans_merge(mode, G):
+    """G key-range plans (fkv_plan_create_range) of one batch, attention with lse (fkv_residual_attention_lse),
+    fkv_merge_lse of the G partial outputs == the oracle over all keys; decode rows and a chunked-prefill chunk
+    (rows whose causal window ends before a range see no key of it: O = 0, lse = -inf in that part)."""
+    from paper_2604_06370_b200.api import merge_lse, partition_keys
+    ag = [recipes.AgentSpec(1000, 1000, None, 0, False, 2000, decode=False)]
+    for i in range(3):
+        ag.append(recipes.AgentSpec(i, i, 1000, 2000, False, 60 + 30 * i))
+    for C in (1, 90):
+        scen = recipes.Scenario("split", ag, q_len=C)
+        fkv = _ctx(scen, 32, 8, 64, mode)
+        driver.build(fkv, scen, seed=31)
+        batch = scen.batch()
+        Q = driver.make_queries(fkv, scen, 31, 0)
+        Ls = max(scen.seqlen(a) for a in batch)
+        Os, ls = [], []
+        for r in range(G):
+            kb, ke = partition_keys(Ls, G, 64, r)
+            pl = fkv.plan([(a, C) for a in batch], key_range=(kb, ke))
+            O, lse = fkv.residual_attention_lse(pl, 0, Q)
+            Os.append(O)
+            ls.append(lse)
+        Om = merge_lse(torch.stack(Os), torch.stack(ls))
+        err = _check(fkv, scen, 31, 0, mode, seqs=range(len(batch)), O=Om)
+        assert err <= TOL, (C, err)
