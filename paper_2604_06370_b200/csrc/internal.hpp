@@ -201,7 +201,9 @@ struct Plan {
   bool l2_evict_first = false;                   // see AttnParams::l2_evict_first
   std::vector<int32_t> stage_desc;               // per image: B_k^h address (2 ints), n_rows, h, Q row index [16]
   int32_t n_ctas = 0;
-  bool key_range = false;  // range plan (§8(f) f4): output rows may see no key of [key_begin, key_end)
+  bool key_range = false;
+  size_t ws_ctr_off = 0;             // kernel 3: workspace offset of the item-queue counters
+  mutable const void* ws_zeroed = nullptr;  // the workspace whose counters were last zeroed for this plan  // range plan (§8(f) f4): output rows may see no key of [key_begin, key_end)
   size_t stage_off = 0;  // workspace offset of the staged operand images (tcgen05 kernel)
   int64_t n_segments = 0, n_entries = 0, key_tiles = 0, alg_bytes = 0;
   // rows-on-lanes tcgen05 kernel (kernel 3): k::RItem / RWu / RTile / RRow records (rows.hpp)

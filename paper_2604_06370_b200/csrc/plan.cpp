@@ -588,6 +588,13 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
       rp.adapters = a.adapters;
       rp.sched_ptr = a.sched_ptr;
       rp.sched_items = a.sched_items;
+      rp.n_items = (int32_t)(p.r_items.size() / sizeof(k::RItem));
+      rp.ctr = (int32_t*)((uint8_t*)ws + p.ws_ctr_off);
+      if (p.ws_zeroed != ws) {  // the kernel leaves the counters zero; a fresh workspace needs them zeroed once
+        e = cudaMemsetAsync(rp.ctr, 0, 8, (cudaStream_t)stream);
+        if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("attention: ") + cudaGetErrorString(e));
+        p.ws_zeroed = ws;
+      }
       rp.base_rows_layer = (int64_t)layer * c.cfg.n_base_pages * c.hkv_local * P;
       rp.res_layer_elems = a.res_layer_stride;
       rp.adapter_layer_elems = a.adapter_layer_stride;

@@ -49,14 +49,17 @@ struct WuC {                   // work-unit candidate: rows of one kv head over 
   std::array<int64_t, 4> loc{};       // locality key (segment start, piece, block, head)
 };
 
-// estimated cycles of one tile on the tensor pipe (tcgen05.mma M=128: max(44, N/2) cycles per K=16 step,
-// measured tools/ub_mma_r2.cu), floored by the softmax (MUFU ex2 of 128 rows x keys on one warpgroup)
+// estimated cycles of one tile: the tensor pipe (tcgen05.mma M=128: max(44, N/2) cycles per K=16 step,
+// tools/ub_mix.cu), the softmax (MUFU ex2 of 128 rows x keys on one warpgroup) and the ring fill (whole K and V
+// pages plus 8 KB per residual slot at the ~26 B/cycle a CTA sustains in the kernel: a 1-key tile costs a page
+// load like a full one), whichever binds
 int64_t tile_cost(int n_keys, int n_slots) {
   auto c = [](int n) { return std::max<int64_t>(44, n / 2); };
   const int ns = (n_keys + 15) & ~15, nk = (n_keys + 15) / 16;
   const int64_t tensor = (8 + n_slots) * c(ns) + nk * (c(128) + c(16 * n_slots));
   const int64_t soft = 1100 * ns / 128;
-  return std::max(tensor, soft) + 150;
+  const int64_t fill = (65536 + 8192 * (int64_t)n_slots) / 26;
+  return std::max(std::max(tensor, soft), fill) + 150;
 }
 
 }  // namespace
@@ -151,6 +154,7 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
         w.loc = {k0, 0, (int64_t)bi, h};
         // a row block that fills at least half the lanes gets its own items; small ones are packed
         if ((int)w.rows.size() * 2 >= kLanes || tiles > 8) big.push_back(std::move(w));
+        else if (getenv("FKV_DIAG_SKIP_SMALL")) continue;  // diagnostics only: drops the small WUs (wrong output)
         else small.push_back(std::move(w));
       }
     }
@@ -160,7 +164,7 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
   int64_t total = 0;
   for (const WuC& w : big) total += w.cost + 3000;
   for (const WuC& w : small) total += w.cost + 500;
-  const double frac = getenv("FKV_PIECE_FRAC") ? atof(getenv("FKV_PIECE_FRAC")) : 0.5;
+  const double frac = getenv("FKV_PIECE_FRAC") ? atof(getenv("FKV_PIECE_FRAC")) : 0.15;
   const int64_t target = std::max<int64_t>(1, (int64_t)(frac * (double)total / sms));
   std::vector<WuC> wus;  // final work units, each with its key range
   auto split = [&](const WuC& w, bool allow) {
@@ -192,6 +196,7 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
   for (const WuC& w : small) split(w, false);
 
   // ---- items: one big WU each; small WUs packed (<= 128 lanes, bounded cost) ------------------------------
+  const int64_t small_cap = std::max<int64_t>(1, total / sms / 4);
   struct ItemC {
     std::vector<int32_t> wu;
     int64_t cost = 0;
@@ -204,7 +209,8 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
     int lanes = 0;
     for (size_t i = n_big; i < wus.size(); ++i) {
       const int nr = (int)wus[i].rows.size();
-      if (!cur.wu.empty() && (lanes + nr > kLanes || cur.cost + wus[i].cost > target)) {
+      // small items stay short (they fill the tail of the dynamic queue): at most 1/4 of a CTA's even share
+      if (!cur.wu.empty() && (lanes + nr > kLanes || cur.cost + wus[i].cost > std::min(target, small_cap))) {
         items.push_back(std::move(cur));
         cur = ItemC();
         lanes = 0;
@@ -285,22 +291,12 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
     if (ca != cb) return ca > cb;
     return items[a].loc < items[b].loc;
   });
+  // dynamic schedule: the persistent CTAs take items from this queue in order (longest first, so the tail is made
+  // of short items; ties in locality order so that the items reading the same base / residual tiles run at the
+  // same time)
   pl.n_ctas = std::max<int32_t>(1, std::min<int32_t>(sms, n_items));
-  std::vector<std::vector<int32_t>> per(pl.n_ctas);
-  std::set<std::pair<int64_t, int32_t>> load;
-  for (int32_t cc = 0; cc < pl.n_ctas; ++cc) load.insert({0, cc});
-  for (int32_t i : idx) {
-    auto lo = *load.begin();
-    load.erase(load.begin());
-    per[lo.second].push_back(i);
-    load.insert({lo.first + items[i].cost, lo.second});
-  }
-  pl.sched_ptr.assign(1, 0);
-  pl.sched_items.clear();
-  for (auto& v : per) {
-    pl.sched_items.insert(pl.sched_items.end(), v.begin(), v.end());
-    pl.sched_ptr.push_back((int32_t)pl.sched_items.size());
-  }
+  pl.sched_items = idx;
+  pl.sched_ptr = {0, n_items};
 
   // ---- combine CSR: output row -> its entries ---------------------------------------------------------------
   const int64_t n_out = pl.n_rows_q * hq;
@@ -363,7 +359,8 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
   pl.off_rtiles = put(pl.blob, pl.r_tiles);
   pl.off_rrows = put(pl.blob, pl.r_rows);
   pl.blob.resize(align256(pl.blob.size()));
-  pl.ws_bytes = align256((size_t)pl.n_entries * (size_t)(k::kEntAcc + d + r) * sizeof(float));
+  pl.ws_ctr_off = align256((size_t)pl.n_entries * (size_t)(k::kEntAcc + d + r) * sizeof(float));
+  pl.ws_bytes = pl.ws_ctr_off + 256;  // + the queue counters
 }
 
 }  // namespace fkv

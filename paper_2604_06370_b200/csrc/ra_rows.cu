@@ -47,6 +47,7 @@ constexpr uint32_t OFF_Q = 0, OFF_QT = 32768, OFF_RING = 40960;
 constexpr uint32_t OFF_BAR = OFF_RING + kNU * kUnit;
 constexpr uint32_t T_O = 256, T_AR = 384;
 constexpr int kThreads = 384;
+constexpr int kRingConsumers = 9;  // item-queue readers: 4 softmax warps, MMA issuer, K, V, R_k, R_v loaders
 
 struct Bars {
   uint64_t full[kNU], empty[kNU];
@@ -54,9 +55,16 @@ struct Bars {
   uint32_t tmem_base;
   uint32_t pad_;
   float2 ml[2][kRowsLanes];
+  uint64_t ring_full[4], ring_empty[4];  // the CTA's item queue (dynamic schedule, see the aux warpgroup)
+  int ring_id[4];
+  int issued[kNU];  // per ring slot: the last unit whose MMAs the issuer has issued (monotonic; see ring_wait_free)
   int prog[16];  // diagnostics: per-role progress counters (reported by the deadlock watchdog)
 };
-constexpr uint32_t kSmemBytes = OFF_BAR + sizeof(Bars);
+// epilogue staging: per aux warp, 8 partial entries of 152 floats (+1 pad word against bank conflicts), so that
+// the entries leave as coalesced 128-byte stores instead of 32 rows x 608-byte strides per warp instruction
+constexpr int kEpiRows = 8, kEpiStride = 153;
+constexpr uint32_t OFF_EPI = (OFF_BAR + (uint32_t)sizeof(Bars) + 127u) & ~127u;
+constexpr uint32_t kSmemBytes = OFF_EPI + 4u * kEpiRows * kEpiStride * 4u;
 static_assert(kSmemBytes <= 232448, "shared memory");
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -77,6 +85,26 @@ __device__ __forceinline__ void mma_ss_m(uint32_t d, uint64_t a, uint64_t b, uin
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d),
       "l"(a), "l"(b), "r"(id), "r"(acc), "r"(dis.x), "r"(dis.y), "r"(dis.z), "r"(dis.w));
+}
+// issued by the whole MMA warp, one elected lane executes: the operands are warp-uniform, so ptxas keeps them on the
+// uniform datapath (a single-lane issuer got an ELECT / R2UR.BROADCAST waterfall loop around every MMA)
+__device__ __forceinline__ void mma_ss_me(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc, uint4 dis) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc), "r"(dis.x), "r"(dis.y), "r"(dis.z), "r"(dis.w));
+}
+__device__ __forceinline__ void mma_ts_me(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc, uint4 dis) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(id), "r"(acc), "r"(dis.x), "r"(dis.y), "r"(dis.z), "r"(dis.w));
+}
+__device__ __forceinline__ void mma_commit_e(uint32_t mbar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(mbar)
+      : "memory");
 }
 // D (+)= A[tmem] B[smem], lane-masked
 __device__ __forceinline__ void mma_ts_m(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc, uint4 dis) {
@@ -134,74 +162,6 @@ __device__ __forceinline__ void stamp_(const RowsParams& p, int ev, int i) {
 #define stamp stamp_<kDbg>
 
 
-// Walk the CTA's tiles in MMA consumption order, software-pipelined across item boundaries:
-//   S(0), S(1) PV(0), S(2) PV(1), ..., S(N-1) PV(N-2), PV(N-1)      over the CTA's N tiles (all items, in order)
-// f(kind, item_ord, t, tile_index, n_tiles_of_item, next): kind 0 = K side of tile t of item item_ord, 1 = V side;
-// `next` = the tile index of the same kind's next step (-1 at the end).
-// The units of one kind are then at most 4 apart in the ring sequence (K, R_k, V, R_v per step): with kNU = 5 slots
-// a producer can never find a slot's `empty` barrier two phases behind (parity aliasing), which the per-item
-// order (K units 6 apart across an item boundary) allowed once K and V had producers of their own.
-template <class F>
-__device__ __forceinline__ void walk(const RowsParams& p, F&& f) {
-  const int i0 = p.sched_ptr[blockIdx.x], i1 = p.sched_ptr[blockIdx.x + 1];
-  int pv_io = -1, pv_t = 0, pv_n = 0, pv_t0 = 0;  // the tile whose V side is pending
-  int t0 = 0, n = 0;
-  if (i0 < i1) {
-    const int id = p.sched_items[i0];
-    t0 = __ldg(&p.items[id].tile0);
-    n = __ldg(&p.items[id].n_tiles);
-  }
-  for (int ii = i0; ii < i1; ++ii) {
-    int nt0 = -1, nn = 0;
-    if (ii + 1 < i1) {
-      const int id = p.sched_items[ii + 1];
-      nt0 = __ldg(&p.items[id].tile0);
-      nn = __ldg(&p.items[id].n_tiles);
-    }
-    for (int t = 0; t < n; ++t) {
-      // next flat tile of the CTA (both kinds step through the same sequence)
-      const int tn = t + 1 < n ? t0 + t + 1 : nt0;
-      f(0, ii - i0, t, t0 + t, n, tn);
-      if (pv_io >= 0) f(1, pv_io, pv_t, pv_t0 + pv_t, pv_n, t0 + t);
-      pv_io = ii - i0; pv_t = t; pv_n = n; pv_t0 = t0;
-    }
-    t0 = nt0;
-    n = nn;
-  }
-  if (pv_io >= 0) f(1, pv_io, pv_t, pv_t0 + pv_t, pv_n, -1);
-}
-
-// Cursor over the CTA's tiles in processing order, `ahead` tiles in front of the loaders: the L2 prefetch of
-// the pages a loader will need `ahead` tiles later (HBM latency is longer than the shared-memory ring covers).
-struct TileCursor {
-  int ii, i1, t, n, tile0;
-  __device__ void init(const RowsParams& p, int ahead) {
-    ii = p.sched_ptr[blockIdx.x];
-    i1 = p.sched_ptr[blockIdx.x + 1];
-    t = -1;
-    n = 0;
-    tile0 = 0;
-    if (ii < i1) {
-      const RItem it = p.items[p.sched_items[ii]];
-      n = it.n_tiles;
-      tile0 = it.tile0;
-    }
-    for (int k = 0; k < ahead; ++k) next(p);
-  }
-  // advance one tile; returns its index or -1 past the end
-  __device__ int next(const RowsParams& p) {
-    if (ii >= i1) return -1;
-    if (++t >= n) {
-      t = 0;
-      if (++ii >= i1) return -1;
-      const RItem it = p.items[p.sched_items[ii]];
-      n = it.n_tiles;
-      tile0 = it.tile0;
-    }
-    return tile0 + t;
-  }
-};
-
 template <bool kDbg>
 __global__ void __launch_bounds__(kThreads, 1)
     ra_rows_kernel(const __grid_constant__ RowsParams p, const __grid_constant__ RowsMaps maps) {
@@ -226,6 +186,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(smem_u32(&B.o_free), 4);
     mbar_init(smem_u32(&B.q_full), 4);
     mbar_init(smem_u32(&B.q_empty), 1);
+    for (int i = 0; i < kNU; ++i) B.issued[i] = -1000;
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(smem_u32(&B.ring_full[i]), 1);
+      mbar_init(smem_u32(&B.ring_empty[i]), kRingConsumers);
+    }
     fence_mbar_init();
   }
   // zero the operand buffers once: stale shared memory must hold finite values (keys beyond a ragged tile
@@ -240,9 +205,93 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = B.tmem_base;
-  const int n_my = p.sched_ptr[blockIdx.x + 1] - p.sched_ptr[blockIdx.x];
-  // register budget per warpgroup (setmaxnreg at the top of each role): softmax 224, loaders / MMA 96, aux 184
-  // (x 128 threads = 64512 registers = the CTA allocation of 168 x 384: more would deadlock setmaxnreg.inc).
+  // ---- the CTA's item queue ------------------------------------------------------------------------------
+  // Items are taken dynamically from a global queue (p.sched_items in the planner's cost order, a counter in the
+  // workspace): the aux warpgroup takes item k + 1 at the start of item k and publishes it in a 4-entry ring;
+  // every other role reads the ring (ring_get blocks, ring_try does not) and releases an item when it is done
+  // with it (kRingConsumers arrivals: the 4 softmax warps, the MMA issuer, the K, V and residual loaders). id -1
+  // = the queue is exhausted.
+  auto ring_get = [&](int k) -> int {
+    wait_bar(smem_u32(&B.ring_full[k & 3]), (k >> 2) & 1);
+    return *reinterpret_cast<volatile int*>(&B.ring_id[k & 3]);
+  };
+  auto ring_release = [&](int k) { mbar_arrive(smem_u32(&B.ring_empty[k & 3])); };
+  // A producer may refill slot u % kNU once unit u - kNU has been consumed (its MMAs completed: `empty`). The
+  // issuer consumes the S-stream and PV-stream units out of order, so a slot's `empty` barrier can lag two
+  // phases behind a producer, and a parity wait alone would then pass early (aliasing). The monotonic
+  // `issued` word removes the ambiguity: once the issuer has issued unit u - kNU, every earlier phase of the slot
+  // has completed (unit u - kNU could only be loaded after u - 2 kNU was consumed), so the parity names one phase.
+  auto slot_wait_free = [&](uint32_t u) {
+    const uint32_t s_ = u % kNU;
+    if (u >= (uint32_t)kNU) {
+      uint32_t n = 0;
+      while (*reinterpret_cast<volatile int*>(&B.issued[s_]) < (int)u - kNU) {
+        if (++n == (1u << 27) && p.hang != nullptr) hang_trap(smem_u32(&B.issued[s_]), u, p.hang, __LINE__);
+      }
+    }
+    wait_bar(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
+  };
+  // Walk the CTA's ring units in producer order, software-pipelined across items. Over the CTA's flat tile
+  // sequence 0..N-1 the 32-KB units are
+  //   K(0) 0, R_k(0) 1;  then per tile j >= 1:  K(j) 4j-2, V(j-1) 4j-1, R_k(j) 4j, R_v(j-1) 4j+1;  V(N-1) 4N-1,
+  //   R_v(N-1) 4N+1
+  // (unit u uses ring slot u % kNU). Each unit thereby reuses the slot of a unit consumed early enough: V(j) that of
+  // K(j) (free once S(j)'s base MMAs ran), R_v(j) that of R_k(j) (after S(j)), K(j+1) that of R_v(j-2) and R_k(j+1)
+  // that of V(j-1) (after PV(j-2), PV(j-1)), so the V side of a tile loads while its softmax runs. The units of
+  // one kind are at most 4 apart, so with kNU = 5 a producer never finds a slot's `empty` barrier two phases
+  // behind (parity aliasing: a per-item order with K units 6 apart did, once K and V had separate producers).
+  // f(kind, u, item, t, tile, n_tiles_of_item, next): kind 0 = K, 1 = V, 2 = R_k, 3 = R_v of tile t of the
+  // item-th item; `next` = the tile of this kind's next unit (-1 none, -2 not known yet). rel(item) is called once
+  // an item is no longer referenced.
+  auto walk = [&](auto&& f, auto&& rel) {
+    int id = ring_get(0);
+    if (id < 0) return;
+    int k = 0, t0 = __ldg(&p.items[id].tile0), n = __ldg(&p.items[id].n_tiles);
+    int pv_k = -1, pv_t = 0, pv_n = 0, pv_t0 = 0;  // the tile whose V side is pending
+    int j = 0;                                     // flat tile index
+    for (;;) {
+      int nid = -1, nt0 = -1, nn = 0;
+      for (int t = 0; t < n; ++t, ++j) {
+        int tn = t0 + t + 1;
+        if (t + 1 == n) {
+          // the next item may not be published yet: it is published after the epilogue of item k - 1, which
+          // waits for the V side emitted below, so only peek here (-2 = unknown: the producer then reads the
+          // next record itself) and block after the V side
+          tn = -2;
+          if (mbar_test(smem_u32(&B.ring_full[(k + 1) & 3]), ((k + 1) >> 2) & 1)) {
+            const int pid = *reinterpret_cast<volatile int*>(&B.ring_id[(k + 1) & 3]);
+            tn = pid >= 0 ? __ldg(&p.items[pid].tile0) : -1;
+          }
+        }
+        const uint32_t uk = j == 0 ? 0u : (uint32_t)(4 * j - 2), urk = j == 0 ? 1u : (uint32_t)(4 * j);
+        f(0, uk, k, t, t0 + t, n, tn);
+        if (pv_k >= 0) f(1, (uint32_t)(4 * j - 1), pv_k, pv_t, pv_t0 + pv_t, pv_n, t0 + t);
+        f(2, urk, k, t, t0 + t, n, tn);
+        if (pv_k >= 0) {
+          f(3, (uint32_t)(4 * j + 1), pv_k, pv_t, pv_t0 + pv_t, pv_n, t0 + t);
+          if (pv_t == pv_n - 1) rel(pv_k);
+        }
+        pv_k = k; pv_t = t; pv_n = n; pv_t0 = t0;
+        if (t + 1 == n) {
+          nid = ring_get(k + 1);
+          if (nid >= 0) {
+            nt0 = __ldg(&p.items[nid].tile0);
+            nn = __ldg(&p.items[nid].n_tiles);
+          }
+        }
+      }
+      if (nid < 0) break;
+      ++k;
+      t0 = nt0;
+      n = nn;
+    }
+    f(1, (uint32_t)(4 * j - 1), pv_k, pv_t, pv_t0 + pv_t, pv_n, -1);
+    f(3, (uint32_t)(4 * j + 1), pv_k, pv_t, pv_t0 + pv_t, pv_n, -1);
+    rel(pv_k);
+  };
+  // register budget per warpgroup (setmaxnreg at the top of each role): softmax 224, loaders / MMA 104, aux 176
+  // (x 128 threads = 64512 registers = the CTA allocation of 168 x 384: more would deadlock setmaxnreg.inc; a
+  // warpgroup going below the launch count of 168 must use .dec: .inc to a lower count is an illegal instruction).
   // Dependent grids (the combine kernel, or the next instance of this kernel) are released only after every
   // warpgroup has moved its registers (named barrier 1 below): registers freed by setmaxnreg.dec must not be
   // handed to a co-scheduled CTA of another grid before our setmaxnreg.inc claims them (observed on B200 as a
@@ -259,8 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = (uint32_t)(32 * wid) << 16;
     const int row = tid;
     int g = 0;
-    for (int io = 0; io < n_my; ++io) {
-      const RItem it = p.items[p.sched_items[p.sched_ptr[blockIdx.x] + io]];
+    for (int io = 0;; ++io) {
+      const int id = ring_get(io);
+      if (id < 0) break;
+      const RItem it = p.items[id];
       const RRow rr = p.rows[it.row0 + row];
       float m_run = -INFINITY, l = 0.f;
       RTile T = p.tiles[it.tile0];
@@ -273,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         wait_bar(smem_u32(&B.s_full[b]), (g >> 1) & 1);
         if (tid == 0) stamp(p, 4, g);
         tc_fence_after();
-        if (lw != 0u) {
+        if (lw != 0u && !(p.flags & 32)) {  // diagnostics: bit 5 skips the softmax work
           const bool active = (lw >> lane) & 1u;
           const uint32_t ts = tm + lane_base + 128u * b;
           uint32_t sr[128];
@@ -354,131 +405,184 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       B.ml[io & 1][row] = make_float2(m_run, l);
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&B.ml_full[io & 1]));
+      if (lane == 0) {
+        mbar_arrive(smem_u32(&B.ml_full[io & 1]));
+        ring_release(io);
+      }
     }
   } else if (wid < 8) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
     release_dependents();
     if (wid == 4) {
-      // ==================================== MMA issuer (one thread) ====================================
-      // Tile fields come from the tile record (n_keys, flags, n_slots, WU) read at the top of each step, before
-      // the barrier waits, so their latency overlaps the waits; the S step keeps the WU's output-lane mask for
-      // its PV step.
-      if (lane == 0) {
-        uint32_t u = 0;
-        int g = 0;   // S tiles issued
-        int gp = 0;  // PV tiles issued
-        const uint32_t qa = sb + OFF_Q;
-        uint4 pv_l0 = make_uint4(0, 0, 0, 0), pv_l1 = pv_l0;  // WU lanes of the S tiles by parity (registers)
-        walk(p, [&](int kind, int io, int t, int ti, int n_tiles, int) {
-          const RTile* Tp = p.tiles + ti;
-          const int n_keys = __ldg(&Tp->n_keys), wu = __ldg(&Tp->wu), n_slots = __ldg(&Tp->n_slots);
-          if (kind == 0) {
-            // ------------------------- S = Q K^T + q~ R_k^T (K tile unit, R_k unit) -------------------------
-            uint4 ml[kRowsMaxSlots];
-#pragma unroll
-            for (int sl = 0; sl < kRowsMaxSlots; ++sl)
-              ml[sl] = sl < n_slots ? __ldg(reinterpret_cast<const uint4*>(p.wus[wu].slot_lanes[sl]))
-                                    : make_uint4(0, 0, 0, 0);
-            {
-              const uint4 l = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].lanes));
-              if (g & 1) pv_l1 = l;
-              else pv_l0 = l;
-            }
-            if (t == 0) {
-              wait_bar(smem_u32(&B.q_full), io & 1);
-              stamp(p, 8, io);
-              fence_async_smem();  // Q rows arrive through cp.async (generic proxy)
-            }
-            const int ns = (n_keys + 15) & ~15;
-            const uint32_t idS = idesc_bf16(128, ns, false, false);
-            const uint32_t dS = tm + 128u * (g & 1);
-            const uint4 none = make_uint4(0, 0, 0, 0);
-            uint32_t s_ = u % kNU;
-            B.prog[4] = (int)u;
-            wait_bar(smem_u32(&B.full[s_]), (u / kNU) & 1);
-            stamp(p, 0, g);
-            tc_fence_after();
-            const uint32_t kb = sb + OFF_RING + s_ * kUnit;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              mma_ss_m(dS, make_desc(qa + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SWZ_128),
-                       make_desc(kb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SWZ_128), idS, k != 0, none);
-            mma_commit(smem_u32(&B.empty[s_]));
-            ++u;
-            if (t == 0) {
-              wait_bar(smem_u32(&B.qt_full[io & 1]), (io >> 1) & 1);
-              stamp(p, 9, io);
-              fence_async_smem();  // q~ written with st.shared by the aux warps
-            }
-            const uint32_t qt = sb + OFF_QT + 4096u * (io & 1);
-            s_ = u % kNU;
-            wait_bar(smem_u32(&B.full[s_]), (u / kNU) & 1);
-            tc_fence_after();
-            fence_async_smem();  // residual pages may land through cp.async (generic proxy)
-            const uint32_t rb = sb + OFF_RING + s_ * kUnit;
-#pragma unroll
-            for (int sl = 0; sl < kRowsMaxSlots; ++sl)
-              if (sl < n_slots)
-                mma_ss_m(dS, make_desc(qt, 16, 256, SWZ_32), make_desc(rb + 4096u * sl, 16, 256, SWZ_32), idS, 1u,
-                         make_uint4(~ml[sl].x, ~ml[sl].y, ~ml[sl].z, ~ml[sl].w));
-            mma_commit(smem_u32(&B.empty[s_]));
-            ++u;
-            mma_commit(smem_u32(&B.s_full[g & 1]));
-            stamp(p, 1, g);
-            if (t == n_tiles - 1) mma_commit(smem_u32(&B.q_empty));
-            ++g;
-          } else {
-            // ------------------------- O += P V ; A_r += P R_v (V tile unit, R_v unit) -------------------------
-            const int b = gp & 1;
-            const uint32_t acc0 = (__ldg(&Tp->flags) & kTileFirst) ? 0u : 1u;
-            const uint4 lw = b ? pv_l1 : pv_l0;
-            wait_bar(smem_u32(&B.p_full[b]), (gp >> 1) & 1);
-            stamp(p, 2, gp);
-            if (t == 0 && io > 0) wait_bar(smem_u32(&B.o_free), (io - 1) & 1);
-            const uint4 dis = make_uint4(~lw.x, ~lw.y, ~lw.z, ~lw.w);
-            const uint32_t idV = idesc_bf16(128, 128, false, true);
-            const uint32_t idR = idesc_bf16(128, 16 * n_slots, false, true);
-            const int nk = (n_keys + 15) >> 4;
-            const uint32_t pa = tm + 128u * b;
-            const uint32_t sv = u % kNU, sr_ = (u + 1) % kNU;
-            B.prog[4] = (int)u + 1000000;
-            wait_bar(smem_u32(&B.full[sv]), (u / kNU) & 1);
-            stamp(p, 13, gp);
-            wait_bar(smem_u32(&B.full[sr_]), ((u + 1) / kNU) & 1);
-            stamp(p, 14, gp);
-            tc_fence_after();
-            fence_async_smem();  // residual pages may land through cp.async (generic proxy)
-            const uint32_t vb = sb + OFF_RING + sv * kUnit, rvb = sb + OFF_RING + sr_ * kUnit;
-            for (int k = 0; k < nk; ++k) {
-              const uint32_t acc = k ? 1u : acc0;
-              const uint32_t a = pa + 8u * k;
-              mma_ts_m(tm + T_O, a, make_desc(vb + 2048u * k, 16384, 1024, SWZ_128), idV, acc, dis);
-              mma_ts_m(tm + T_AR, a, make_desc(rvb + 512u * k, 4096, 256, SWZ_32), idR, acc, dis);
-            }
-            mma_commit(smem_u32(&B.empty[sv]));
-            mma_commit(smem_u32(&B.empty[sr_]));
-            u += 2;
-            mma_commit(smem_u32(&B.o_done));
-            stamp(p, 3, gp);
-            if (t == n_tiles - 1) mma_commit(smem_u32(&B.o_final));
-            ++gp;
-          }
-        });
-      }
-    } else if (wid == 5 || wid == 7) {
-      // ======= K_base (warp 5) / V_base (warp 7) tiles: one TMA box {64 d, 128 keys, 2 d-halves} per tile (P = 128) =======
-      // (one issuing thread streams ~45 B/clk at most, tools/ub_fill.cu: K and V get a thread each). The next tile's
-      // record is read one step ahead (its latency overlaps this step's wait for a free ring slot).
+      // ============================ MMA issuer (whole warp, one elected lane issues) ============================
+      // Two streams over the CTA's flat tile sequence, issued in whichever order their inputs arrive:
+      //   S(k)  = Q K^T + q~ R_k^T        needs K(k), R_k(k) (and the item's Q / q~ images at its first tile);
+      //           S(k) may run at most one tile ahead of PV (S buffer k & 1 holds P(k-2) until PV(k-2) is issued);
+      //   PV(k) = O += P V, A_r += P R_v  needs softmax(k) done, V(k), R_v(k) (and the epilogue of the previous
+      //           item done at an item's first tile).
+      // A late K tile then no longer holds up a PV whose data is ready (and vice versa), so ring slots are freed
+      // as soon as their MMAs can run. Ring units of tile k (producer order, see walk): K at 2 * ck(k), R_k next;
+      // V at 2 * cv(k), R_v next, with ck(0) = 0, ck(k) = 2k - 1, cv(k) = 2k + 2, cv(N - 1) = 2N - 1.
       {
-        // lane 0 issues the TMA boxes; the whole warp runs the walk so that its 32 lanes can prefetch the page of
-        // the tile `p.prefetch` steps ahead into L2 (prefetch.global.L2 over the LSU path: the TMA engine's
-        // delivery rate is its outstanding bytes over the load latency, and L2 hits halve that latency)
-        const int my_kind = wid == 5 ? 0 : 1;
-        TileCursor pf;
-        if (p.prefetch > 0) pf.init(p, p.prefetch);
-        const uint8_t* plane = (const uint8_t*)(my_kind == 0 ? p.base_k : p.base_v);
-        uint32_t u = 0;
+        struct Cur {  // position in the CTA's flat tile sequence; its item comes from the ring (non-blocking)
+          int k = 0, id = 0, t = 0, n = 0, t0 = 0;
+          bool loaded = false;
+        };
+        auto try_load = [&](Cur& c) -> bool {
+          if (c.loaded) return true;
+          if (!mbar_test(smem_u32(&B.ring_full[c.k & 3]), (c.k >> 2) & 1)) return false;
+          c.id = *reinterpret_cast<volatile int*>(&B.ring_id[c.k & 3]);
+          c.loaded = true;
+          if (c.id >= 0) {
+            c.t0 = __ldg(&p.items[c.id].tile0);
+            c.n = __ldg(&p.items[c.id].n_tiles);
+          }
+          return true;
+        };
+        auto advance = [&](Cur& c) -> bool {  // true when c left its item
+          if (++c.t < c.n) return false;
+          c.t = 0;
+          ++c.k;
+          c.loaded = false;
+          return true;
+        };
+        Cur cs, cp;
+        int ks = 0, kp = 0;  // flat indices of the next S / PV tile
+        const uint32_t qa = sb + OFF_Q;
+        const uint4 none = make_uint4(0, 0, 0, 0);
+        // the next S tile's record, WU lanes and per-slot lane masks, loaded right after the previous S was issued
+        // (their global-load latency overlaps the wait for the tile's data); S(k) hands (n_keys, n_slots, flags,
+        // lanes) to PV(k) in registers by parity
+        int s_nk = 0, s_ns = 0, s_fl = 0;
+        uint4 s_l = none, s_ml[kRowsMaxSlots];
+        auto load_s = [&](const Cur& c) {
+          const RTile* Tp = p.tiles + c.t0 + c.t;
+          s_nk = __ldg(&Tp->n_keys);
+          s_ns = __ldg(&Tp->n_slots);
+          s_fl = __ldg(&Tp->flags);
+          const int wu = __ldg(&Tp->wu);
+          s_l = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].lanes));
+#pragma unroll
+          for (int sl = 0; sl < kRowsMaxSlots; ++sl)
+            s_ml[sl] = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].slot_lanes[sl]));
+        };
+        int pv_nk0 = 0, pv_nk1 = 0, pv_ns0 = 0, pv_ns1 = 0, pv_fl0 = 0, pv_fl1 = 0;
+        uint4 pv_l0 = none, pv_l1 = none;
+        bool s_rec = false;  // s_* hold the record of cs's tile
+        uint32_t spins = 0;
+        for (;;) {
+          if (try_load(cp) && cp.id < 0) break;  // PV stream done: every tile issued
+          bool did = false;
+          if (ks <= kp + 1 && try_load(cs) && cs.id >= 0) {
+            if (!s_rec) {
+              load_s(cs);
+              s_rec = true;
+            }
+            const uint32_t uk = ks == 0 ? 0u : (uint32_t)(4 * ks - 2), ur = ks == 0 ? 1u : (uint32_t)(4 * ks);
+            const bool first = cs.t == 0;
+            bool ready = mbar_test(smem_u32(&B.full[uk % kNU]), (uk / kNU) & 1) &&
+                         mbar_test(smem_u32(&B.full[ur % kNU]), (ur / kNU) & 1);
+            if (ready && first)
+              ready = mbar_test(smem_u32(&B.q_full), cs.k & 1) &&
+                      mbar_test(smem_u32(&B.qt_full[cs.k & 1]), (cs.k >> 1) & 1);
+            if (ready) {
+              // ------------------------- S = Q K^T + q~ R_k^T -------------------------
+              const int n_keys = s_nk, n_slots = s_ns;
+              if (ks & 1) { pv_l1 = s_l; pv_nk1 = s_nk; pv_ns1 = s_ns; pv_fl1 = s_fl; }
+              else { pv_l0 = s_l; pv_nk0 = s_nk; pv_ns0 = s_ns; pv_fl0 = s_fl; }
+              stamp(p, 0, ks);
+              if (first) stamp(p, 8, cs.k);
+              tc_fence_after();
+              // Q rows (cp.async) and q~ (st.shared) of a new item are generic-proxy writes; residual pages come by
+              // bulk copy (async proxy) unless FKV_ROWS_FLAGS bit 0 selects cp.async
+              if (first || (p.flags & 1)) fence_async_smem();
+              const int nsk = (n_keys + 15) & ~15;
+              const uint32_t idS = idesc_bf16(128, nsk, false, false);
+              const uint32_t dS = tm + 128u * (ks & 1);
+              const uint32_t kb = sb + OFF_RING + (uk % kNU) * kUnit;
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                mma_ss_me(dS, make_desc(qa + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SWZ_128),
+                         make_desc(kb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SWZ_128), idS, k != 0, none);
+              mma_commit_e(smem_u32(&B.empty[uk % kNU]));
+              *reinterpret_cast<volatile int*>(&B.issued[uk % kNU]) = (int)uk;
+              const uint32_t qt = sb + OFF_QT + 4096u * (cs.k & 1);
+              const uint32_t rb = sb + OFF_RING + (ur % kNU) * kUnit;
+              const int nsl = (p.flags & 8) ? 0 : n_slots;  // diagnostics: bit 3 skips the residual S MMAs
+#pragma unroll
+              for (int sl = 0; sl < kRowsMaxSlots; ++sl)
+                if (sl < nsl)
+                  mma_ss_me(dS, make_desc(qt, 16, 256, SWZ_32), make_desc(rb + 4096u * sl, 16, 256, SWZ_32), idS, 1u,
+                           make_uint4(~s_ml[sl].x, ~s_ml[sl].y, ~s_ml[sl].z, ~s_ml[sl].w));
+              mma_commit_e(smem_u32(&B.empty[ur % kNU]));
+              *reinterpret_cast<volatile int*>(&B.issued[ur % kNU]) = (int)ur;
+              mma_commit_e(smem_u32(&B.s_full[ks & 1]));
+              stamp(p, 1, ks);
+              if (cs.t == cs.n - 1) mma_commit_e(smem_u32(&B.q_empty));
+              ++ks;
+              advance(cs);
+              s_rec = false;
+              if (try_load(cs) && cs.id >= 0) {
+                load_s(cs);  // the next S tile's record: its latency overlaps the wait for its data
+                s_rec = true;
+              }
+              did = true;
+            }
+          }
+          if (!did && kp < ks) {
+            const uint32_t uv = (uint32_t)(4 * kp + 3), urv = (uint32_t)(4 * kp + 5);
+            const int b = kp & 1;
+            bool ready = mbar_test(smem_u32(&B.p_full[b]), (kp >> 1) & 1) &&
+                         mbar_test(smem_u32(&B.full[uv % kNU]), (uv / kNU) & 1) &&
+                         mbar_test(smem_u32(&B.full[urv % kNU]), (urv / kNU) & 1);
+            if (ready && cp.t == 0 && cp.k > 0) ready = mbar_test(smem_u32(&B.o_free), (cp.k - 1) & 1);
+            if (ready) {
+              // ------------------------- O += P V ; A_r += P R_v -------------------------
+              const int n_keys = b ? pv_nk1 : pv_nk0, n_slots = b ? pv_ns1 : pv_ns0;
+              const uint32_t acc0 = ((b ? pv_fl1 : pv_fl0) & kTileFirst) ? 0u : 1u;
+              const uint4 lw = b ? pv_l1 : pv_l0;
+              stamp(p, 2, kp);
+              tc_fence_after();
+              if (p.flags & 1) fence_async_smem();  // residual pages by cp.async (diagnostics)
+              const uint4 dis = make_uint4(~lw.x, ~lw.y, ~lw.z, ~lw.w);
+              const uint32_t idV = idesc_bf16(128, 128, false, true);
+              const uint32_t idR = idesc_bf16(128, 16 * n_slots, false, true);
+              const int nk = (n_keys + 15) >> 4;
+              const uint32_t pa = tm + 128u * b;
+              const uint32_t vb = sb + OFF_RING + (uv % kNU) * kUnit, rvb = sb + OFF_RING + (urv % kNU) * kUnit;
+              for (int k = 0; k < nk; ++k) {
+                const uint32_t acc = k ? 1u : acc0;
+                const uint32_t a = pa + 8u * k;
+                mma_ts_me(tm + T_O, a, make_desc(vb + 2048u * k, 16384, 1024, SWZ_128), idV, acc, dis);
+                if (!(p.flags & 16))  // diagnostics: bit 4 skips the R_v MMAs
+                  mma_ts_me(tm + T_AR, a, make_desc(rvb + 512u * k, 4096, 256, SWZ_32), idR, acc, dis);
+              }
+              mma_commit_e(smem_u32(&B.empty[uv % kNU]));
+              mma_commit_e(smem_u32(&B.empty[urv % kNU]));
+              *reinterpret_cast<volatile int*>(&B.issued[uv % kNU]) = (int)uv;
+              *reinterpret_cast<volatile int*>(&B.issued[urv % kNU]) = (int)urv;
+              mma_commit_e(smem_u32(&B.o_done));
+              stamp(p, 3, kp);
+              if (cp.t == cp.n - 1) mma_commit_e(smem_u32(&B.o_final));
+              ++kp;
+              const int kprev = cp.k;
+              if (advance(cp) && lane == 0) ring_release(kprev);
+              did = true;
+            }
+          }
+          if (!did) {
+            B.prog[4] = ks * 1000 + kp;
+            if (++spins == (1u << 28) && p.hang != nullptr) hang_trap(0, ks * 1000 + kp, p.hang, __LINE__);
+          }
+        }
+      }
+    } else if (wid == 5) {
+      // ======= K_base (lane 0) and V_base (lane 1) tiles: one TMA box {64 d, 128 keys, 2 d-halves} per tile =======
+      // (P = 128; per-page 2D boxes otherwise). Each lane runs its own walk over its kind's units (one issuing thread
+      // streams ~45 B/clk at most, tools/ub_fill.cu: K and V get a thread each); the next tile's record is read one
+      // step ahead (its latency overlaps the wait for a free ring slot).
+      if (lane < 2) {
+        const int my_kind = lane;  // 0 = K, 1 = V
         int kt = 0;
         const int P = p.P;
         const int ppt = 128 / P;  // pages per tile
@@ -486,11 +590,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap* m2 = my_kind == 0 ? &maps.k2d : &maps.v2d;
         int c_pg = -1, c_h = 0, c_nk = 0, c_bo = 0;
         bool have = false;
-        walk(p, [&](int kind, int, int, int ti, int, int tn) {
-          if (kind != my_kind) {
-            u += 2;
-            return;
-          }
+        walk([&](int kind, uint32_t u, int, int, int ti, int, int tn) {
+          if (kind != my_kind) return;
           if (!have) {
             const RTile* T0 = p.tiles + ti;
             c_pg = __ldg(&T0->base_page); c_h = __ldg(&T0->kv_head); c_nk = __ldg(&T0->n_keys);
@@ -502,29 +603,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             n_pg = __ldg(&Tn->base_page); n_h = __ldg(&Tn->kv_head); n_nk = __ldg(&Tn->n_keys);
             n_bo = __ldg(&Tn->base_off);
           }
-          if (p.prefetch > 0 && P == 128) {
-            const int tf = pf.next(p);
-            if (tf >= 0) {
-              const RTile* Tf = p.tiles + tf;
-              const int fpg = __ldg(&Tf->base_page), fh = __ldg(&Tf->kv_head);
-              if (fpg >= 0) {
-                const uint8_t* src =
-                    plane + ((size_t)p.base_rows_layer + (size_t)fpg * p.hkv * P + (size_t)fh * P) * 256;
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                  asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 128 * (lane + 32 * j)));
-              }
-            }
-          }
           const int64_t hrow = (int64_t)c_h * P;
           const uint32_t s_ = u % kNU;
-          if (lane == 0) B.prog[wid] = (int)u;
-          wait_bar(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
-          if (my_kind == 0 && lane == 0) stamp(p, 6, kt++);
+          B.prog[5 + my_kind] = (int)u;
+          slot_wait_free(u);
+          stamp(p, my_kind == 0 ? 6 : 15, kt);
           const uint32_t dst = sb + OFF_RING + s_ * kUnit;
-          if (lane != 0) {
-            // lanes 1..31 only prefetch
-          } else if (P == 128) {
+          if (P == 128) {
             mbar_expect_tx(smem_u32(&B.full[s_]), c_pg >= 0 ? 32768u : 0u);
             if (c_pg >= 0)
               tma_load_3d(dst, m3, 0, (int)(p.base_rows_layer + (int64_t)c_pg * p.hkv * P + hrow), 0,
@@ -541,73 +626,54 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_2d(dst + 16384 + pi * P * 128, m2, 64, r0, smem_u32(&B.full[s_]));
             }
           }
-          if (lane == 0) B.prog[wid + 4] = (int)u;
-          u += 2;
+          B.prog[9 + my_kind] = (int)u;
+          ++kt;
           c_pg = n_pg; c_h = n_h; c_nk = n_nk; c_bo = n_bo;
-          have = true;
-        });
+          have = tn != -2;
+        }, [&](int k) { ring_release(k); });
       }
     } else {
-      // ====== residual pages (warp 6: R_k and R_v): one bulk copy per (slot, page), lanes in parallel ======
-      // lane s owns slot s (P = 128: one page per slot and tile; records read one step ahead). R_k of tile k+1
-      // and R_v of tile k alternate in the walk; both use the same residual pages (the two planes share the page
-      // table), so the R_k step keeps its page for the tile's R_v step.
-      uint32_t u = 0;
+      // ====== residual pages: warp 6 R_k, warp 7 R_v; one bulk copy per (slot, page), lanes in parallel ======
+      // lane s owns slot s (P = 128: one page per slot and tile; the next tile's record is read one step ahead)
+      const int my_kind = wid == 6 ? 2 : 3;
       const int P = p.P;
       const int ppt = 128 / P;  // pages per slot and tile (<= 8)
-      const uint8_t* rpk = (const uint8_t*)p.res_k + (size_t)p.layer * p.res_layer_elems * 2;
-      const uint8_t* rpv = (const uint8_t*)p.res_v + (size_t)p.layer * p.res_layer_elems * 2;
-      int c_pg = -1, c_nk = 0, c_ns = 0;      // the next R_k step's tile (prefetched)
-      int v0_pg = -1, v0_nk = 0, v0_ns = 0, v1_pg = -1, v1_nk = 0, v1_ns = 0;  // pending R_v tiles (by parity)
-      int kstep = 0, vstep = 0;
+      const uint8_t* rp = (const uint8_t*)(my_kind == 3 ? p.res_v : p.res_k) + (size_t)p.layer * p.res_layer_elems * 2;
+      int c_pg = -1, c_nk = 0, c_ns = 0;
       bool have = false;
+      int kt = 0;
       auto rec = [&](int ti, int& pg, int& nk, int& ns) {
         const RTile* T0 = p.tiles + ti;
         nk = __ldg(&T0->n_keys);
         ns = __ldg(&T0->n_slots);
         pg = (P == 128 && lane < ns) ? p.res_pages[__ldg(&T0->res_off[lane])] : -1;
       };
-      TileCursor pf;
-      if (p.prefetch > 0) pf.init(p, p.prefetch);
-      walk(p, [&](int kind, int, int, int ti, int, int tn) {
-        const bool is_rv = kind == 1;
-        int pg, nk, ns;
-        if (!is_rv && p.prefetch > 0 && P == 128) {
-          // residual pages (both planes) of the tile `prefetch` steps ahead into L2: lane = (slot, plane, quarter)
-          const int tf = pf.next(p);
-          if (tf >= 0) {
-            const RTile* Tf = p.tiles + tf;
-            const int sl = lane >> 2, pl = (lane >> 1) & 1, hf = lane & 1;
-            if (sl < __ldg(&Tf->n_slots)) {
-              const int fpg = p.res_pages[__ldg(&Tf->res_off[sl])];
-              if (fpg >= 0) {
-                const uint8_t* src = (pl ? rpv : rpk) + (size_t)fpg * 4096 + 2048 * hf;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + 128 * j));
-              }
-            }
-          }
-        }
-        if (!is_rv) {
-          if (!have) rec(ti, c_pg, c_nk, c_ns);
-          pg = c_pg; nk = c_nk; ns = c_ns;
-          if (kstep & 1) { v1_pg = pg; v1_nk = nk; v1_ns = ns; }
-          else { v0_pg = pg; v0_nk = nk; v0_ns = ns; }
-          ++kstep;
-          if (tn >= 0) rec(tn, c_pg, c_nk, c_ns);
-          have = true;
-        } else {
-          if (vstep & 1) { pg = v1_pg; nk = v1_nk; ns = v1_ns; }
-          else { pg = v0_pg; nk = v0_nk; ns = v0_ns; }
-          ++vstep;
-        }
-        const uint8_t* rp = is_rv ? rpv : rpk;
+      walk([&](int kind, uint32_t u, int, int, int ti, int, int tn) {
+        if (kind != my_kind) return;
+        if (!have) rec(ti, c_pg, c_nk, c_ns);
+        const int pg = c_pg, nk = c_nk, ns = c_ns;
+        if (tn >= 0) rec(tn, c_pg, c_nk, c_ns);
+        have = tn >= 0;  // -2: the next item is not known yet, -1: none
         const RTile* Tp = p.tiles + ti;
-        const uint32_t s_ = (u + 1) % kNU;
-        if (lane == 0) B.prog[6] = (int)u + 1;
-        wait_bar(smem_u32(&B.empty[s_]), (((u + 1) / kNU) & 1) ^ 1);
+        const uint32_t s_ = u % kNU;
+        if (lane == 0) B.prog[my_kind == 2 ? 7 : 8] = (int)u;
+        slot_wait_free(u);
+        if (lane == 0) stamp(p, my_kind == 2 ? 18 : 20, kt);
         const uint32_t dst = sb + OFF_RING + s_ * kUnit;
-        if (P == 128) {
+        if (P == 128 && (p.flags & 1)) {
+          // 16-byte cp.async by all lanes (LSU path, per-lane addresses: no uniform-operand waterfall); completion
+          // through cp.async.mbarrier.arrive (pending +1 per lane) and one plain arrive
+          for (int sl = 0; sl < ns; ++sl) {
+            const int pgs = __shfl_sync(0xffffffffu, pg, sl);
+            if (pgs < 0) continue;
+            const uint8_t* src = rp + (size_t)pgs * 4096;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) cp_async16(dst + 4096u * sl + 16u * (lane + 32 * c), src + 16 * (lane + 32 * c));
+          }
+          cp_async_arrive_inc(smem_u32(&B.full[s_]));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&B.full[s_]));
+        } else if (P == 128) {
           const int mine = pg >= 0 ? 4096 : 0;
           int tot = mine;
 #pragma unroll
@@ -636,22 +702,33 @@ __global__ void __launch_bounds__(kThreads, 1)
               bulk_g2s(dst + 4096u * sl + pi * P * 32, rp + (size_t)pgq * P * 32, P * 32, smem_u32(&B.full[s_]));
           }
         }
-        if (lane == 0) B.prog[10] = (int)u + 1;
-        u += 2;
+        if (lane == 0) B.prog[my_kind == 2 ? 11 : 12] = (int)u;
+        ++kt;
+      }, [&](int k) {
+        if (lane == 0) ring_release(k);
       });
     }
   } else {
     // ======================= aux warpgroup: q~, Q image, epilogue (thread = row = TMEM lane) =======================
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 184;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 176;\n" ::: "memory");
     release_dependents();
     const int row = tid - 256;
     const uint32_t lane_base = (uint32_t)(32 * (wid - 8)) << 16;
-    const int i0 = p.sched_ptr[blockIdx.x];
     const __nv_bfloat16* Qg = (const __nv_bfloat16*)p.Q;
+    // the queue's producer (one thread): take the next item from the global queue and publish it as ring entry k
+    auto push = [&](int k) {
+      if (row == 0) {
+        const int q = atomicAdd(p.ctr, 1);
+        const int id = q < p.n_items ? __ldg(&p.sched_items[q]) : -1;
+        wait_bar(smem_u32(&B.ring_empty[k & 3]), ((k >> 2) & 1) ^ 1);
+        *reinterpret_cast<volatile int*>(&B.ring_id[k & 3]) = id;
+        mbar_arrive(smem_u32(&B.ring_full[k & 3]));  // release: the id store is visible to the waiters
+      }
+    };
     // q~ = Q B_k^h^T (bf16, fp32 accumulate) of item `io` into q~ image io & 1 with warp-level MMA
     // (m16n8k16): the 16 rows of an m16 tile are computed once per distinct (adapter, kv head) among them
-    auto qtilde = [&](int io) {
-      const RItem it = p.items[p.sched_items[i0 + io]];
+    auto qtilde = [&](int io, int id) {
+      const RItem it = p.items[id];
       const uint32_t qtb = sb + OFF_QT + 4096u * (io & 1);
       const int gq = lane >> 2, tq = lane & 3;
       for (int mt = 0; mt < 2; ++mt) {
@@ -722,8 +799,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (row == 0) stamp(p, 10, io);
     };
     // Q rows of item `io` into the (single) Q image, SW128 K-major [d-half][row][128 B]
-    auto qimage = [&](int io) {
-      const RItem it = p.items[p.sched_items[i0 + io]];
+    auto qimage = [&](int id) {
+      const RItem it = p.items[id];
       const int qr = p.rows[it.row0 + row].q_row;
       if (qr >= 0) {
         const uint8_t* src = (const uint8_t*)(Qg + (size_t)qr * 128);
@@ -735,19 +812,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&B.q_full));
     };
-    if (n_my > 0) {
-      qimage(0);
-      qtilde(0);
+    push(0);
+    int id = ring_get(0);
+    int n_done = 0;
+    if (id >= 0) {
+      qimage(id);
+      qtilde(0, id);
     }
-    for (int io = 0; io < n_my; ++io) {
-      if (io + 1 < n_my) {
-        qtilde(io + 1);  // its image buffer was freed by the last S of item io - 1 (waited in the last iteration)
+    for (int io = 0; id >= 0; ++io) {
+      push(io + 1);
+      const int nid = ring_get(io + 1);
+      if (nid >= 0) {
+        qtilde(io + 1, nid);  // its image buffer was freed by the last S of item io - 1 (waited in the last iteration)
         wait_bar(smem_u32(&B.q_empty), io & 1);
-        qimage(io + 1);
+        qimage(nid);
       }
       // epilogue of item io
-      if (row == 0) B.prog[8] = io;
-      const RItem it = p.items[p.sched_items[i0 + io]];
+      if (row == 0) B.prog[13] = io;
+      const RItem it = p.items[id];
       const RRow rr = p.rows[it.row0 + row];
       wait_bar(smem_u32(&B.ml_full[io & 1]), (io >> 1) & 1);
       wait_bar(smem_u32(&B.o_final), io & 1);
@@ -755,46 +837,81 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       float* e = rr.entry >= 0 ? p.ws + (size_t)rr.entry * p.entry_stride : nullptr;
       const float2 ml = B.ml[io & 1][row];
-#pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        uint32_t o[32];
-        FKV_TMEM_LD32(tm + lane_base + T_O + c0, o);
-        tmem_ld_wait();
-        if (e) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *(float4*)(e + kEntAcc + c0 + j) = make_float4(__uint_as_float(o[j]), __uint_as_float(o[j + 1]),
-                                                           __uint_as_float(o[j + 2]), __uint_as_float(o[j + 3]));
-        }
-      }
+      // O and the row's slot of A_r into registers (all loads in flight together), hand the accumulators back
+      // to the next item's PV (o_free) and only then store the partial entry: the stores no longer delay it
+      uint32_t o[128], ar[16];
+      FKV_TMEM_LD32(tm + lane_base + T_O + 0, (o + 0));
+      FKV_TMEM_LD32(tm + lane_base + T_O + 32, (o + 32));
+      FKV_TMEM_LD32(tm + lane_base + T_O + 64, (o + 64));
+      FKV_TMEM_LD32(tm + lane_base + T_O + 96, (o + 96));
       const int slot = rr.meta & 0xff;
       for (int s = 0; s < kRowsMaxSlots; ++s) {
         if (!__any_sync(0xffffffffu, rr.q_row >= 0 && slot == s)) continue;
-        uint32_t o[16];
-        FKV_TMEM_LD16(tm + lane_base + T_AR + 16 * s, o);
+        uint32_t t16[16];
+        FKV_TMEM_LD16(tm + lane_base + T_AR + 16 * s, t16);
         tmem_ld_wait();
-        if (e && slot == s) {
+        if (slot == s) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *(float4*)(e + kEntAcc + 128 + j) = make_float4(__uint_as_float(o[j]), __uint_as_float(o[j + 1]),
-                                                            __uint_as_float(o[j + 2]), __uint_as_float(o[j + 3]));
+          for (int j = 0; j < 16; ++j) ar[j] = t16[j];
         }
       }
-      if (e) *(float2*)e = ml;
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&B.o_free));
+      // entry = [m, l, pad x 6, acc[128], acc_r[16]] (kEntAcc = 8): staged 8 rows at a time, then each row is
+      // written by the whole warp (5 x 128-byte coalesced stores)
+      float* stg = reinterpret_cast<float*>(smem + OFF_EPI) + (wid - 8) * kEpiRows * kEpiStride;
+      for (int r0 = 0; r0 < 32; r0 += kEpiRows) {
+        if (lane >= r0 && lane < r0 + kEpiRows) {
+          float* d = stg + (lane - r0) * kEpiStride;
+          d[0] = ml.x;
+          d[1] = ml.y;
+#pragma unroll
+          for (int j = 0; j < 6; ++j) d[2 + j] = 0.f;
+#pragma unroll
+          for (int j = 0; j < 128; ++j) d[kEntAcc + j] = __uint_as_float(o[j]);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) d[kEntAcc + 128 + j] = __uint_as_float(ar[j]);
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int q = 0; q < kEpiRows; ++q) {
+          const int ent = __shfl_sync(0xffffffffu, rr.entry, r0 + q);
+          if (ent >= 0) {
+            float* g = p.ws + (size_t)ent * p.entry_stride;
+            const float* sr = stg + q * kEpiStride;
+#pragma unroll
+            for (int c = 0; c < 5; ++c)
+              if (lane + 32 * c < kEntAcc + 128 + 16) g[lane + 32 * c] = sr[lane + 32 * c];
+          }
+        }
+        __syncwarp();
+      }
+      (void)e;
       if (row == 0) stamp(p, 12, io);
+      ++n_done;
+      id = nid;
     }
+    if (row == 0) B.prog[15] = n_done;
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (wid == 4) tmem_dealloc(tm, 512);
+  if (tid == 0) {
+    // the last CTA to finish resets the queue counters for the next launch over the same workspace
+    __threadfence();
+    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
+      p.ctr[0] = 0;
+      p.ctr[1] = 0;
+      __threadfence();
+    }
+  }
   if (kDbg && tid == 0 && blockIdx.x < 512) {
     p.dbg[30 * 512 + blockIdx.x] = clock64() - t_start;
-    p.dbg[31 * 512 + blockIdx.x] = n_my;
+    p.dbg[31 * 512 + blockIdx.x] = B.prog[15];
   }
 }
 

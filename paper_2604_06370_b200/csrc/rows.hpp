@@ -67,8 +67,10 @@ struct RowsParams {
   const int32_t* base_pages;
   const int32_t* res_pages;
   const int64_t* adapters;     // [adapter slot][2]: B_K, B_V device pointers (layer 0)
-  const int32_t* sched_ptr;    // CTA c runs items sched_items[sched_ptr[c] .. sched_ptr[c + 1])
-  const int32_t* sched_items;
+  const int32_t* sched_ptr;    // (unused by the dynamic schedule)
+  const int32_t* sched_items;  // the item queue in the planner's order (cost-descending, locality)
+  int32_t* ctr;                // workspace: [0] next queue position, [1] finished CTAs (zero between launches)
+  int32_t n_items;
   int64_t base_rows_layer;     // TMA row index of (layer, page 0, head 0, key 0) = layer * nb * hkv * P
   int64_t res_layer_elems;     // elements per layer of a residual pool (= nr * P * r)
   int64_t adapter_layer_elems; // elements per layer of B_K / B_V (= hkv_local * r * d)

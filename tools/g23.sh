@@ -1,0 +1,4 @@
+mkdir -p gpurun_out/g23
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q --timeout 120 -k "c1_parity or page_sizes or random_suite" > gpurun_out/g23/pytest_quick.txt 2>&1
+for f in 0.15 0.08 0.3; do FKV_PIECE_FRAC=$f timeout 120 python tools/timeline_rows.py --tiles 8 > gpurun_out/g23/tl_$f.txt 2>&1; done
+FKV_HANG_DIAG=1 timeout 150 python tools/repro_bench.py 32 4 nosync > gpurun_out/g23/nosync.txt 2>&1

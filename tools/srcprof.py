@@ -33,7 +33,7 @@ for f in os.listdir(tmp):
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?)\s*;", ln)
         if m and cur_fun and ksub in cur_fun:
             line_of[int(m.group(1), 16)] = (cur_line, m.group(2))
-csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", "regex:" + "ra_tc"],
+csvtxt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", "regex:" + os.environ.get("KREGEX", "ra_tc")],
                         capture_output=True, text=True).stdout
 rows = list(csv.reader(csvtxt.splitlines()))
 kern = None

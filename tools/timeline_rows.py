@@ -12,9 +12,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-EV = {0: "S:Kfull", 1: "S:commit", 2: "PV:pfull", 3: "PV:commit", 4: "W0:sfull", 5: "W0:pfull", 6: "LD:K0empty",
-      13: "PV:V0full", 14: "PV:RV0full", 15: "RV:empty", 16: "RV:issued"}
-COLS = [0, 1, 4, 5, 2, 13, 14, 3, 6, 15, 16]
+EV = {0: "S:start", 1: "S:commit", 2: "PV:start", 3: "PV:commit", 4: "W0:sfull", 5: "W0:pfull", 6: "K:issue",
+      16: "K:landed", 15: "V:issue", 17: "V:landed", 18: "Rk:issue", 19: "Rk:landed", 20: "Rv:issue", 21: "Rv:landed"}
+COLS = [6, 16, 18, 19, 0, 1, 4, 5, 15, 17, 20, 21, 2, 3]
 
 
 def main():
@@ -59,7 +59,7 @@ def main():
     torch.cuda.synchronize()
     lib.fkv_debug_timeline(fkv.ctx, None, 0)
     d = dbg.view(32, 512).cpu().numpy()
-    ev = d[:17]
+    ev = d[:22]
     t0 = ev[ev > 0].min()
     rel = lambda e, i: int(d[e, i] - t0) if d[e, i] else -1
     print("tile  " + " ".join(f"{EV[e]:>10s}" for e in COLS))

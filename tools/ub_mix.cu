@@ -130,6 +130,32 @@ __global__ void __launch_bounds__(256, 1) run(int n_tiles, int bg, const uint8_t
     for (int s = 0; s < 2; ++s) mbar_wait(smem_u32(&bgbar[(i + s) & 1]), ph[(i + s) & 1]);
     out[blockIdx.x * 4 + 2] = bytes;
     out[blockIdx.x * 4 + 3] = clock64() - t0;
+  } else if (wid >= 2 && (bg & 8)) {
+    // mbarrier spinners: 6 warps polling a barrier phase that completes only at the end (like the kernel's waiting
+    // roles); bit 16 of bg: back off with nanosleep between polls
+    __shared__ __align__(8) uint64_t never;
+    if (threadIdx.x == 64) { mbar_init(smem_u32(&never), 1); fence_mbar_init(); }
+    __syncwarp();
+    uint32_t ok = 0;
+    while (!stop) {
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                   : "=r"(ok) : "r"(smem_u32(&never)), "r"(0u) : "memory");
+      if (bg & 16) __nanosleep(64);
+    }
+    if (ok == 7) out[0] = 1;
+  } else if (wid >= 4 && (bg & 4)) {
+    // softmax-like ALU / MUFU load on every SMSP (warps 4-7), no TMEM traffic
+    float a = threadIdx.x * 1e-3f, b2 = 0.f;
+    while (!stop) {
+#pragma unroll 16
+      for (int i = 0; i < 64; ++i) {
+        float y;
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(a));
+        b2 = fmaf(y, 0.999f, b2);
+        a = fmaf(a, 1.0001f, 1e-7f);
+      }
+    }
+    if (b2 == 12345.f) out[0] = 1;
   } else if (wid >= 4 && (bg & 2)) {
     const uint32_t lb = (uint32_t)(32 * (wid - 4)) << 16;
     while (!stop) {
@@ -179,7 +205,7 @@ int main() {
   uint8_t* g;
   cudaMalloc(&g, 8 << 20);
   cudaMemset(g, 1, 8 << 20);
-  for (int bg : {0, 1, 2, 3}) {
+  for (int bg : {0, 8, 24}) {
     go<0>(bg, g, "cur: S8+R8 N128 SS, PV 8x(TS128 SW128+SW32)", 128);
     go<1>(bg, g, "N256: S8+R8 SS, PV 16 TS MN-SW32", 256);
     go<2>(bg, g, "N256: S8+R8 SS, PV 16 TS MN-SW128", 256);
