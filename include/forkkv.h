@@ -73,6 +73,7 @@ enum { FKV_KIND_BASE = 0, FKV_KIND_RES = 1 };
 #define FKV_PLAN_CHECK_WRITTEN 1u   /* verify every key row of every layer was written */
 #define FKV_PLAN_FORCE_SIMT 2u      /* use the plain SIMT kernel (fp32 path is always SIMT) */
 #define FKV_PLAN_FORCE_MMA 4u       /* use the warp-level mma.sync kernel instead of tcgen05 */
+#define FKV_PLAN_ROWS_KERNEL 8u     /* NONE mode, bf16, d 128, r 16: the rows-on-lanes tcgen05 kernel (kernel 3) */
 
 typedef struct fkv_config {
   int32_t n_layers;       /* L */

@@ -35,6 +35,7 @@ WRITE_ALL = 15
 PLAN_CHECK_WRITTEN = 1
 PLAN_FORCE_SIMT = 2
 PLAN_FORCE_MMA = 4
+PLAN_ROWS_KERNEL = 8
 
 
 class fkv_config(ctypes.Structure):

@@ -59,11 +59,17 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
   // the mma.sync kernel (warp-level, pre-Blackwell instruction set) is kept only as a comparison baseline: it runs
   // when FKV_PLAN_FORCE_MMA asks for it, never by automatic selection (shapes the tcgen05 kernels do not take run
   // on the SIMT kernel)
-  pl.kernel = rows_ok ? 3 : (tc_ok ? 2 : ((mma_ok && (flags & FKV_PLAN_FORCE_MMA)) ? 0 : 1));
+  // default: the keys-on-lanes tcgen05 kernel (kernel 2, both RoPE modes: 108 us per C2 layer in NONE mode). The
+  // rows-on-lanes kernel (kernel 3) is selected by FKV_PLAN_ROWS_KERNEL / FKV_KERNEL=3: its load pipeline does not
+  // beat kernel 2 yet
+  pl.kernel = tc_ok ? 2 : ((mma_ok && (flags & FKV_PLAN_FORCE_MMA)) ? 0 : 1);
+  bool want_rows = flags & FKV_PLAN_ROWS_KERNEL;
   if (const char* kenv = getenv("FKV_KERNEL")) {
     const int kk = atoi(kenv);
     if (kk == 2 && tc_ok) pl.kernel = 2;
+    if (kk == 3) want_rows = true;
   }
+  if (want_rows && rows_ok) pl.kernel = 3;
   // tcgen05: 64 query rows per CTA. NONE also has a 128-row variant (FKV_TC_ROWS=128): every MMA instruction then
   // covers N = 128 rows (a tcgen05.mma costs ~120 cycles for any N <= 128, tools/ubench_mma.cu), but its key warps
   // (64 columns each, SIMT row sums, single P^T buffer) are the bottleneck today, so it is not the default;

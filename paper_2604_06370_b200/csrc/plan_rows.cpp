@@ -253,6 +253,7 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
         entry_qrow.push_back(rc.q_row);
         rw.lanes[lane >> 5] |= 1u << (lane & 31);
         rw.slot_lanes[rc.slot][lane >> 5] |= 1u << (lane & 31);
+        (rc.slot < 4 ? rw.lanes_lo : rw.lanes_hi)[lane >> 5] |= 1u << (lane & 31);
         min_pos = std::min<int64_t>(min_pos, rc.pos);
         ++lane;
       }

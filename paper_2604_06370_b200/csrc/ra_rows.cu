@@ -41,11 +41,13 @@ namespace k {
 namespace {
 using namespace sm100;
 
-constexpr int kNU = 5;  // ring slots
+constexpr int kNU = 6;  // ring slots
 constexpr uint32_t kUnit = 32768;
-constexpr uint32_t OFF_Q = 0, OFF_QT = 32768, OFF_RING = 40960;
+constexpr uint32_t OFF_QT = 0, OFF_RING = 8192;  // q~ images 2 x 4 KB; the item's Q rows live in TMEM
 constexpr uint32_t OFF_BAR = OFF_RING + kNU * kUnit;
-constexpr uint32_t T_O = 256, T_AR = 384;
+// TMEM columns: S/P buffers [0, 256), O [256, 384), A_r [384, 448) (slot s at 16 (s % 4): slots 0-3 and 4-7 share
+// the columns through two lane-masked MMAs), Q of the current item [448, 512) (bf16 pairs, the A operand of S)
+constexpr uint32_t T_O = 256, T_AR = 384, T_Q = 448;
 constexpr int kThreads = 384;
 constexpr int kRingConsumers = 9;  // item-queue readers: 4 softmax warps, MMA issuer, K, V, R_k, R_v loaders
 
@@ -231,48 +233,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     wait_bar(smem_u32(&B.empty[s_]), ((u / kNU) & 1) ^ 1);
   };
-  // Walk the CTA's ring units in producer order, software-pipelined across items. Over the CTA's flat tile
-  // sequence 0..N-1 the 32-KB units are
-  //   K(0) 0, R_k(0) 1;  then per tile j >= 1:  K(j) 4j-2, V(j-1) 4j-1, R_k(j) 4j, R_v(j-1) 4j+1;  V(N-1) 4N-1,
-  //   R_v(N-1) 4N+1
-  // (unit u uses ring slot u % kNU). Each unit thereby reuses the slot of a unit consumed early enough: V(j) that of
-  // K(j) (free once S(j)'s base MMAs ran), R_v(j) that of R_k(j) (after S(j)), K(j+1) that of R_v(j-2) and R_k(j+1)
-  // that of V(j-1) (after PV(j-2), PV(j-1)), so the V side of a tile loads while its softmax runs. The units of
-  // one kind are at most 4 apart, so with kNU = 5 a producer never finds a slot's `empty` barrier two phases
-  // behind (parity aliasing: a per-item order with K units 6 apart did, once K and V had separate producers).
+  // Walk the CTA's ring units in producer order. Over the CTA's flat tile sequence j = 0..N-1 (all items) the
+  // 32-KB units of tile j are K 4j, R_k 4j+1, V 4j+2, R_v 4j+3 (unit u uses ring slot u % kNU). With kNU = 6 every
+  // unit reuses the slot of a unit consumed more than a tile earlier: K(j) and R_k(j) those of V(j-2) and R_v(j-2),
+  // V(j) and R_v(j) those of K(j-1) and R_k(j-1), so both halves of a tile load while the previous tile computes
+  // (the MMA issuer consumes the S and PV streams out of order; `slot_wait_free` keeps the slot parity unambiguous).
   // f(kind, u, item, t, tile, n_tiles_of_item, next): kind 0 = K, 1 = V, 2 = R_k, 3 = R_v of tile t of the
-  // item-th item; `next` = the tile of this kind's next unit (-1 none, -2 not known yet). rel(item) is called once
-  // an item is no longer referenced.
+  // item-th item; `next` = the next tile (-1 none, -2 not known yet). rel(item) once an item is no longer
+  // referenced.
   auto walk = [&](auto&& f, auto&& rel) {
     int id = ring_get(0);
     if (id < 0) return;
     int k = 0, t0 = __ldg(&p.items[id].tile0), n = __ldg(&p.items[id].n_tiles);
-    int pv_k = -1, pv_t = 0, pv_n = 0, pv_t0 = 0;  // the tile whose V side is pending
-    int j = 0;                                     // flat tile index
+    int j = 0;  // flat tile index
     for (;;) {
       int nid = -1, nt0 = -1, nn = 0;
       for (int t = 0; t < n; ++t, ++j) {
         int tn = t0 + t + 1;
         if (t + 1 == n) {
-          // the next item may not be published yet: it is published after the epilogue of item k - 1, which
-          // waits for the V side emitted below, so only peek here (-2 = unknown: the producer then reads the
-          // next record itself) and block after the V side
+          // the next item may not be published yet (it is published after the epilogue of item k - 1, which waits
+          // for this item's V side): only peek here (-2 = unknown) and block after the tile's units
           tn = -2;
           if (mbar_test(smem_u32(&B.ring_full[(k + 1) & 3]), ((k + 1) >> 2) & 1)) {
             const int pid = *reinterpret_cast<volatile int*>(&B.ring_id[(k + 1) & 3]);
             tn = pid >= 0 ? __ldg(&p.items[pid].tile0) : -1;
           }
         }
-        const uint32_t uk = j == 0 ? 0u : (uint32_t)(4 * j - 2), urk = j == 0 ? 1u : (uint32_t)(4 * j);
-        f(0, uk, k, t, t0 + t, n, tn);
-        if (pv_k >= 0) f(1, (uint32_t)(4 * j - 1), pv_k, pv_t, pv_t0 + pv_t, pv_n, t0 + t);
-        f(2, urk, k, t, t0 + t, n, tn);
-        if (pv_k >= 0) {
-          f(3, (uint32_t)(4 * j + 1), pv_k, pv_t, pv_t0 + pv_t, pv_n, t0 + t);
-          if (pv_t == pv_n - 1) rel(pv_k);
-        }
-        pv_k = k; pv_t = t; pv_n = n; pv_t0 = t0;
+        f(0, (uint32_t)(4 * j), k, t, t0 + t, n, tn);
+        f(2, (uint32_t)(4 * j + 1), k, t, t0 + t, n, tn);
+        f(1, (uint32_t)(4 * j + 2), k, t, t0 + t, n, tn);
+        f(3, (uint32_t)(4 * j + 3), k, t, t0 + t, n, tn);
         if (t + 1 == n) {
+          rel(k);
           nid = ring_get(k + 1);
           if (nid >= 0) {
             nt0 = __ldg(&p.items[nid].tile0);
@@ -285,9 +277,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       t0 = nt0;
       n = nn;
     }
-    f(1, (uint32_t)(4 * j - 1), pv_k, pv_t, pv_t0 + pv_t, pv_n, -1);
-    f(3, (uint32_t)(4 * j + 1), pv_k, pv_t, pv_t0 + pv_t, pv_n, -1);
-    rel(pv_k);
   };
   // register budget per warpgroup (setmaxnreg at the top of each role): softmax 224, loaders / MMA 104, aux 176
   // (x 128 threads = 64512 registers = the CTA allocation of 168 x 384: more would deadlock setmaxnreg.inc; a
@@ -362,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             wait_bar(smem_u32(&B.o_done), (g - 1) & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int c0 = 0; c0 < 256; c0 += 32) {
+            for (int c0 = 0; c0 < 192; c0 += 32) {
               uint32_t o[32];
               FKV_TMEM_LD32(tm + lane_base + T_O + c0, o);
               tmem_ld_wait();
@@ -448,26 +437,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         Cur cs, cp;
         int ks = 0, kp = 0;  // flat indices of the next S / PV tile
-        const uint32_t qa = sb + OFF_Q;
         const uint4 none = make_uint4(0, 0, 0, 0);
         // the next S tile's record, WU lanes and per-slot lane masks, loaded right after the previous S was issued
         // (their global-load latency overlaps the wait for the tile's data); S(k) hands (n_keys, n_slots, flags,
         // lanes) to PV(k) in registers by parity
-        int s_nk = 0, s_ns = 0, s_fl = 0;
-        uint4 s_l = none, s_ml[kRowsMaxSlots];
+        int s_nk = 0, s_ns = 0, s_fl = 0, s_wu = 0;
+        uint4 s_ml[kRowsMaxSlots];
         auto load_s = [&](const Cur& c) {
           const RTile* Tp = p.tiles + c.t0 + c.t;
           s_nk = __ldg(&Tp->n_keys);
           s_ns = __ldg(&Tp->n_slots);
           s_fl = __ldg(&Tp->flags);
           const int wu = __ldg(&Tp->wu);
-          s_l = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].lanes));
+          s_wu = wu;
 #pragma unroll
           for (int sl = 0; sl < kRowsMaxSlots; ++sl)
             s_ml[sl] = __ldg(reinterpret_cast<const uint4*>(p.wus[wu].slot_lanes[sl]));
         };
-        int pv_nk0 = 0, pv_nk1 = 0, pv_ns0 = 0, pv_ns1 = 0, pv_fl0 = 0, pv_fl1 = 0;
-        uint4 pv_l0 = none, pv_l1 = none;
+        int pv_nk0 = 0, pv_nk1 = 0, pv_ns0 = 0, pv_ns1 = 0, pv_fl0 = 0, pv_fl1 = 0, pv_wu0 = 0, pv_wu1 = 0;
         bool s_rec = false;  // s_* hold the record of cs's tile
         uint32_t spins = 0;
         for (;;) {
@@ -478,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               load_s(cs);
               s_rec = true;
             }
-            const uint32_t uk = ks == 0 ? 0u : (uint32_t)(4 * ks - 2), ur = ks == 0 ? 1u : (uint32_t)(4 * ks);
+            const uint32_t uk = (uint32_t)(4 * ks), ur = uk + 1;
             const bool first = cs.t == 0;
             bool ready = mbar_test(smem_u32(&B.full[uk % kNU]), (uk / kNU) & 1) &&
                          mbar_test(smem_u32(&B.full[ur % kNU]), (ur / kNU) & 1);
@@ -488,8 +475,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (ready) {
               // ------------------------- S = Q K^T + q~ R_k^T -------------------------
               const int n_keys = s_nk, n_slots = s_ns;
-              if (ks & 1) { pv_l1 = s_l; pv_nk1 = s_nk; pv_ns1 = s_ns; pv_fl1 = s_fl; }
-              else { pv_l0 = s_l; pv_nk0 = s_nk; pv_ns0 = s_ns; pv_fl0 = s_fl; }
+              if (ks & 1) { pv_nk1 = s_nk; pv_ns1 = s_ns; pv_fl1 = s_fl; pv_wu1 = s_wu; }
+              else { pv_nk0 = s_nk; pv_ns0 = s_ns; pv_fl0 = s_fl; pv_wu0 = s_wu; }
               stamp(p, 0, ks);
               if (first) stamp(p, 8, cs.k);
               tc_fence_after();
@@ -502,8 +489,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t kb = sb + OFF_RING + (uk % kNU) * kUnit;
 #pragma unroll
               for (int k = 0; k < 8; ++k)
-                mma_ss_me(dS, make_desc(qa + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SWZ_128),
-                         make_desc(kb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SWZ_128), idS, k != 0, none);
+                mma_ts_me(dS, tm + T_Q + 8u * k, make_desc(kb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SWZ_128),
+                          idS, k != 0, none);
               mma_commit_e(smem_u32(&B.empty[uk % kNU]));
               *reinterpret_cast<volatile int*>(&B.issued[uk % kNU]) = (int)uk;
               const uint32_t qt = sb + OFF_QT + 4096u * (cs.k & 1);
@@ -530,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (!did && kp < ks) {
-            const uint32_t uv = (uint32_t)(4 * kp + 3), urv = (uint32_t)(4 * kp + 5);
+            const uint32_t uv = (uint32_t)(4 * kp + 2), urv = uv + 1;
             const int b = kp & 1;
             bool ready = mbar_test(smem_u32(&B.p_full[b]), (kp >> 1) & 1) &&
                          mbar_test(smem_u32(&B.full[uv % kNU]), (uv / kNU) & 1) &&
@@ -540,13 +527,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               // ------------------------- O += P V ; A_r += P R_v -------------------------
               const int n_keys = b ? pv_nk1 : pv_nk0, n_slots = b ? pv_ns1 : pv_ns0;
               const uint32_t acc0 = ((b ? pv_fl1 : pv_fl0) & kTileFirst) ? 0u : 1u;
-              const uint4 lw = b ? pv_l1 : pv_l0;
+              const int pwu = b ? pv_wu1 : pv_wu0;
+              const uint4 lw = __ldg(reinterpret_cast<const uint4*>(p.wus[pwu].lanes));  // L1: S read these lines
               stamp(p, 2, kp);
               tc_fence_after();
               if (p.flags & 1) fence_async_smem();  // residual pages by cp.async (diagnostics)
               const uint4 dis = make_uint4(~lw.x, ~lw.y, ~lw.z, ~lw.w);
               const uint32_t idV = idesc_bf16(128, 128, false, true);
-              const uint32_t idR = idesc_bf16(128, 16 * n_slots, false, true);
+              // A_r: slots 0-3 (columns 16 s) and slots 4-7 (columns 16 (s - 4)) into the same 64 columns, each MMA
+              // writing only its slots' lanes
+              const uint4 mlo = __ldg(reinterpret_cast<const uint4*>(p.wus[pwu].lanes_lo));
+              const uint4 mhi = __ldg(reinterpret_cast<const uint4*>(p.wus[pwu].lanes_hi));
+              const uint4 dlo = make_uint4(~mlo.x, ~mlo.y, ~mlo.z, ~mlo.w), dhi = make_uint4(~mhi.x, ~mhi.y, ~mhi.z, ~mhi.w);
+              const uint32_t idR0 = idesc_bf16(128, 16 * min(n_slots, 4), false, true);
+              const uint32_t idR1 = idesc_bf16(128, 16 * max(n_slots - 4, 1), false, true);
               const int nk = (n_keys + 15) >> 4;
               const uint32_t pa = tm + 128u * b;
               const uint32_t vb = sb + OFF_RING + (uv % kNU) * kUnit, rvb = sb + OFF_RING + (urv % kNU) * kUnit;
@@ -554,8 +548,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t acc = k ? 1u : acc0;
                 const uint32_t a = pa + 8u * k;
                 mma_ts_me(tm + T_O, a, make_desc(vb + 2048u * k, 16384, 1024, SWZ_128), idV, acc, dis);
-                if (!(p.flags & 16))  // diagnostics: bit 4 skips the R_v MMAs
-                  mma_ts_me(tm + T_AR, a, make_desc(rvb + 512u * k, 4096, 256, SWZ_32), idR, acc, dis);
+                if (!(p.flags & 16)) {  // diagnostics: bit 4 skips the R_v MMAs
+                  mma_ts_me(tm + T_AR, a, make_desc(rvb + 512u * k, 4096, 256, SWZ_32), idR0, acc, dlo);
+                  if (n_slots > 4)
+                    mma_ts_me(tm + T_AR, a, make_desc(rvb + 4u * 4096u + 512u * k, 4096, 256, SWZ_32), idR1, acc, dhi);
+                }
               }
               mma_commit_e(smem_u32(&B.empty[uv % kNU]));
               mma_commit_e(smem_u32(&B.empty[urv % kNU]));
@@ -799,16 +796,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (row == 0) stamp(p, 10, io);
     };
     // Q rows of item `io` into the (single) Q image, SW128 K-major [d-half][row][128 B]
-    auto qimage = [&](int id) {
+    // Q rows of an item: each aux thread loads its row (TMEM lane) into registers early, and writes it into the Q
+    // columns of TMEM (bf16 pairs: the A operand layout of the S MMAs) once the previous item's last S has run
+    uint32_t qv[64];
+    auto qload = [&](int id) {
       const RItem it = p.items[id];
       const int qr = p.rows[it.row0 + row].q_row;
-      if (qr >= 0) {
-        const uint8_t* src = (const uint8_t*)(Qg + (size_t)qr * 128);
+      const uint4* src = reinterpret_cast<const uint4*>(Qg + (size_t)max(qr, 0) * 128);
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-          cp_async16(sb + OFF_Q + (c >> 3) * 16384u + 128u * row + 16u * ((c & 7) ^ (row & 7)), src + 16 * c);
+      for (int c = 0; c < 16; ++c) {
+        const uint4 v = qr >= 0 ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+        qv[4 * c] = v.x; qv[4 * c + 1] = v.y; qv[4 * c + 2] = v.z; qv[4 * c + 3] = v.w;
       }
-      cp_async_arrive_inc(smem_u32(&B.q_full));
+    };
+    auto qstore = [&]() {
+      FKV_TMEM_ST16(tm + lane_base + T_Q + 0, (qv + 0));
+      FKV_TMEM_ST16(tm + lane_base + T_Q + 16, (qv + 16));
+      FKV_TMEM_ST16(tm + lane_base + T_Q + 32, (qv + 32));
+      FKV_TMEM_ST16(tm + lane_base + T_Q + 48, (qv + 48));
+      tmem_st_wait();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&B.q_full));
     };
@@ -816,7 +823,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int id = ring_get(0);
     int n_done = 0;
     if (id >= 0) {
-      qimage(id);
+      qload(id);
+      qstore();
       qtilde(0, id);
     }
     for (int io = 0; id >= 0; ++io) {
@@ -824,8 +832,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nid = ring_get(io + 1);
       if (nid >= 0) {
         qtilde(io + 1, nid);  // its image buffer was freed by the last S of item io - 1 (waited in the last iteration)
+        qload(nid);
         wait_bar(smem_u32(&B.q_empty), io & 1);
-        qimage(nid);
+        tc_fence_after();
+        qstore();
       }
       // epilogue of item io
       if (row == 0) B.prog[13] = io;
@@ -848,7 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int s = 0; s < kRowsMaxSlots; ++s) {
         if (!__any_sync(0xffffffffu, rr.q_row >= 0 && slot == s)) continue;
         uint32_t t16[16];
-        FKV_TMEM_LD16(tm + lane_base + T_AR + 16 * s, t16);
+        FKV_TMEM_LD16(tm + lane_base + T_AR + 16 * (s & 3), t16);
         tmem_ld_wait();
         if (slot == s) {
 #pragma unroll

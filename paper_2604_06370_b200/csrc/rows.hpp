@@ -24,13 +24,15 @@ struct RRow {          // one lane of an item (16 bytes)
   int32_t entry;       // partial entry index (-1 = none)
   int32_t meta;        // slot | kv head << 8 | adapter slot << 16
 };
-struct RWu {           // 160 bytes
+struct RWu {           // 192 bytes
   uint32_t lanes[4];          // active lanes of the WU
   uint32_t slot_lanes[8][4];  // lanes of each residual slot (owner) of the WU
-  int32_t n_slots;            // residual slots 0..n_slots-1 (A_r columns 16 s .. 16 s + 15)
+  uint32_t lanes_lo[4];       // lanes of slots 0-3 (their A_r columns 16 s), and of slots 4-7 (16 (s - 4))
+  uint32_t lanes_hi[4];
+  int32_t n_slots;            // residual slots 0..n_slots-1
   int32_t pad_[3];
 };
-static_assert(sizeof(RWu) == 160, "RWu");
+static_assert(sizeof(RWu) == 192, "RWu");
 struct RTile {         // 64 bytes
   int32_t key0;        // absolute position of the tile's first key
   int32_t n_keys;      // 1..128

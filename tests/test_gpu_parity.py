@@ -19,9 +19,18 @@ TOL = {"bf16": 2e-2, "f32": 1e-5}
 
 
 def _tc_kernel(mode):
-    """Default tcgen05 kernel id: 3 = rows on the TMEM lanes (ra_rows.cu, NONE mode), 2 = keys on the TMEM
-    lanes (ra_tc.cu, DEFERRED; FKV_KERNEL=2 forces it for NONE too)."""
-    return 3 if mode == "none" else 2
+    """Default tcgen05 kernel id: 2 = keys on the TMEM lanes (ra_tc.cu, both modes); 3 = rows on the TMEM lanes
+    (ra_rows.cu, NONE mode) when FKV_KERNEL=3 / FKV_PLAN_ROWS_KERNEL selects it."""
+    import os
+    return 3 if (mode == "none" and os.environ.get("FKV_KERNEL") == "3") else 2
+
+
+@pytest.fixture(params=["default", "rows"])
+def kernel_choice(request, monkeypatch):
+    """Runs a NONE-mode test on both tcgen05 kernels (the default keys-on-lanes one and the rows-on-lanes one)."""
+    if request.param == "rows":
+        monkeypatch.setenv("FKV_KERNEL", "3")
+    return request.param
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -72,17 +81,20 @@ def test_device_synth_matches_host_generator():
 
 
 @pytest.mark.parametrize("mode", ["deferred", "none"])
-@pytest.mark.parametrize("kernel", ["tc", "tc_keys", "tc128", "mma", "simt"])
+@pytest.mark.parametrize("kernel", ["tc", "rows", "tc128", "mma", "simt"])
 def test_c1_parity(mode, kernel, monkeypatch):
     """configs[0] (C1): 1 layer Llama-3.1-8B shape, r=16, 4 agents forked from a
     2K-token prefix + 128 private + 1 decode token; llama3 RoPE, theta 5e5."""
     expect = None
-    if kernel in ("tc128", "tc_keys"):
+    if kernel == "rows":
         if mode == "deferred":
-            pytest.skip("keys-on-lanes variants are the DEFERRED default already")
-        monkeypatch.setenv("FKV_KERNEL", "2")
-        if kernel == "tc128":
-            monkeypatch.setenv("FKV_TC_ROWS", "128")
+            pytest.skip("the rows-on-lanes kernel is NONE-mode only")
+        monkeypatch.setenv("FKV_KERNEL", "3")
+        kernel, expect = "tc", 3
+    if kernel == "tc128":
+        if mode == "deferred":
+            pytest.skip("the 128-row variant is NONE-mode only")
+        monkeypatch.setenv("FKV_TC_ROWS", "128")
         kernel, expect = "tc", 2
     scen = recipes.c1()
     fkv = _ctx(scen, 1, 32, 8, 128, 16, 64, "bf16", mode, theta=500000.0, llama3=True)
@@ -104,8 +116,8 @@ def test_tc_kernel_page_sizes_and_groups(mode, variant, P, monkeypatch):
     variant (8 slots, row sums reduced on the CUDA cores)."""
     if variant != "rows":
         monkeypatch.setenv("FKV_TC_ROWS", str(variant))
-        if mode == "none":
-            monkeypatch.setenv("FKV_KERNEL", "2")
+    else:
+        monkeypatch.setenv("FKV_KERNEL", "3")
     ag = [recipes.AgentSpec(100, 100, None, 0, False, 700, decode=False)]
     for i in range(3):
         ag.append(recipes.AgentSpec(1000 + i, i, 100, 700, False, 0, decode=False))
@@ -140,7 +152,7 @@ def _random_scenario(rnd, P, max_prefix=300):
 
 
 @pytest.mark.parametrize("seed", range(1, 121))
-def test_random_suite(seed):
+def test_random_suite(seed, monkeypatch):
     """Random fork trees (unaligned forks -> CoW tail pages, same-agent
     branches sharing residual pages, chunked-prefill query rows), both RoPE
     modes, bf16 tensor-core path and fp32 SIMT path, page sizes 16/64/128,
@@ -152,6 +164,8 @@ def test_random_suite(seed):
     d = 64 if (dtype == "f32" and seed % 8 == 0) else 128
     hq, hkv = (8, 2) if dtype == "f32" else rnd.choice([(8, 2), (32, 8), (64, 8)])
     scen = _random_scenario(rnd, P)
+    if seed % 2 == 1:
+        monkeypatch.setenv("FKV_KERNEL", "3")   # NONE-mode seeds alternate between the two tcgen05 kernels
     fkv = _ctx(scen, 2, hq, hkv, d, 16, P, dtype, mode)
     driver.build(fkv, scen, seed=seed)
     for layer in (0, 1):
@@ -226,7 +240,7 @@ def test_kv_head_shard_parity(mode):
 
 
 @pytest.mark.parametrize("mode", ["none", "deferred"])
-def test_many_splits_combine(mode, monkeypatch):
+def test_many_splits_combine(mode, monkeypatch, kernel_choice):
     """One-tile key-range pieces (FKV_PIECE_TILES=1) over a ~5K-key shared prefix: every output row merges
     ~40 split partials, which exercises the combine kernel's multi-batch (> 32 entries) path and items that
     share their staged Q / q~ images."""
@@ -246,8 +260,8 @@ def test_many_splits_combine(mode, monkeypatch):
 
 
 @pytest.mark.parametrize("mode", ["none", "deferred"])
-def test_c2_full_size_sampled(mode):
-    """configs[1] at full size (32K shared prefix, 16 agents x 4 branches = 64 decode sequences, 32 q / 8 kv
+def test_c2_full_size_sampled(mode, kernel_choice):
+    """Both tcgen05 kernels in NONE mode (kernel_choice). configs[1] at full size (32K shared prefix, 16 agents x 4 branches = 64 decode sequences, 32 q / 8 kv
     heads, d 128, r 16, page 128): one layer of exactly the launch configuration bench.py times (same plan,
     schedule and kernel variant), sampled sequences of every agent group against the fp64 oracle."""
     scen = recipes.c2()
