@@ -344,13 +344,54 @@ class Run:
                     fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 1)
                 fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 2)
             else:
-                if not self.prefill:
-                    host["kv"](layer)
-                    fkv.write_kv(layer, batch, starts, ones, host["dkb"], host["dvb"], host["drk"], host["drv"])
-                    self.launches += 1
-                fkv.residual_attention_host(pl, layer, host["q"][layer], host["o"][layer], host["dq"], host["do"])
+                self._host_layer(host, pl, layer, starts)
             self.launches += _launches_per_layer(pl.info.kernel)
+        if host is not None:
+            self._host_drain(host)
         return pl
+
+    def _host_layer(self, host, pl, layer, starts):
+        """e2e leg, one layer: the layer's inputs (Q rows and the new K/V/residual rows, pinned host memory) go
+        H2D on a copy stream one layer ahead into double-buffered device staging, the compute stream waits for
+        them, and O goes D2H on the copy stream behind the compute event, so copies overlap the previous /
+        next layer's kernels (the same public calls a serving loop makes: write_kv + residual_attention)."""
+        import torch
+        fkv, batch, L_ = self.fkv, self.wl.batch, self.wl.L
+        cs, ev_in, ev_out = host["cs"], host["ev_in"], host["ev_out"]
+        if layer == 0:
+            self._host_h2d(host, 0)
+        b = layer & 1
+        dv = host["dev"][b]
+        self.stream.wait_event(ev_in[b])
+        if not self.prefill:
+            fkv.write_kv(layer, batch, starts, [1] * len(batch), dv["kb"], dv["vb"], dv["rk"], dv["rv"])
+            self.launches += 1
+        fkv.residual_attention(pl, layer, dv["q"], dv["o"])
+        ev_out[b].record(self.stream)
+        with torch.cuda.stream(cs):
+            if layer + 1 < L_:
+                cs.wait_event(ev_out[b ^ 1])   # the previous layer (or step) is done with buffer b ^ 1
+                self._host_h2d(host, layer + 1)
+            cs.wait_event(ev_out[b])
+            host["o"][layer].copy_(dv["o"], non_blocking=True)
+
+    def _host_h2d(self, host, layer):
+        import torch
+        b = layer & 1
+        dv = host["dev"][b]
+        with torch.cuda.stream(host["cs"]):
+            dv["q"].copy_(host["q"][layer], non_blocking=True)
+            if not self.prefill:
+                for k in ("kb", "vb", "rk", "rv"):
+                    dv[k].copy_(host["kv"][k][layer], non_blocking=True)
+            host["ev_in"][b].record(host["cs"])
+
+    def _host_drain(self, host):
+        """The step's result is on the host when the copy stream is done: the compute stream joins it."""
+        import torch
+        e = torch.cuda.Event()
+        e.record(host["cs"])
+        self.stream.wait_event(e)
 
     def graph_median_ms(self, reps=25):
         """Main-kernel time of layer 0 as the median over `reps` CUDA-graph replays."""
@@ -497,17 +538,13 @@ def run_ours(args):
         qh = torch.empty(L_, run.n_q_rows, hq, d, dtype=torch.bfloat16, pin_memory=True)
         qh.copy_(run.Q.cpu())
         oh = torch.empty_like(qh).pin_memory()
-        kvh = [t.cpu().pin_memory() for t in (run.kb, run.vb, run.rk, run.rv)]
-        dq = torch.empty(run.n_q_rows, hq, d, dtype=torch.bfloat16, device=run.dev)
-        do = torch.empty_like(dq)
-        dkv = [torch.empty_like(t[0]) for t in (run.kb, run.vb, run.rk, run.rv)]
-
-        def kv(layer):
-            for dst, src in zip(dkv, kvh):
-                dst.copy_(src[layer], non_blocking=True)
-
-        host = {"q": qh, "o": oh, "dq": dq, "do": do, "kv": kv, "dkb": dkv[0], "dvb": dkv[1], "drk": dkv[2],
-                "drv": dkv[3]}
+        kvh = {k: t.cpu().pin_memory() for k, t in zip(("kb", "vb", "rk", "rv"), (run.kb, run.vb, run.rk, run.rv))}
+        devb = [{"q": torch.empty(run.n_q_rows, hq, d, dtype=torch.bfloat16, device=run.dev),
+                 "o": torch.empty(run.n_q_rows, hq, d, dtype=torch.bfloat16, device=run.dev),
+                 **{k: torch.empty_like(t[0]) for k, t in zip(("kb", "vb", "rk", "rv"),
+                                                              (run.kb, run.vb, run.rk, run.rv))}} for _ in range(2)]
+        host = {"q": qh, "o": oh, "kv": kvh, "dev": devb, "cs": torch.cuda.Stream(device=run.dev),
+                "ev_in": [torch.cuda.Event(), torch.cuda.Event()], "ev_out": [torch.cuda.Event(), torch.cuda.Event()]}
         for _ in range(2):
             run.step(host=host)
         torch.cuda.synchronize()
@@ -522,6 +559,8 @@ def run_ours(args):
         ems = _max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
         h2d = L_ * (run.n_q_rows * hq * d * 2 + (0 if run.prefill else
                                                  sum(t[0].numel() * 2 for t in (run.kb, run.vb, run.rk, run.rv))))
+        if not run.prefill:
+            h2d += run.info.device_bytes   # the step's plan blob (fkv_plan_upload)
         d2h = L_ * run.n_q_rows * hq * d * 2
         e2e = {"value": value * ms / ems, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 

@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libforkkv.so")
+# FKV_LIB_PATH: an alternative build of the same library (diagnostic A/B variants, tools/variants.sh)
+LIB_PATH = os.environ.get("FKV_LIB_PATH") or os.path.join(HERE, "libforkkv.so")
 
 OK = 0
 E_INVALID = 1

@@ -607,8 +607,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           stamp(p, my_kind == 0 ? 6 : 15, kt);
           const uint32_t dst = sb + OFF_RING + s_ * kUnit;
           if (P == 128) {
-            mbar_expect_tx(smem_u32(&B.full[s_]), c_pg >= 0 ? 32768u : 0u);
-            if (c_pg >= 0)
+            const bool ld = c_pg >= 0 && !(p.flags & 128);  // diagnostics: bit 7 skips the base copies
+            mbar_expect_tx(smem_u32(&B.full[s_]), ld ? 32768u : 0u);
+            if (ld)
               tma_load_3d(dst, m3, 0, (int)(p.base_rows_layer + (int64_t)c_pg * p.hkv * P + hrow), 0,
                           smem_u32(&B.full[s_]));
           } else {
@@ -671,13 +672,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&B.full[s_]));
         } else if (P == 128) {
-          const int mine = pg >= 0 ? 4096 : 0;
+          const int mine = (pg >= 0 && !(p.flags & 64)) ? 4096 : 0;  // diagnostics: bit 6 skips the residual copies
           int tot = mine;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
           if (lane == 0) mbar_expect_tx(smem_u32(&B.full[s_]), (uint32_t)tot);
           __syncwarp();
-          if (pg >= 0) bulk_g2s(dst + 4096u * lane, rp + (size_t)pg * 4096, 4096, smem_u32(&B.full[s_]));
+          if (mine) bulk_g2s(dst + 4096u * lane, rp + (size_t)pg * 4096, 4096, smem_u32(&B.full[s_]));
         } else {
           // pages of 16..64 tokens: (slot, page) pieces over the lanes (tile fields re-read: not prefetched)
           const int np = ns * ppt;
