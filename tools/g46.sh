@@ -1,0 +1,6 @@
+O=gpurun_out/g46; mkdir -p $O
+for v in base rs2nq1 rs2vs2 nq1; do
+  FKV_LIB_PATH=paper_2604_06370_b200/variants/libforkkv_$v.so timeout 300 python tools/timeline.py --mode none --page 128 --tiles 2 > $O/tl_$v.txt 2>&1
+  FKV_LIB_PATH=paper_2604_06370_b200/variants/libforkkv_$v.so timeout 300 python bench.py --steps 10 --no-cpu-baseline --no-deferred --no-e2e > $O/bench_$v.json 2>$O/bench_$v.err
+done
+FKV_LIB_PATH=paper_2604_06370_b200/variants/libforkkv_rs2nq1.so timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "c2_full or c1 or page" > $O/pytest_rs2nq1.txt 2>&1
