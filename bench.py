@@ -100,10 +100,11 @@ class ClockSampler:
 class Workload:
     """A BASELINE.json config as seen by one rank."""
 
-    def __init__(self, name, world=1, rank=0):
+    def __init__(self, name, world=1, rank=0, fanout_rank=(16, 64)):
         from workloads import recipes
         self.name, self.kind, self.scaling = name, "decode", "weak"
         self.L, self.Hq, self.Hkv, self.d, self.r = 32, 32, 8, 128, 16
+        self.r_eff = None
         self.kv = (0, 8)
         self.parallelism = f"agent-batch x{world} (partitioner H=1, D={world}): every rank its own agent batch"
         if name == "c1":
@@ -116,6 +117,15 @@ class Workload:
         elif name == "c5":
             self.scen = recipes.c5()
             self.desc = "configs[4] point: Llama-3.1-8B 32 layers, 64 independent agents over a 32K prefix, r=16"
+        elif name == "sweep":
+            # configs[4]: rank r x fork fan-out N. Ranks below 16 are zero-padded into a rank-16 pool (C-8: exact) so
+            # the tcgen05 kernel runs them; the roofline counts the r-wide bytes only (the padding is overhead)
+            R, N = int(fanout_rank[0]), int(fanout_rank[1])
+            self.r_eff, self.r = R, (16 if R <= 16 else R)
+            self.scen = recipes.fanout(N)
+            self.desc = (f"configs[4] sweep point: Llama-3.1-8B 32 layers, fork fan-out {N} agents (distinct adapters, "
+                         f"own residual) over a 32K prefix, LoRA rank {R}" +
+                         (f" (zero-padded into a rank-{self.r} pool, C-8)" if self.r != R else ""))
         elif name == "c4":
             from paper_2604_06370_b200.api import partition, partition_shard
             self.L, self.Hq, self.Hkv = 80, 64, 8
@@ -166,7 +176,7 @@ def _cpu_baseline(wl, mode, seed, max_seqs, budget_s=20.0):
     q_sample = min(wl.C, 4)
     done, spent = 0, 0.0
     for a in wl.batch[:max_seqs]:
-        inp = recipes.oracle_inputs(wl.scen, seed, a, 0, wl.kv[1] - wl.kv[0], wl.d, wl.r,
+        inp = recipes.oracle_inputs(wl.scen, seed, a, 0, wl.kv[1] - wl.kv[0], wl.d, wl.r_eff or wl.r,
                                     (wl.kv[1] - wl.kv[0]) * wl.Hq // wl.Hkv, q_sample, "bf16", kv_heads=wl.kv)
         t0 = time.perf_counter()
         ra.residual_attention(inv_freq_=fr, rope_mode=ra.ROPE_DEFERRED if mode == "deferred" else ra.ROPE_NONE,
@@ -186,14 +196,14 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    wl = Workload(args.config)
+    wl = Workload(args.config, 1, 0, (getattr(args, "rank", 16), getattr(args, "fanout", 64)))
     from oracle import ra
     from workloads import recipes
     fr = ra.inv_freq(wl.d, 500000.0, llama3=True)
     threads = min(8, os.cpu_count() or 1)
     a = wl.batch[0]
     q_sample = min(wl.C, 4)
-    inp = recipes.oracle_inputs(wl.scen, args.seed, a, 0, wl.kv[1] - wl.kv[0], wl.d, wl.r,
+    inp = recipes.oracle_inputs(wl.scen, args.seed, a, 0, wl.kv[1] - wl.kv[0], wl.d, wl.r_eff or wl.r,
                                 (wl.kv[1] - wl.kv[0]) * wl.Hq // wl.Hkv, q_sample, "bf16", kv_heads=wl.kv)
     times = []
     for i in range(args.warmup + args.steps):
@@ -243,6 +253,14 @@ KERNEL_NAMES = {0: "mma.sync grouped (baseline)", 1: "simt", 2: "tcgen05 keys-on
                 3: "tcgen05 rows-on-lanes"}
 
 
+def alg_bytes_of(info, wl):
+    """The planner's algorithmic bytes per layer; for an adapter rank r_eff zero-padded into a rank-r pool only the
+    r_eff-wide part of the rank-proportional bytes (residual pages + adapters) counts."""
+    if wl.r_eff is None or wl.r_eff == wl.r:
+        return info.alg_bytes
+    return info.alg_bytes - info.alg_rank_bytes * (wl.r - wl.r_eff) // wl.r
+
+
 def _launches_per_layer(kernel):
     """Our kernels per layer: main (+ the stager of kernel 2) + combine."""
     return 3 if kernel == 2 else 2
@@ -276,7 +294,7 @@ class Run:
         hq = fkv.hq
         self.hq = hq
         self.seed = seed = args.seed + (1000 * rank if wl.scaling == "weak" else 0)
-        driver.build(fkv, scen, seed, h0=self.h0)
+        driver.build(fkv, scen, seed, h0=self.h0, r_eff=wl.r_eff)
         dev = self.dev = torch.device("cuda", dev_index)
         self.prefill = wl.kind == "prefill"
         self.n_q_rows = B * C
@@ -293,6 +311,9 @@ class Run:
             synth_fill(self.vb[layer], seed, synth.KIND_VBASE, 777, layer, 0, head0=self.h0)
             synth_fill(self.rk[layer], seed, synth.KIND_RK, 777, layer, 0)
             synth_fill(self.rv[layer], seed, synth.KIND_RV, 777, layer, 0)
+        if wl.r_eff is not None and wl.r_eff < wl.r:
+            self.rk[:, :, wl.r_eff:] = 0
+            self.rv[:, :, wl.r_eff:] = 0
         self.pl0 = fkv.plan([(a, C) for a in batch], upload=False)
         self.plan_buf = torch.empty(max(1 << 24, 2 * self.pl0.info.device_bytes), dtype=torch.uint8, device=dev)
         self.ws_buf = torch.empty(max(64, 2 * self.pl0.info.workspace_bytes // 4), dtype=torch.float32, device=dev)
@@ -325,7 +346,7 @@ class Run:
             self.info = pl.info
         self.pl = pl
         if record:
-            self.alg_bytes.append(pl.info.alg_bytes)
+            self.alg_bytes.append(alg_bytes_of(pl.info, self.wl))
         starts = [self.seqlens[a] - 1 for a in batch]
         Q, O = self.Q, self.O
         for layer in range(wl.L):
@@ -523,7 +544,7 @@ def run_ours(args):
         # the hot path has no data-path collective: ranks exchange only scalars (barrier, max time,
         # token counts), over gloo so that ranks sharing one GPU work too
         dist.init_process_group("gloo")
-    wl = Workload(args.config, world, rank)
+    wl = Workload(args.config, world, rank, (args.rank, args.fanout))
     run = Run(args, wl, args.mode, world, rank, dev_index)
     ms, clocks = _timed(run, args, world, True, dev_index)
     launches = run.launches
@@ -619,7 +640,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "sweep"])
+    ap.add_argument("--rank", type=int, default=16, help="sweep: LoRA rank (8 / 16 / 64)")
+    ap.add_argument("--fanout", type=int, default=64, help="sweep: agents forked from the prefix (4..256)")
     ap.add_argument("--mode", default="none", choices=["deferred", "none"],
                     help="none = the north-star split q(K_base + R_K B_K)^T = qK_base^T + (qB_K^T)R_K^T (default); "
                          "deferred = the paper's RoPE on the rebuilt residual (Alg.1), DESIGN.md C-1")

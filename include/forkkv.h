@@ -131,9 +131,11 @@ typedef struct fkv_plan_info {
   int64_t n_seqs, n_rows, n_segments, n_items, n_ctas, n_warps, n_entries;
   int64_t key_tiles;        /* 64-key tiles summed over CTAs (one layer) */
   int64_t alg_bytes;        /* algorithmic HBM bytes per layer (SURVEY §8(d) formula) */
-  int64_t kernel;           /* 0 = tensor-core grouped (mma), 1 = SIMT, 2 = tcgen05 */
+  int64_t kernel;           /* 0 = mma.sync (forced only), 1 = SIMT, 2 = tcgen05 keys-on-lanes, 3 = tcgen05 rows-on-lanes */
   int64_t device_bytes;     /* bytes fkv_plan_upload needs */
   int64_t workspace_bytes;  /* bytes fkv_residual_attention needs */
+  int64_t alg_rank_bytes;   /* the part of alg_bytes proportional to the rank r (residual pages + adapters):
+                               an adapter of rank r' < r zero-padded into the pool (C-8) needs r'/r of it */
 } fkv_plan_info;
 
 /* ---- lifetime ------------------------------------------------------- */

@@ -60,7 +60,7 @@ class fkv_seq(ctypes.Structure):
 class fkv_plan_info(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("n_seqs", "n_rows", "n_segments", "n_items", "n_ctas", "n_warps",
                                                "n_entries", "key_tiles", "alg_bytes", "kernel", "device_bytes",
-                                               "workspace_bytes")]
+                                               "workspace_bytes", "alg_rank_bytes")]
 
 
 _vp = ctypes.c_void_p

@@ -296,6 +296,7 @@ fkv_status fkv_plan_get_info(const fkv_plan* plan, fkv_plan_info* info) {
   info->kernel = p.kernel;
   info->device_bytes = (int64_t)p.blob.size();
   info->workspace_bytes = (int64_t)p.ws_bytes;
+  info->alg_rank_bytes = p.alg_rank_bytes;
   return FKV_OK;
 }
 

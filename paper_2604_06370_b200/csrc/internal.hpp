@@ -205,7 +205,7 @@ struct Plan {
   size_t ws_ctr_off = 0;             // kernel 3: workspace offset of the item-queue counters
   mutable const void* ws_zeroed = nullptr;  // the workspace whose counters were last zeroed for this plan  // range plan (§8(f) f4): output rows may see no key of [key_begin, key_end)
   size_t stage_off = 0;  // workspace offset of the staged operand images (tcgen05 kernel)
-  int64_t n_segments = 0, n_entries = 0, key_tiles = 0, alg_bytes = 0;
+  int64_t n_segments = 0, n_entries = 0, key_tiles = 0, alg_bytes = 0, alg_rank_bytes = 0;
   // rows-on-lanes tcgen05 kernel (kernel 3): k::RItem / RWu / RTile / RRow records (rows.hpp)
   std::vector<uint8_t> r_items, r_wus, r_tiles, r_rows;
   size_t off_ritems = 0, off_rwus = 0, off_rtiles = 0, off_rrows = 0;

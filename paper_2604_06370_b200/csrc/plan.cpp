@@ -477,6 +477,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
   // residual once per (segment, owner), adapters once, Q in + O out.
   std::set<int32_t> used_adapters;
   for (const DevSeq& s : pl.seqs) used_adapters.insert(s.adapter_slot);
+  pl.alg_rank_bytes = res_bytes + (int64_t)used_adapters.size() * 2 * r * d * hkv * (int64_t)el;
   pl.alg_bytes = base_bytes + res_bytes + (int64_t)used_adapters.size() * 2 * r * d * hkv * (int64_t)el +
                  pl.n_rows_q * c.hq_local * d * 2 * (int64_t)el;
   // blob

@@ -329,6 +329,7 @@ void build_rows_plan(Ctx& c, Plan& pl, const std::vector<PlanSeg>& segs, const s
   // owner), adapters once, Q in + O out
   std::set<int32_t> used_adapters;
   for (const DevSeq& s : pl.seqs) used_adapters.insert(s.adapter_slot);
+  pl.alg_rank_bytes = res_bytes + (int64_t)used_adapters.size() * 2 * r * d * hkv * (int64_t)el;
   pl.alg_bytes = base_bytes + res_bytes + (int64_t)used_adapters.size() * 2 * r * d * hkv * (int64_t)el +
                  pl.n_rows_q * hq * d * 2 * (int64_t)el;
   pl.n_segments = (int64_t)segs.size();

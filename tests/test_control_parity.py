@@ -175,6 +175,9 @@ def test_plan_groups_shared_prefix():
     ad = 4 * 2 * 16 * 128 * 8 * el
     qo = 4 * 32 * 128 * 2 * el
     assert pl.info.alg_bytes == shared + private + res + ad + qo
+    # the rank-proportional part (residual pages + adapters): what a rank r' < r adapter padded into the pool
+    # scales by r'/r (bench.py alg_bytes_of, C-8)
+    assert pl.info.alg_rank_bytes == res + ad
 
 
 def test_partitioner():

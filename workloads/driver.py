@@ -13,7 +13,7 @@ _CHUNK = 65536       # rows per staged write (base rows: 65536 x Hkv x d x 2 B =
 _CHUNK_RES = 1 << 20  # residual-only writes are r-wide: stage up to 1M rows
 
 
-def make_adapter(fkv, seed: int, adapter_id: int, h0: int):
+def make_adapter(fkv, seed: int, adapter_id: int, h0: int, r_eff: Optional[int] = None):
     import torch
     from paper_2604_06370_b200.api import synth_fill
     tdt = torch.bfloat16 if fkv.dtype_name == "bf16" else torch.float32
@@ -26,11 +26,14 @@ def make_adapter(fkv, seed: int, adapter_id: int, h0: int):
                        scale=synth.SCALE[synth.KIND_BK])
             synth_fill(bv[layer, hl], seed, synth.KIND_BV, adapter_id, layer, 0, head0=h0 + hl,
                        scale=synth.SCALE[synth.KIND_BV])
+    if r_eff is not None and r_eff < fkv.r:   # an adapter of rank r_eff zero-padded into the pool rank (C-8)
+        bk[:, :, r_eff:] = 0
+        bv[:, :, r_eff:] = 0
     return bk, bv
 
 
 def write_rows(fkv, seed: int, agent: int, writer: int, pos0: int, n: int, mask: int, h0: int,
-               layers: Optional[Iterable[int]] = None, stage=None):
+               layers: Optional[Iterable[int]] = None, stage=None, r_eff: Optional[int] = None):
     import torch
     from paper_2604_06370_b200.api import synth_fill
     if n <= 0:
@@ -59,16 +62,20 @@ def write_rows(fkv, seed: int, agent: int, writer: int, pos0: int, n: int, mask:
             if mask & 12:
                 synth_fill(rk, seed, synth.KIND_RK, writer, layer, pos0 + o)
                 synth_fill(rv, seed, synth.KIND_RV, writer, layer, pos0 + o)
+                if r_eff is not None and r_eff < fkv.r:   # xA_i of a rank-r_eff adapter, zero-padded (C-8)
+                    rk[:, r_eff:] = 0
+                    rv[:, r_eff:] = 0
             fkv.write_kv(layer, [agent], [pos0 + o], [c], kb, vb, rk, rv, mask)
 
 
-def build(fkv, scen: Scenario, seed: int, h0: int = 0, layers=None):
-    """Create every agent of the scenario through the API and write its rows."""
+def build(fkv, scen: Scenario, seed: int, h0: int = 0, layers=None, r_eff: Optional[int] = None):
+    """Create every agent of the scenario through the API and write its rows (r_eff: adapters and residual rows
+    of rank r_eff < fkv.r, zero-padded into the pool, C-8)."""
     from paper_2604_06370_b200 import _lib as L
     stage = {}
     adapters = sorted({s.adapter for s in scen.agents})
     for ad in adapters:
-        bk, bv = make_adapter(fkv, seed, ad, h0)
+        bk, bv = make_adapter(fkv, seed, ad, h0, r_eff)
         fkv.register_adapter(ad, bk, bv)
     for s in scen.agents:
         if s.parent is None:
@@ -76,11 +83,11 @@ def build(fkv, scen: Scenario, seed: int, h0: int = 0, layers=None):
         else:
             fkv.fork(s.parent, s.fork_len, s.id, s.adapter, L.FORK_SHARE_RESIDUAL if s.share_res else 0)
             if not s.share_res:
-                write_rows(fkv, seed, s.id, s.id, 0, s.fork_len, L.WRITE_RK | L.WRITE_RV, h0, layers, stage)
+                write_rows(fkv, seed, s.id, s.id, 0, s.fork_len, L.WRITE_RK | L.WRITE_RV, h0, layers, stage, r_eff)
         if s.n_private:
             toks = synth.tokens(seed, s.id, s.fork_len, s.n_private).tolist()
             fkv.append([s.id], [s.n_private], toks)
-            write_rows(fkv, seed, s.id, s.id, s.fork_len, s.n_private, L.WRITE_ALL, h0, layers, stage)
+            write_rows(fkv, seed, s.id, s.id, s.fork_len, s.n_private, L.WRITE_ALL, h0, layers, stage, r_eff)
 
 
 def make_queries(fkv, scen: Scenario, seed: int, layer: int, step: int = 0, h0: int = 0, out=None):

@@ -123,6 +123,12 @@ def c5(prefix=32768, n_agents=64, private=128) -> Scenario:
     return Scenario("C5", ag)
 
 
+def fanout(n_agents, prefix=32768, private=128) -> Scenario:
+    """configs[4] sweep point: fork fan-out N (4-256) agents with distinct adapters, each with its own residual
+    over the shared prefix (the C5 shape at fan-out N)."""
+    return c5(prefix=prefix, n_agents=n_agents, private=private)
+
+
 # ---- host-side oracle inputs --------------------------------------------------
 
 _RUN_CACHE: Dict = {}
