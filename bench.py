@@ -284,7 +284,7 @@ class Run:
         nr += B + 8
         # every timed / warm-up / e2e decode step appends one token per sequence (DEFERRED needs the RoPE table to
         # cover them: ADVICE r1)
-        appends = args.warmup + 2 * args.steps + 4
+        appends = args.warmup + 3 * args.steps + 4
         max_pos = max(scen.seqlen(s.id) for s in scen.agents) + appends + 16
         t_setup = time.time()
         self.fkv = fkv = ForkKV(n_layers=wl.L, n_q_heads=wl.Hq, n_kv_heads=wl.Hkv, head_dim=wl.d, rank=wl.r,
@@ -327,7 +327,7 @@ class Run:
         self.events, self.launches, self.alg_bytes, self.info = [], 0, [], self.pl0.info
         self.pl = self.pl0
 
-    def step(self, record=False, host=None):
+    def step(self, record=False, host=None, events=None):
         """One pass of the whole hot path over one batch: (decode) append + plan + upload, then per layer
         kv_write + main kernel + combine."""
         import torch
@@ -355,7 +355,7 @@ class Run:
                     fkv.write_kv(layer, batch, starts, ones, self.kb[layer], self.vb[layer], self.rk[layer],
                                  self.rv[layer])
                     self.launches += 1
-                if record:
+                if record if events is None else events:
                     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
                     e0.record(self.stream)
                     fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 1)
@@ -465,12 +465,20 @@ def _timed(run, args, world, dist_ok, dev_index):
     t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     t0.record(run.stream)
+    # the timed steps carry no per-kernel events: an event recorded between two PDL-chained launches makes the
+    # second wait for the first to drain (the overlap a serving loop gets); the kernel times for the roofline come
+    # from the instrumented pass below (same steps, same inputs)
     for _ in range(args.steps):
-        run.step(record=True)
+        run.step(record=True, events=bool(os.environ.get("FKV_BENCH_EVENTS_IN_TIMED")))
     t1.record(run.stream)
     torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    if not run.events:
+        for _ in range(args.steps):
+            run.step(record=False, events=True)
+        torch.cuda.synchronize()
     clocks = clk.stop()
-    return t0.elapsed_time(t1) / args.steps, clocks
+    return ms, clocks
 
 
 def _max_over_ranks(x, world):
