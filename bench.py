@@ -468,8 +468,13 @@ def _timed(run, args, world, dist_ok, dev_index):
     # the timed steps carry no per-kernel events: an event recorded between two PDL-chained launches makes the
     # second wait for the first to drain (the overlap a serving loop gets); the kernel times for the roofline come
     # from the instrumented pass below (same steps, same inputs)
+    nvtx = bool(os.environ.get("FKV_NVTX"))   # ncu --nvtx --nvtx-include "timed/": the launch list of these steps
+    if nvtx:
+        torch.cuda.nvtx.range_push("timed")
     for _ in range(args.steps):
         run.step(record=True, events=bool(os.environ.get("FKV_BENCH_EVENTS_IN_TIMED")))
+    if nvtx:
+        torch.cuda.nvtx.range_pop()
     t1.record(run.stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps

@@ -41,43 +41,73 @@ __device__ __forceinline__ void copy_elems(void* dst, const void* src, int64_t n
   }
 }
 
-__global__ void kv_write_kernel(PoolView pv, int32_t layer, Runs<kMaxRuns> runs, int32_t n_runs, const uint8_t* kb,
-                                const uint8_t* vb, const uint8_t* rk, const uint8_t* rv, uint32_t mask) {
+// One CTA per run (blockIdx.y strides over its rows). Every 16-byte chunk of a row (K_base and V_base of all the
+// rank's kv heads, R_k, R_v) is one independent load + store by one thread, so a row costs one memory latency
+// (a per-head copy loop serialises its loads behind the previous head's stores: the pointers may alias).
+// Residual rows of the swizzled format (res_col) land with their two 16-byte halves swapped on rows 4..7 of each
+// 8-row group. Unaligned shapes (tiny d or r) take the element-wise path.
+template <int N>
+__global__ void __launch_bounds__(256) kv_write_kernel(PoolView pv, int32_t layer, Runs<N> runs, int32_t n_runs,
+                                                       const uint8_t* kb, const uint8_t* vb, const uint8_t* rk,
+                                                       const uint8_t* rv, uint32_t mask) {
   pdl_wait();
   pdl_trigger();
   const int run = blockIdx.x;
   if (run >= n_runs) return;
   const WriteRun w = runs.r[run];
   const int es = pv.dtype == FKV_DTYPE_BF16 ? 2 : 4;
-  const int64_t row_base = (int64_t)pv.hkv * pv.d;  // elements per source base row
+  const int64_t hb = (int64_t)pv.d * es;         // bytes of one head row
+  const int64_t bb = (int64_t)pv.hkv * hb;       // bytes of one source base row (all local heads)
+  const int64_t rb = (int64_t)pv.r * es;         // bytes of one residual row
+  const bool vec = (hb % 16) == 0 && (rb % 16) == 0 &&
+                   (((uintptr_t)kb | (uintptr_t)vb | (uintptr_t)rk | (uintptr_t)rv) & 15) == 0;
   for (int j = blockIdx.y; j < w.n; j += gridDim.y) {
     const int64_t src = w.src_row + j;
-    for (int h = 0; h < pv.hkv; ++h) {
-      const int64_t dst =
-          ((((int64_t)layer * pv.nb + w.base_page) * pv.hkv + h) * pv.P + (w.row0 + j)) * (int64_t)pv.d;
-      if (mask & FKV_WRITE_KBASE)
-        copy_elems((uint8_t*)pv.base_k + dst * es, kb + (src * row_base + (int64_t)h * pv.d) * es, pv.d, es,
-                   threadIdx.x, blockDim.x);
-      if (mask & FKV_WRITE_VBASE)
-        copy_elems((uint8_t*)pv.base_v + dst * es, vb + (src * row_base + (int64_t)h * pv.d) * es, pv.d, es,
-                   threadIdx.x, blockDim.x);
+    const int row = w.row0 + j;
+    const int64_t bdst0 = (((int64_t)layer * pv.nb + w.base_page) * pv.hkv * pv.P + row) * hb;  // head 0
+    const int64_t rdst = (((int64_t)layer * pv.nr + w.res_page) * pv.P + row) * rb;
+    if (vec) {
+      const int nbc = (int)(bb / 16), nrc = (int)(rb / 16);
+      const int swz = pv.res_swz && ((row >> 2) & 1);  // 2 chunks per residual row in the swizzled format
+      for (int i = threadIdx.x; i < 2 * nbc + 2 * nrc; i += blockDim.x) {
+        const uint8_t* sp;
+        uint8_t* dp;
+        if (i < 2 * nbc) {
+          const int v = i >= nbc, c = i - v * nbc;
+          if (!(mask & (v ? FKV_WRITE_VBASE : FKV_WRITE_KBASE))) continue;
+          const int64_t off = (int64_t)c * 16, h = off / hb;
+          sp = (v ? vb : kb) + src * bb + off;
+          dp = (uint8_t*)(v ? pv.base_v : pv.base_k) + bdst0 + h * pv.P * hb + (off - h * hb);
+        } else {
+          const int v = i - 2 * nbc >= nrc, c = i - 2 * nbc - v * nrc;
+          if (!(mask & (v ? FKV_WRITE_RV : FKV_WRITE_RK))) continue;
+          sp = (v ? rv : rk) + src * rb + c * 16;
+          dp = (uint8_t*)(v ? pv.res_v : pv.res_k) + rdst + (swz ? (c ^ 1) : c) * 16;
+        }
+        *(uint4*)dp = __ldg((const uint4*)sp);
+      }
+      continue;
     }
-    const int64_t rdst = (((int64_t)layer * pv.nr + w.res_page) * pv.P + (w.row0 + j)) * (int64_t)pv.r;
-    if (pv.res_swz && ((w.row0 + j) >> 2) & 1) {  // swizzled row: swap the two 8-element halves
+    for (int h = 0; h < pv.hkv; ++h) {
+      const int64_t dst = bdst0 + (int64_t)h * pv.P * hb;
+      if (mask & FKV_WRITE_KBASE)
+        copy_elems((uint8_t*)pv.base_k + dst, kb + src * bb + h * hb, pv.d, es, threadIdx.x, blockDim.x);
+      if (mask & FKV_WRITE_VBASE)
+        copy_elems((uint8_t*)pv.base_v + dst, vb + src * bb + h * hb, pv.d, es, threadIdx.x, blockDim.x);
+    }
+    if (pv.res_swz && (row >> 2) & 1) {  // swizzled row: swap the two 8-element halves
       const int hr = pv.r / 2;
       for (int hh = 0; hh < 2; ++hh) {
         if (mask & FKV_WRITE_RK)
-          copy_elems((uint8_t*)pv.res_k + (rdst + hh * hr) * es, rk + (src * pv.r + (1 - hh) * hr) * es, hr, es,
+          copy_elems((uint8_t*)pv.res_k + rdst + hh * hr * es, rk + (src * pv.r + (1 - hh) * hr) * es, hr, es,
                      threadIdx.x, blockDim.x);
         if (mask & FKV_WRITE_RV)
-          copy_elems((uint8_t*)pv.res_v + (rdst + hh * hr) * es, rv + (src * pv.r + (1 - hh) * hr) * es, hr, es,
+          copy_elems((uint8_t*)pv.res_v + rdst + hh * hr * es, rv + (src * pv.r + (1 - hh) * hr) * es, hr, es,
                      threadIdx.x, blockDim.x);
       }
     } else {
-      if (mask & FKV_WRITE_RK)
-        copy_elems((uint8_t*)pv.res_k + rdst * es, rk + src * pv.r * es, pv.r, es, threadIdx.x, blockDim.x);
-      if (mask & FKV_WRITE_RV)
-        copy_elems((uint8_t*)pv.res_v + rdst * es, rv + src * pv.r * es, pv.r, es, threadIdx.x, blockDim.x);
+      if (mask & FKV_WRITE_RK) copy_elems((uint8_t*)pv.res_k + rdst, rk + src * rb, pv.r, es, threadIdx.x, blockDim.x);
+      if (mask & FKV_WRITE_RV) copy_elems((uint8_t*)pv.res_v + rdst, rv + src * rb, pv.r, es, threadIdx.x, blockDim.x);
     }
   }
 }
@@ -370,12 +400,18 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnParams p) {
 
 cudaError_t launch_kv_write(const PoolView& pv, int32_t layer, const WriteRun* runs, int32_t n_runs, const void* kb,
                             const void* vb, const void* rk, const void* rv, uint32_t mask, cudaStream_t s) {
-  Runs<kMaxRuns> rr;
-  for (int i = 0; i < n_runs; ++i) rr.r[i] = runs[i];
   int maxn = 1;
   for (int i = 0; i < n_runs; ++i) maxn = max(maxn, runs[i].n);
   dim3 grid(n_runs, min(maxn, 16));
-  return launch_pdl(kv_write_kernel, grid, dim3(128), 0, s, pv, layer, rr, n_runs, (const uint8_t*)kb,
+  if (n_runs <= 64) {  // a decode step's runs: a 2-KB parameter block instead of 16 KB (launch cost)
+    Runs<64> rr;
+    for (int i = 0; i < n_runs; ++i) rr.r[i] = runs[i];
+    return launch_pdl(kv_write_kernel<64>, grid, dim3(256), 0, s, pv, layer, rr, n_runs, (const uint8_t*)kb,
+                      (const uint8_t*)vb, (const uint8_t*)rk, (const uint8_t*)rv, mask);
+  }
+  Runs<kMaxRuns> rr;
+  for (int i = 0; i < n_runs; ++i) rr.r[i] = runs[i];
+  return launch_pdl(kv_write_kernel<kMaxRuns>, grid, dim3(256), 0, s, pv, layer, rr, n_runs, (const uint8_t*)kb,
                     (const uint8_t*)vb, (const uint8_t*)rk, (const uint8_t*)rv, mask);
 }
 

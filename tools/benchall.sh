@@ -13,7 +13,7 @@ timeout 400 python bench.py --config c5 --steps 5 --no-cpu-baseline > $O/bench_c
 timeout 900 python bench.py --config c4 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_c4_none.json 2> $O/err_c4.txt
 timeout 400 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_c2_reference.json 2> $O/err_ref.txt
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --no-cpu-baseline --no-deferred --no-e2e > $O/bench_c2_2ranks_1gpu.json 2> $O/err_2ranks.txt
-timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ra_|combine|kv_write" -s 128 -c 128 --csv --log-file $O/launches_c2_none.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-deferred --no-graph > /dev/null 2>&1
+FKV_NVTX=1 timeout 400 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2_none.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-deferred --no-graph > /dev/null 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:ra_tc_kernel -s 3 -c 1 -o $O/prof_c2_none python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-deferred --no-graph > /dev/null 2>&1
 FKV_KERNEL=3 timeout 600 ncu --set full --import-source on --clock-control none -k regex:ra_rows -s 3 -c 1 -o $O/prof_c2_rows python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-deferred --no-graph > /dev/null 2>&1
 timeout 600 compute-sanitizer --tool racecheck --print-limit 10 python -m pytest tests/test_gpu_parity.py -q -k "test_c1_parity and tc-none" > $O/sanitizer_racecheck.txt 2>&1
