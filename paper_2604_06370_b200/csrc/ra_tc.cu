@@ -49,6 +49,10 @@ namespace {
 using namespace sm100;
 
 constexpr int kD = 128, kR = 16, kTile = 128, kMaxSlots = 8;
+#ifndef FKV_LAZY_START
+#define FKV_LAZY_START 1
+#endif
+constexpr bool kLazyStart = FKV_LAZY_START;  // first tile of a non-causal item: m = 0 reference (no column max)
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
@@ -1321,11 +1325,15 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
           uint64_t x2[16];
           float mx = -INFINITY;
+          // lazy start (NONE, 64 rows, items whose every query column sees every key): the first tile takes the
+          // running max m = 0 as its reference instead of computing the column maxima; the slow path below still
+          // runs when a score leaves [-64, 8] of it (p then stays within [2^-64, 2^8]: no bf16 / fp32 underflow)
+          const bool lazy0 = C::PVROW && kLazyStart && j == 0 && causal_mask == 0;
           {
             const float4* mp = (const float4*)&mrun[cb];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const float4 m4 = mp[q];
+              const float4 m4 = lazy0 ? make_float4(0.f, 0.f, 0.f, 0.f) : mp[q];
               const uint64_t s01 = f2(__uint_as_float(sr[4 * q]), __uint_as_float(sr[4 * q + 1]));
               const uint64_t s23 = f2(__uint_as_float(sr[4 * q + 2]), __uint_as_float(sr[4 * q + 3]));
               x2[2 * q] = fma2(s01, sc2, f2(-m4.x, -m4.y));
@@ -1351,7 +1359,16 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           // lazy rescaling: only when some score exceeds the running max by > 2^8
           float alpha_l = 1.f;  // this lane's column (cb + lane) rescale factor (row-sum partials)
           if (tid == 0) EV(20, T);
-          if (bar_or(bar_id, 128, mx > 8.0f)) {
+          bool out = mx > 8.0f;
+          if (lazy0) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              float a, b2;
+              uf2(x2[q], a, b2);
+              out |= (a < -64.f && a > -INFINITY) || (b2 < -64.f && b2 > -INFINITY);
+            }
+          }
+          if (bar_or(bar_id, 128, out)) {
             if (tid == 0) EV(21, T);
             // first tile of the item: every column is fresh (m = -inf), nothing to read back or rescale
             const bool first = j == 0;
@@ -1461,6 +1478,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               const float x1 = ok1 ? __uint_as_float(sr[2 * q + 1]) * scl - (m1 == -INFINITY ? 0.f : m1) : -INFINITY;
               x2[q] = f2(x0, x1);
             }
+          } else if (lazy0) {
+            // the reference stays: every warp of the warpgroup stores it for its chunk's columns (same value), and
+            // reads it back on the next tile after its own store
+            mrun[cb + lane] = 0.f;
+            __syncwarp();
           }
           // P^T row of this key (bf16, MN-major SW128), the chunk's columns
           uint32_t pk[16];
