@@ -479,9 +479,11 @@ def _timed(run, args, world, dist_ok, dev_index):
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
     if not run.events:
+        launches = run.launches   # gpu_launches counts the timed steps only
         for _ in range(args.steps):
             run.step(record=False, events=True)
         torch.cuda.synchronize()
+        run.launches = launches
     clocks = clk.stop()
     return ms, clocks
 

@@ -1213,6 +1213,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         }
         named_bar_sync(bar_id, 128);
       }
+      // lazy start: the item's running max is the m = 0 reference held in registers (lref) until a slow path moves
+      // it into m_run (no shared-memory stores from the fast path)
+      uint32_t lrefm = 0;  // bit ch: chunk ch runs on the register reference
       // PVROW: this thread's per-column partial row sums (its keys, fp32 p) over the item's tiles, pairs of columns;
       // reduced over the keys once at the item end
       uint64_t lsum2[C::PVROW ? NCH : 1][C::PVROW ? 16 : 1];
@@ -1329,11 +1332,12 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           // running max m = 0 as its reference instead of computing the column maxima; the slow path below still
           // runs when a score leaves [-64, 8] of it (p then stays within [2^-64, 2^8]: no bf16 / fp32 underflow)
           const bool lazy0 = C::PVROW && kLazyStart && j == 0 && causal_mask == 0;
+          const bool lref = (lrefm >> ch) & 1u;
           {
             const float4* mp = (const float4*)&mrun[cb];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const float4 m4 = lazy0 ? make_float4(0.f, 0.f, 0.f, 0.f) : mp[q];
+              const float4 m4 = (lazy0 || lref) ? make_float4(0.f, 0.f, 0.f, 0.f) : mp[q];
               const uint64_t s01 = f2(__uint_as_float(sr[4 * q]), __uint_as_float(sr[4 * q + 1]));
               const uint64_t s23 = f2(__uint_as_float(sr[4 * q + 2]), __uint_as_float(sr[4 * q + 3]));
               x2[2 * q] = fma2(s01, sc2, f2(-m4.x, -m4.y));
@@ -1377,11 +1381,13 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               const float4* mp = (const float4*)&mrun[cb];
 #pragma unroll
               for (int q = 0; q < 8; ++q) {
-                const float4 m4 = mp[q];
+                const float4 m4 = lref ? make_float4(0.f, 0.f, 0.f, 0.f) : mp[q];
                 mo[4 * q] = m4.x; mo[4 * q + 1] = m4.y; mo[4 * q + 2] = m4.z; mo[4 * q + 3] = m4.w;
               }
             }
-            const float mo_l = first ? -INFINITY : mrun[cb + lane];
+            const float mo_l = first ? -INFINITY : (lref ? 0.f : mrun[cb + lane]);
+            // the register reference becomes m_run's baseline before the atomics (ordered by the barrier below)
+            if (lref && wq == 0) mrun[cb + lane] = 0.f;
             float v[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
@@ -1478,11 +1484,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               const float x1 = ok1 ? __uint_as_float(sr[2 * q + 1]) * scl - (m1 == -INFINITY ? 0.f : m1) : -INFINITY;
               x2[q] = f2(x0, x1);
             }
+            lrefm &= ~(1u << ch);  // m_run holds the chunk's running max from here on
           } else if (lazy0) {
-            // the reference stays: every warp of the warpgroup stores it for its chunk's columns (same value), and
-            // reads it back on the next tile after its own store
-            mrun[cb + lane] = 0.f;
-            __syncwarp();
+            lrefm |= 1u << ch;  // the m = 0 reference stays (registers)
           }
           // P^T row of this key (bf16, MN-major SW128), the chunk's columns
           uint32_t pk[16];
@@ -1564,7 +1568,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           const int c = CPW * w + kl, o = c >> 4, r = c & 15;
           if (o < I.n_slots && r < R.n_rows[o]) {
             float* ent = p.ws + (int64_t)(R.entry_off[o] + r) * p.entry_stride;
-            ent[0] = mrun[c];
+            ent[0] = ((lrefm >> (kl >> 5)) & 1u) ? 0.f : mrun[c];  // column c = CPW w + kl is in chunk kl / 32
             ent[1] = lwb[c] + lwb[kRows + c] + lwb[2 * kRows + c] + lwb[3 * kRows + c];
           }
           mrun[c] = -INFINITY;  // this buffer's next item (ii + 2) starts fresh
