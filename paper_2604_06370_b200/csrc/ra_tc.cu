@@ -52,7 +52,13 @@ constexpr int kD = 128, kR = 16, kTile = 128, kMaxSlots = 8;
 #ifndef FKV_LAZY_START
 #define FKV_LAZY_START 1
 #endif
-constexpr bool kLazyStart = FKV_LAZY_START;  // first tile of a non-causal item: m = 0 reference (no column max)
+constexpr bool kLazyStart = FKV_LAZY_START;
+// diagnostics only (A/B builds, wrong output): skip loads / math to find the binding pipeline stage.
+// bit 1: K_base TMA, 2: V_base TMA, 4: R_k copies, 8: R_v copies, 16: key-warp exponentials (P = bf16(x))
+#ifndef FKV_DIAG_SKIP
+#define FKV_DIAG_SKIP 0
+#endif
+constexpr int kSkip = FKV_DIAG_SKIP;  // first tile of a non-causal item: m = 0 reference (no column max)
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
@@ -69,11 +75,23 @@ struct Cfg {
   // a deeper ring; P^T in 64-key halves so softmax(T+1) overlaps PV(T)
   // K_base ring in 16-KB d-half units (a 128-key tile = 2 units): 4 units = two whole tiles (one 3D TMA box per
   // tile); 128-row CTAs: 3 units (each d-half its own box, S(T+1)'s first half streams in while S(T) runs)
-  static constexpr int KU = kRowsT == 128 ? 3 : 4;
+#ifndef FKV_KU64
+#define FKV_KU64 4
+#endif
+#ifndef FKV_VS64
+#define FKV_VS64 3
+#endif
+#ifndef FKV_NPH64
+#define FKV_NPH64 4
+#endif
+#ifndef FKV_NQ64
+#define FKV_NQ64 2
+#endif
+  static constexpr int KU = kRowsT == 128 ? 3 : (kDef ? 4 : FKV_KU64);
   static constexpr int RS = 1;                      // R_k ring (4 KB per slot)
-  static constexpr int VS = kRowsT == 128 ? 2 : 3;  // V-side ring (64-key half of V_base | R_v per slot | ones)
-  static constexpr int NPH = kRowsT == 128 ? 2 : 4;  // P^T ring of 64-key halves (PV of half h needs only it)
-  static constexpr int NQ = (kDef || kRowsT == 128) ? 1 : 2;  // per-item Q / X buffers (freed by the S-side MMAs)
+  static constexpr int VS = kRowsT == 128 ? 2 : (kDef ? 3 : FKV_VS64);  // V-side ring (64-key half of V_base | R_v per slot | ones)
+  static constexpr int NPH = kRowsT == 128 ? 2 : (kDef ? 4 : FKV_NPH64);  // P^T ring of 64-key halves (PV of half h needs only it)
+  static constexpr int NQ = (kDef || kRowsT == 128) ? 1 : FKV_NQ64;  // per-item Q / X buffers (freed by the S-side MMAs)
   static constexpr int NRC = 4;  // per-item header ring (held by the key warps until the item's epilogue)
   // Accumulator layout switches (both measured on B200): split accumulation chains (SH / PAR = 2) do not help, a
   // tcgen05.mma costs ~120 cycles for N <= 128 whether or not it depends on the previous one
@@ -115,8 +133,8 @@ struct kDefOf<Cfg<D, R>> {
 };
 template <class C>
 struct MiscT {
-  uint64_t kfull[4], kempty[4], rfull[1], rempty[1], vfull[3], vempty[3], rvfull[3], qfull[2], qempty[2], sfull[2],
-      sfree[2], pfull[4], pfree[4], accfree[2], recfull[C::NRC], recempty[C::NRC], kl[kDefOf<C>::value ? 4 * kKlBufs : 1];  // kl: DEFERRED klfull | klready
+  uint64_t kfull[C::KU], kempty[C::KU], rfull[1], rempty[1], vfull[C::VS], vempty[C::VS], rvfull[C::VS], qfull[2],
+      qempty[2], sfull[2], sfree[2], pfull[C::NPH], pfree[C::NPH], accfree[2], recfull[C::NRC], recempty[C::NRC], kl[kDefOf<C>::value ? 4 * kKlBufs : 1];  // kl: DEFERRED klfull | klready
   // running column max (PVROW: two buffers by item parity, reset by the item's end, so items start barrier-free)
   alignas(16) float m_run[(C::PVROW ? 2 : 1) * C::ROWS];
   alignas(16) float lw[C::ONES ? 4 : (C::PVROW ? 2 : 1) * 4 * C::ROWS];  // row-sum partials per key warp [4][ROWS]
@@ -423,7 +441,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   // K ring: d-half h of tile T in unit (2T + h) % KU, its (2T + h) / KU-th use; one 3D box (one barrier) per tile
   // when the two units of a tile are adjacent (KU = 4, P = 128)
-  const bool k_single = C::KU == 4 && p.P == kTile;
+  const bool k_single = C::KU % 2 == 0 && p.P == kTile;
   auto k_unit = [](uint32_t T, int h) { return (int)((2 * T + h) % C::KU); };
   auto k_use = [](uint32_t T, int h) { return (2 * T + h) / C::KU; };
   auto k_free = [&](uint32_t T) {  // both units of tile T free (the S MMAs of their previous tile completed)
@@ -457,10 +475,10 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       mbar_init(smem_u32(&ms.qempty[i]), 1);  // S-side commit (the last MMA reading Q / X)
       mbar_init(smem_u32(&ms.sfull[i]), 1);
       mbar_init(smem_u32(&ms.sfree[i]), 256);
+    }
+    for (int i = 0; i < C::NPH; ++i) {
       mbar_init(smem_u32(&ms.pfull[i]), 128);  // the key threads of one 64-key half (both warpgroups)
       mbar_init(smem_u32(&ms.pfree[i]), 1);
-      mbar_init(smem_u32(&ms.pfull[2 + i]), 128);
-      mbar_init(smem_u32(&ms.pfree[2 + i]), 1);
     }
     for (int i = 0; i < C::NRC; ++i) {
       mbar_init(smem_u32(&ms.recfull[i]), p.P == kTile ? 32 : 1);
@@ -478,6 +496,8 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
     fence_mbar_init();
   }
   if (wid == 11) tmem_alloc(smem_u32(&ms.tmem_base), 512);
+  if (kSkip)  // diagnostics: skipped copies leave zeros (finite scores), not stale bytes
+    for (uint32_t c = tid; c < C::OFF_MISC / 16; c += 384) *(uint4*)(smem + 16 * c) = make_uint4(0, 0, 0, 0);
   for (int c = tid; c < (C::PVROW ? 2 : 1) * C::ROWS; c += 384) ms.m_run[c] = -INFINITY;
   // the all-ones R_v slot (index 4) of every V-side entry: A^T lanes 64..79 accumulate the row sums l
   if (C::ONES)
@@ -527,7 +547,10 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           if (k_free(nk)) {
             if (lane == 0) {
               EV(0, nk);
-              if (k_single) {
+              if (kSkip & 1) {
+                mbar_arrive(smem_u32(&ms.kfull[k_unit(nk, 0)]));
+                if (!k_single) mbar_arrive(smem_u32(&ms.kfull[k_unit(nk, 1)]));
+              } else if (k_single) {
                 const uint32_t bar = smem_u32(&ms.kfull[k_unit(nk, 0)]);
                 mbar_expect_tx(bar, 32768);
                 // base tiles stream through L2 evict-first: the residual pages (reused by every kv head) and
@@ -565,7 +588,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             const uint32_t dst = sbase + C::OFF_R + slot * C::RB;
 #pragma unroll
             for (int o = 0; o < kSlots; ++o) {
-              if ((rR.a.z >> (8 + o)) & 1) {
+              if (!(kSkip & 4) && ((rR.a.z >> (8 + o)) & 1)) {
                 const __nv_bfloat16* src = rkl + (int64_t)rR.page(o) * kTile * kR;
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -970,7 +993,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           for (int h = 0; h < 2; ++h) {
             const uint32_t nv = 2 * T + h, slot = nv % C::VS;
             if (nv >= (uint32_t)C::VS) wait_free(smem_u32(&ms.vempty[slot]), ((nv / C::VS) - 1) & 1);
-            if (lane == 0) {  // V_base 64-key half (16 KB, one 3D box)
+            if (lane == 0 && (kSkip & 2)) {
+              mbar_arrive(smem_u32(&ms.vfull[slot]));
+            } else if (lane == 0) {  // V_base 64-key half (16 KB, one 3D box)
               EV(7, nv);
               const uint32_t bar = smem_u32(&ms.vfull[slot]);
               mbar_expect_tx(bar, 16384);
@@ -982,7 +1007,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             const uint32_t dst = sbase + C::OFF_V + slot * C::VE + 16384;
 #pragma unroll
             for (int o = 0; o < kSlots; ++o) {
-              if (o < ns) {
+              if (!(kSkip & 8) && o < ns) {
                 const __nv_bfloat16* src = rvl + ((int64_t)rc.page(o) * kTile + 64 * h) * kR;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -1319,9 +1344,16 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             if (tid == 0) EV(3, T);
             tc_fence_after();
           }
+          if constexpr ((kSkip & 32) != 0) {  // diagnostics: null consumer (pipeline handshakes only)
+            tc_fence_before();
+            mbar_arrive(smem_u32(&ms.sfree[sb]));
+            if (np >= (uint32_t)C::NPH) mbar_wait(smem_u32(&ms.pfree[ps]), ((np / C::NPH) - 1) & 1);
+            continue;
+          }
           uint32_t sr[32];
           FKV_TMEM_LD32(tm + C::tS(sb, 0) + cb + lb, sr);
           tmem_ld_wait();
+          if (!kDef && tid == 0) EV(28, T);
           if (ch == NCH - 1) {
             tc_fence_before();
             mbar_arrive(smem_u32(&ms.sfree[sb]));
@@ -1372,7 +1404,9 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               out |= (a < -64.f && a > -INFINITY) || (b2 < -64.f && b2 > -INFINITY);
             }
           }
-          if (bar_or(bar_id, 128, out)) {
+          const bool slow_ = bar_or(bar_id, 128, out);
+          if (!kDef && tid == 0) EV(29, T);
+          if (slow_) {
             if (tid == 0) EV(21, T);
             // first tile of the item: every column is fresh (m = -inf), nothing to read back or rescale
             const bool first = j == 0;
@@ -1494,7 +1528,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           for (int q = 0; q < 16; ++q) {
             float a, b2;
             uf2(x2[q], a, b2);
-            const float ea = ex2(a), eb = ex2(b2);
+            const float ea = (kSkip & 16) ? a : ex2(a), eb = (kSkip & 16) ? b2 : ex2(b2);
             pk[q] = pack_bf16x2(ea, eb);
             if constexpr (C::PVROW) lsum2[ch][q] = fadd2(lsum2[ch][q], f2(ea, eb));
           }
@@ -1507,6 +1541,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           for (int q = 0; q < 4; ++q)
             *(uint4*)(pbuf + mnmajor_off(cb + q * 8, kl & 63, 8, 8192, 1024)) =
                 make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          if (!kDef && tid == 0) EV(11, T);
           if constexpr (!C::ONES && !C::PVROW) {
             // row sums l without an all-ones MMA slot: the warp's 32 keys summed per column (of the bf16 P the
             // MMA uses), lane l -> column cb + l; per-warp partials, rescaled with the running max
@@ -1532,6 +1567,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
         }
         fence_async_smem();
+        if (!kDef && tid == 0) EV(12, T);
         mbar_arrive(smem_u32(&ms.pfull[ps]));
         if (tid == 0) EV(4, T);
         if (C::AB > 1 && j == 0 && pend_ii >= 0) {

@@ -71,12 +71,22 @@ def main():
     print("items: P:Qitem / S:Qfull", [(int(d[9, i] - t0), int(d[10, i] - t0)) for i in range(64) if d[9, i]])
     print("key warps per item: start / end / epilogue done", [(int(d[25, i] - t0), int(d[26, i] - t0), int(d[27, i] - t0) if d[27, i] else -1) for i in range(64) if d[25, i]])
     if a.detail >= 0:
+        print("key-warp phases per tile (cycles from W:sfull): S loaded, pre-bar_or, post-bar_or, pfree wait/ok, P stored, "
+              "fenced, pfull, next sfull")
+        for T in range(a.detail, a.detail + 12):
+            b0 = d[3, T]
+            if not b0 or not d[3, T + 1]:
+                break
+            g = lambda e, i=T: int(d[e, i] - b0) if d[e, i] else -1
+            print(f"  T{T}: {g(28)} {g(20)} {g(29)} {g(16)}/{g(17)} {g(11)} {g(12)} {g(4)} {int(d[3, T + 1] - b0)}")
         T = a.detail
         base = d[0, T]
         f = lambda e, i: int(d[e, i] - base) if d[e, i] else -1
         print(f"tile {T} (cycles from its K issue): K issue 0, S kfull {f(1, T)}, S sfree {f(8, T)}, S commit {f(2, T)}, "
               f"W sfull {f(3, T)}, W pfree-wait {f(16, T)} ok {f(17, T)}, W pfull {f(4, T)}, PV pfull {f(5, T)}, "
               f"PV commit {f(18, T)}")
+        print(f"   key warps (NONE): sfull {f(3, T)}, S loaded {f(28, T)}, before bar_or {f(20, T)}, after bar_or {f(29, T)}, "
+              f"pfree-wait {f(16, T)} ok {f(17, T)}, P stored {f(11, T)}, fenced {f(12, T)}, pfull {f(4, T)}")
         print(f"   key warps: sfull {f(3, T)}, before bar_or {f(20, T)}, slow {f(21, T)}, pre-atomic {f(22, T)}, "
               f"post-atomic {f(23, T)}, pre-recompute {f(24, T)}, pfree-wait {f(16, T)}")
         for h in range(2):
