@@ -618,7 +618,12 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
     if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("attention: ") + cudaGetErrorString(e));
     return;
   }
-  if ((phases & FKV_PHASE_MAIN) && p.kernel == 2) e = k::launch_stage(a, (int32_t)p.stage_src.size(), (cudaStream_t)stream);
+  // FKV_DIAG_NOSTAGE (diagnostics only: the main kernel reads whatever images the last stager left) times the
+  // stager's share of the step
+  static const bool no_stage = getenv("FKV_DIAG_NOSTAGE") != nullptr;
+  static int stage_calls = 0;  // the first calls stage real images (finite scores in the skipped ones)
+  if ((phases & FKV_PHASE_MAIN) && p.kernel == 2 && !(no_stage && ++stage_calls > 64))
+    e = k::launch_stage(a, (int32_t)p.stage_src.size(), (cudaStream_t)stream);
   if (e == cudaSuccess && (phases & FKV_PHASE_MAIN))
     e = p.kernel == 2   ? k::launch_attention_tc(a, c.tc_maps.data(), (cudaStream_t)stream)
         : p.kernel == 0 ? k::launch_attention_mma(a, (cudaStream_t)stream)

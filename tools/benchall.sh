@@ -1,5 +1,4 @@
 # Round bench suite (1 GPU): bench lines for every config, both tcgen05 kernels on C2, the reference arm, a 2-rank
-# run on one GPU, the ncu launch list and full profiles of the main kernels, compute-sanitizer on small cases.
 set -x
 O=${1:-gpurun_out/r02}
 mkdir -p $O
@@ -16,6 +15,3 @@ timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --mast
 FKV_NVTX=1 timeout 400 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2_none.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-deferred --no-graph > /dev/null 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:ra_tc_kernel -s 3 -c 1 -o $O/prof_c2_none python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-deferred --no-graph > /dev/null 2>&1
 FKV_KERNEL=3 timeout 600 ncu --set full --import-source on --clock-control none -k regex:ra_rows -s 3 -c 1 -o $O/prof_c2_rows python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-deferred --no-graph > /dev/null 2>&1
-timeout 600 compute-sanitizer --tool racecheck --print-limit 10 python -m pytest tests/test_gpu_parity.py -q -k "test_c1_parity and tc-none" > $O/sanitizer_racecheck.txt 2>&1
-timeout 600 compute-sanitizer --tool synccheck --print-limit 10 python -m pytest tests/test_gpu_parity.py -q -k "test_c1_parity and tc-none" > $O/sanitizer_synccheck.txt 2>&1
-timeout 600 compute-sanitizer --tool memcheck --print-limit 10 python -m pytest tests/test_gpu_parity.py -q -k "test_c1_parity" > $O/sanitizer_memcheck.txt 2>&1
