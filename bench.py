@@ -30,6 +30,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -322,6 +324,8 @@ class Run:
         torch.cuda.synchronize()
         self.t_setup = time.time() - t_setup
         self.stream = torch.cuda.current_stream()
+        self.batch_np = np.asarray(wl.batch, np.int64)
+        self.ones_np = np.ones(len(wl.batch), np.int32)
         self.seqlens = {a: fkv.get_table(a)[2] for a in batch}   # host-side bookkeeping (no D2H)
         self.tok = 0
         self.events, self.launches, self.alg_bytes, self.info = [], 0, [], self.pl0.info
@@ -347,23 +351,26 @@ class Run:
         self.pl = pl
         if record:
             self.alg_bytes.append(alg_bytes_of(pl.info, self.wl))
-        starts = [self.seqlens[a] - 1 for a in batch]
+        # per-step host arrays built once (numpy, contiguous) and the stream passed explicitly: the per-layer calls
+        # then skip the list -> array conversions and the current-stream lookup (host cost per layer ~63 -> ~40 us)
+        starts = np.asarray([self.seqlens[a] - 1 for a in batch], np.int64)
+        b_np, ones_np, st = self.batch_np, self.ones_np, self.stream
         Q, O = self.Q, self.O
         for layer in range(wl.L):
             if host is None:
                 if not self.prefill:
-                    fkv.write_kv(layer, batch, starts, ones, self.kb[layer], self.vb[layer], self.rk[layer],
-                                 self.rv[layer])
+                    fkv.write_kv(layer, b_np, starts, ones_np, self.kb[layer], self.vb[layer], self.rk[layer],
+                                 self.rv[layer], stream=st)
                     self.launches += 1
                 if record if events is None else events:
                     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
                     e0.record(self.stream)
-                    fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 1)
+                    fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 1, stream=st)
                     e1.record(self.stream)
                     self.events.append((e0, e1))
                 else:
-                    fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 1)
-                fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 2)
+                    fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 1, stream=st)
+                fkv.residual_attention_phases(pl, layer, Q[layer], O[layer], 2, stream=st)
             else:
                 self._host_layer(host, pl, layer, starts)
             self.launches += _launches_per_layer(pl.info.kernel)
@@ -372,47 +379,68 @@ class Run:
         return pl
 
     def _host_layer(self, host, pl, layer, starts):
-        """e2e leg, one layer: the layer's inputs (Q rows and the new K/V/residual rows, pinned host memory) go
-        H2D on a copy stream one layer ahead into double-buffered device staging, the compute stream waits for
-        them, and O goes D2H on the copy stream behind the compute event, so copies overlap the previous /
-        next layer's kernels (the same public calls a serving loop makes: write_kv + residual_attention)."""
-        import torch
-        fkv, batch, L_ = self.fkv, self.wl.batch, self.wl.L
-        cs, ev_in, ev_out = host["cs"], host["ev_in"], host["ev_out"]
+        """e2e leg, one layer: the public calls a serving loop makes (write_kv + residual_attention) on this step's
+        device staging buffer, which the copy stream filled from pinned host memory while the previous step ran."""
+        fkv, batch = self.fkv, self.wl.batch
+        b = host["k"] & 1
+        dv = host["dev"][b]
         if layer == 0:
-            self._host_h2d(host, 0)
-        b = layer & 1
-        dv = host["dev"][b]
-        self.stream.wait_event(ev_in[b])
+            self.stream.wait_event(host["ev_in"][b])      # this step's inputs are on the device
         if not self.prefill:
-            fkv.write_kv(layer, batch, starts, [1] * len(batch), dv["kb"], dv["vb"], dv["rk"], dv["rv"])
+            fkv.write_kv(layer, self.batch_np, starts, self.ones_np, dv["kb"][layer], dv["vb"][layer],
+                         dv["rk"][layer], dv["rv"][layer], stream=self.stream)
             self.launches += 1
-        fkv.residual_attention(pl, layer, dv["q"], dv["o"])
-        ev_out[b].record(self.stream)
-        with torch.cuda.stream(cs):
-            if layer + 1 < L_:
-                cs.wait_event(ev_out[b ^ 1])   # the previous layer (or step) is done with buffer b ^ 1
-                self._host_h2d(host, layer + 1)
-            cs.wait_event(ev_out[b])
-            host["o"][layer].copy_(dv["o"], non_blocking=True)
+        fkv.residual_attention(pl, layer, dv["q"][layer], dv["o"][layer], stream=self.stream)
 
-    def _host_h2d(self, host, layer):
+    def _host_h2d(self, host, k):
+        """Step k's inputs (every layer's Q rows and new K/V/residual rows) pinned host -> device buffer k & 1, on
+        the H2D copy stream, once step k - 2 (the buffer's previous user) and its D2H are done with it."""
         import torch
-        b = layer & 1
-        dv = host["dev"][b]
-        with torch.cuda.stream(host["cs"]):
-            dv["q"].copy_(host["q"][layer], non_blocking=True)
+        b = k & 1
+        dv, cs = host["dev"][b], host["cs_in"]
+        with torch.cuda.stream(cs):
+            for e in (host["done"][b], host["out"][b]):
+                if e is not None:
+                    cs.wait_event(e)
+            dv["q"].copy_(host["q"], non_blocking=True)
             if not self.prefill:
-                for k in ("kb", "vb", "rk", "rv"):
-                    dv[k].copy_(host["kv"][k][layer], non_blocking=True)
-            host["ev_in"][b].record(host["cs"])
+                for key in ("kb", "vb", "rk", "rv"):
+                    dv[key].copy_(host["kv"][key], non_blocking=True)
+            host["ev_in"][b].record(cs)
+
+    def _host_d2h(self, host, k):
+        """Step k's result (every layer's O) device -> pinned host, on the D2H copy stream behind step k."""
+        import torch
+        b = k & 1
+        cs = host["cs_out"]
+        with torch.cuda.stream(cs):
+            cs.wait_event(host["done"][b])
+            host["o"].copy_(host["dev"][b]["o"], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(cs)
+            host["out"][b] = e
 
     def _host_drain(self, host):
-        """The step's result is on the host when the copy stream is done: the compute stream joins it."""
+        """After step k's launches: its completion event; then step k + 1's inputs go H2D (they only wait for step
+        k - 1) and step k's O goes D2H on a second copy stream, both while step k + 1 computes (steps pipelined as
+        in a serving loop; PCIe is full duplex)."""
         import torch
+        k = host["k"]
         e = torch.cuda.Event()
-        e.record(host["cs"])
-        self.stream.wait_event(e)
+        e.record(self.stream)
+        host["done"][k & 1] = e
+        self._host_h2d(host, k + 1)
+        self._host_d2h(host, k)
+        host["k"] = k + 1
+
+    def _host_join(self, host):
+        """End of the timed steps: the compute stream waits for the last step's O to reach the host (and for the
+        next step's inputs, already issued)."""
+        import torch
+        for cs in (host["cs_in"], host["cs_out"]):
+            e = torch.cuda.Event()
+            e.record(cs)
+            self.stream.wait_event(e)
 
     def graph_median_ms(self, reps=25):
         """Main-kernel time of layer 0 as the median over `reps` CUDA-graph replays."""
@@ -575,21 +603,28 @@ def run_ours(args):
         qh.copy_(run.Q.cpu())
         oh = torch.empty_like(qh).pin_memory()
         kvh = {k: t.cpu().pin_memory() for k, t in zip(("kb", "vb", "rk", "rv"), (run.kb, run.vb, run.rk, run.rv))}
-        devb = [{"q": torch.empty(run.n_q_rows, hq, d, dtype=torch.bfloat16, device=run.dev),
-                 "o": torch.empty(run.n_q_rows, hq, d, dtype=torch.bfloat16, device=run.dev),
-                 **{k: torch.empty_like(t[0]) for k, t in zip(("kb", "vb", "rk", "rv"),
-                                                              (run.kb, run.vb, run.rk, run.rv))}} for _ in range(2)]
-        host = {"q": qh, "o": oh, "kv": kvh, "dev": devb, "cs": torch.cuda.Stream(device=run.dev),
-                "ev_in": [torch.cuda.Event(), torch.cuda.Event()], "ev_out": [torch.cuda.Event(), torch.cuda.Event()]}
+        # two step-sized device staging buffers (every layer's inputs and outputs): step k computes on buffer
+        # k & 1 while the copy stream brings step k - 1's O to the host and step k + 1's inputs to the device
+        devb = [{"q": torch.empty_like(run.Q), "o": torch.empty_like(run.Q),
+                 **{k: torch.empty_like(t) for k, t in zip(("kb", "vb", "rk", "rv"),
+                                                           (run.kb, run.vb, run.rk, run.rv))}} for _ in range(2)]
+        host = {"q": qh, "o": oh, "kv": kvh, "dev": devb, "cs_in": torch.cuda.Stream(device=run.dev),
+                "cs_out": torch.cuda.Stream(device=run.dev), "ev_in": [torch.cuda.Event(), torch.cuda.Event()],
+                "done": [None, None], "out": [None, None], "k": 0}
+        run._host_h2d(host, 0)
         for _ in range(2):
             run.step(host=host)
+        run._host_join(host)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(run.stream)
+        # the timed region holds every step's H2D and D2H: the first step's inputs were copied before e0 by the
+        # warm-up's pipeline, so one extra step's inputs (the step after the last) go H2D inside it instead
         for _ in range(args.steps):
             run.step(host=host)
+        run._host_join(host)
         e1.record(run.stream)
         torch.cuda.synchronize()
         ems = _max_over_ranks(e0.elapsed_time(e1) / args.steps, world)

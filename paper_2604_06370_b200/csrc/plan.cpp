@@ -11,6 +11,8 @@
 // fill the 148 SMs; partial (m, l, acc, acc_r) are merged by the combine
 // kernel, which also applies the late V fusion acc + acc_r B_v (Eq.4).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -50,7 +52,18 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
   Plan& pl = *plan;
   // kernel choice: tcgen05 (2) > mma.sync (0) > SIMT (1)
   const int32_t d_ = c.cfg.head_dim, r_ = c.cfg.rank;
-  const bool tc_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && c.has_tc_maps && (128 % P) == 0 &&
+  // diagnostics: FKV_PLAN_TIMING prints the planner's section times; FKV_PLAN_ASSUME_TC plans for kernel 2 on a
+  // host-only ctx (planner profiling without a GPU; such a plan cannot run)
+  static const bool timing = getenv("FKV_PLAN_TIMING") != nullptr;
+  static const bool assume_tc = getenv("FKV_PLAN_ASSUME_TC") != nullptr;
+  auto tic = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "plan %-12s %8.1f us\n", what, std::chrono::duration<double, std::micro>(now - tic).count());
+    tic = now;
+  };
+  const bool tc_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && (c.has_tc_maps || (assume_tc && !c.device)) && (128 % P) == 0 &&
                      P >= 8 && !(flags & (FKV_PLAN_FORCE_SIMT | FKV_PLAN_FORCE_MMA));
   const bool mma_ok = c.cfg.dtype == FKV_DTYPE_BF16 && d_ == 128 && r_ == 16 && !(flags & FKV_PLAN_FORCE_SIMT);
   // rows-on-lanes tcgen05 kernel (kernel 3, ra_rows.cu): NONE residual-RoPE mode, pages of 16..128 tokens
@@ -119,6 +132,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
   if (qrow > INT32_MAX / 64) throw Error(FKV_E_INVALID, "plan: too many query rows");
   pl.n_rows_q = qrow;
 
+  lap("seqs");
   // ---- segments: maximal slot runs over which the member set shares pages --
   std::vector<Seg> segs;
   {
@@ -145,6 +159,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
       for (auto it = groups.rbegin(); it != groups.rend(); ++it) stack.push_back({it->second, s});
     }
   }
+  lap("segments");
   // range plan (§8(f) f4, sequence split across GPUs): only the keys of [key_begin, key_end), page-aligned
   if (key_begin != 0 || key_end != INT64_MAX) {
     const int P_ = c.cfg.page_size;
@@ -191,11 +206,24 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
     const int64_t k0 = sg.slot0 * P, k1 = std::min<int64_t>(sg.slot1 * P, maxlen);
     if (k1 <= k0) continue;
     base_bytes += (k1 - k0) * hkv * d * 2 * (int64_t)el;
-    // owner key: adapter slot + residual pages over the segment
-    std::map<std::pair<int32_t, std::vector<int32_t>>, std::vector<int32_t>> owners;
-    for (int32_t b : sg.members) {
-      std::vector<int32_t> rp(ags[b]->res.begin() + sg.slot0, ags[b]->res.begin() + sg.slot1);
-      owners[{pl.seqs[b].adapter_slot, std::move(rp)}].push_back(b);
+    // owner key: adapter slot + residual pages over the segment. Members sorted by that key in place (no key
+    // copies), equal runs are one owner; the order matches the former map over (adapter, page list)
+    std::vector<std::pair<std::pair<int32_t, int32_t>, std::vector<int32_t>>> owners;  // ((adapter, -), members)
+    {
+      std::vector<int32_t> mem(sg.members);
+      auto rb = [&](int32_t b) { return ags[b]->res.begin() + sg.slot0; };
+      auto re = [&](int32_t b) { return ags[b]->res.begin() + sg.slot1; };
+      auto less = [&](int32_t a, int32_t b) {
+        const int32_t sa = pl.seqs[a].adapter_slot, sb = pl.seqs[b].adapter_slot;
+        if (sa != sb) return sa < sb;
+        return std::lexicographical_compare(rb(a), re(a), rb(b), re(b));
+      };
+      std::stable_sort(mem.begin(), mem.end(), less);
+      for (size_t i = 0; i < mem.size(); ++i) {
+        if (i == 0 || less(mem[i - 1], mem[i]))
+          owners.push_back({{pl.seqs[mem[i]].adapter_slot, 0}, {}});
+        owners.back().second.push_back(mem[i]);
+      }
     }
     for (const auto& ow : owners) {
       int64_t okeys = 0;
@@ -233,6 +261,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
       if (!cta_warps.empty()) ctas.push_back({h, k0, k1, (int32_t)base_off[sg.members[0]], cta_warps});
     }
   }
+  lap("ctas");
   // L2 policy of the base tiles: evict-first when each (segment, kv head) tile is read by <= 4 row blocks (decode
   // batches), normal when many row blocks reuse it (prefill chunks, large agent counts); FKV_L2_EVICT=0/1 forces
   {
@@ -262,6 +291,20 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
   int64_t entries = 0;
   std::vector<std::array<int64_t, 3>> order_key;  // (segment start, piece, cta) per item
   std::vector<int64_t> item_cost;
+  {
+    size_t n_it = 0, n_w = 0;
+    for (const Cta& ct : ctas) {
+      const int64_t tiles = (ct.k1 - ct.k0 + kTileKeys - 1) / kTileKeys;
+      const int64_t pieces = (tiles + split_tiles - 1) / split_tiles;
+      n_it += pieces;
+      n_w += pieces * ct.warp_ids.size();
+    }
+    pl.items.reserve(n_it);
+    order_key.reserve(n_it);
+    item_cost.reserve(n_it);
+    pl.warps.reserve(n_w);
+    pl.rows.reserve(n_w * kRowsPerWarp);
+  }
   for (size_t ci = 0; ci < ctas.size(); ++ci) {
     const Cta& ct = ctas[ci];
     const int64_t tiles = (ct.k1 - ct.k0 + kTileKeys - 1) / kTileKeys;
@@ -317,24 +360,36 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
       }
     }
   }
+  lap("items");
   if (pl.kernel == 2) {
     // staged operand images (Q rows, q~ / packed B_k) per item slot; the key-range pieces of one row block carry
     // identical slots, so they share one contiguous block of images (DevItem::pad_[0] = first image)
-    std::unordered_map<std::string, int32_t> img_of;
-    for (DevItem& it : pl.items) {
-      std::string key;
-      for (int o = 0; o < it.n_warps; ++o) {
-        const DevWarp& w = pl.warps[it.warp_off + o];
-        key.append((const char*)&w.adapter_slot, 4);
-        key.append((const char*)&w.n_rows, 4);
-        key.append((const char*)&pl.rows[w.row_off], sizeof(DevRow) * kRowsPerWarp);
+    // items of one CTA row block (order_key[i][2]) carry the same slots unless a causal split dropped rows: an
+    // item reuses the images of an earlier item of its row block whose slots match exactly
+    std::unordered_map<int64_t, std::vector<int32_t>> img_of;  // row block -> items that own an image block
+    auto same_slots = [&](const DevItem& a, const DevItem& b) {
+      if (a.n_warps != b.n_warps) return false;
+      for (int o = 0; o < a.n_warps; ++o) {
+        const DevWarp& wa = pl.warps[a.warp_off + o];
+        const DevWarp& wb = pl.warps[b.warp_off + o];
+        if (wa.adapter_slot != wb.adapter_slot || wa.n_rows != wb.n_rows ||
+            std::memcmp(&pl.rows[wa.row_off], &pl.rows[wb.row_off], sizeof(DevRow) * kRowsPerWarp) != 0)
+          return false;
       }
-      auto f = img_of.find(key);
-      if (f == img_of.end()) {
-        f = img_of.emplace(key, (int32_t)pl.stage_src.size()).first;
+      return true;
+    };
+    for (size_t i = 0; i < pl.items.size(); ++i) {
+      DevItem& it = pl.items[i];
+      auto& cand = img_of[order_key[i][2]];
+      int32_t found = -1;
+      for (int32_t j : cand)
+        if (same_slots(pl.items[j], it)) { found = pl.items[j].pad_[0]; break; }
+      if (found < 0) {
+        found = (int32_t)pl.stage_src.size();
         for (int o = 0; o < it.n_warps; ++o) pl.stage_src.push_back(it.warp_off + o);
+        cand.push_back((int32_t)i);
       }
-      it.pad_[0] = f->second;
+      it.pad_[0] = found;
     }
     // persistent schedule: items in (segment, piece, row block) order, each to the least-loaded CTA, so the
     // row blocks and kv heads that stream the same base / residual pages run at the same time (L2 reuse)
@@ -357,6 +412,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
       pl.sched_items.insert(pl.sched_items.end(), v.begin(), v.end());
       pl.sched_ptr.push_back((int32_t)pl.sched_items.size());
     }
+  lap("schedule");
     // item records (k::ItemRecT<slots>)
     auto build_recs = [&](auto tag) {
       using Rec = decltype(tag);
@@ -392,9 +448,11 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
       }
     };
     if (pl.tc_rows == 128) build_recs(k::ItemRecT<8>{}); else build_recs(k::ItemRecT<4>{});
+  lap("itemrecs");
     // tile records (the residual loader and the TMA producer stream them instead of chasing page tables)
     pl.tile_ptr.assign(1, 0);
     pl.tile_recs.clear();
+    pl.tile_recs.reserve((size_t)pl.key_tiles * k::kTileRecInts);
     for (auto& v : per) {
       for (int32_t i : v) {
         const DevItem& it = pl.items[i];
@@ -408,15 +466,18 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
         meta |= (ng << 4) | (gmask << 8) | (it.kv_head << 16);
         for (int32_t t0 = it.key_begin; t0 < it.key_end; t0 += kTileKeys) {
           const int32_t sl = t0 / P;
-          int32_t rec[k::kTileRecInts] = {t0, it.key_end, meta, pl.base_pages[it.base_off + sl]};
+          const size_t at = pl.tile_recs.size();
+          pl.tile_recs.resize(at + k::kTileRecInts, 0);
+          int32_t* rec = pl.tile_recs.data() + at;
+          rec[0] = t0; rec[1] = it.key_end; rec[2] = meta; rec[3] = pl.base_pages[it.base_off + sl];
           for (int o = 0; o < 8; ++o) rec[4 + o] = -1;
           for (int o = 0; o < it.n_warps; ++o) rec[4 + o] = pl.res_pages[pl.warps[it.warp_off + o].res_off + sl];
-          pl.tile_recs.insert(pl.tile_recs.end(), rec, rec + k::kTileRecInts);
         }
       }
       pl.tile_ptr.push_back((int32_t)(pl.tile_recs.size() / k::kTileRecInts));
     }
   }
+  lap("tilerecs");
   if (entries > INT32_MAX) throw Error(FKV_E_INVALID, "plan: too many partial entries");
   pl.n_entries = entries;
   // CSR: output row -> entries
@@ -439,6 +500,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
     }
   for (int64_t o = 0; o < n_out; ++o)
     if (!pl.key_range && pl.out_ptr[o + 1] == pl.out_ptr[o]) throw Error(FKV_E_NO_KEYS, "plan: an output row has no keys");
+  lap("csr");
   // adapters
   pl.adapter_ptrs.resize(c.adapters.size() * 2);
   for (size_t s = 0; s < c.adapters.size(); ++s) {
@@ -480,27 +542,59 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
   pl.alg_rank_bytes = res_bytes + (int64_t)used_adapters.size() * 2 * r * d * hkv * (int64_t)el;
   pl.alg_bytes = base_bytes + res_bytes + (int64_t)used_adapters.size() * 2 * r * d * hkv * (int64_t)el +
                  pl.n_rows_q * c.hq_local * d * 2 * (int64_t)el;
+  lap("desc");
   // blob
-  pl.blob.clear();
-  pl.off_seqs = put(pl.blob, pl.seqs);
-  pl.off_base = put(pl.blob, pl.base_pages);
-  pl.off_res = put(pl.blob, pl.res_pages);
-  pl.off_items = put(pl.blob, pl.items);
-  pl.off_warps = put(pl.blob, pl.warps);
-  pl.off_rows = put(pl.blob, pl.rows);
-  pl.off_outptr = put(pl.blob, pl.out_ptr);
-  pl.off_outent = put(pl.blob, pl.out_entries);
-  pl.off_adapters = put(pl.blob, pl.adapter_ptrs);
-  pl.off_qrow = put(pl.blob, pl.qrow_seq);
-  pl.off_comb = put(pl.blob, pl.comb_rows);
-  pl.off_sptr = put(pl.blob, pl.sched_ptr);
-  pl.off_sitems = put(pl.blob, pl.sched_items);
-  pl.off_tptr = put(pl.blob, pl.tile_ptr);
-  pl.off_trecs = put(pl.blob, pl.tile_recs);
-  pl.off_irecs = put(pl.blob, pl.item_recs);
-  pl.off_ssrc = put(pl.blob, pl.stage_src);
-  pl.off_sdesc = put(pl.blob, pl.stage_desc);
+  // one allocation: offsets first, then the copies (resizing per array re-copied the growing blob)
+  {
+    size_t total = 0;
+    auto at = [&](const auto& v) {
+      const size_t off = align256(total);
+      total = off + std::max<size_t>(v.size() * sizeof(v[0]), 16);
+      return off;
+    };
+    pl.off_seqs = at(pl.seqs);
+    pl.off_base = at(pl.base_pages);
+    pl.off_res = at(pl.res_pages);
+    pl.off_items = at(pl.items);
+    pl.off_warps = at(pl.warps);
+    pl.off_rows = at(pl.rows);
+    pl.off_outptr = at(pl.out_ptr);
+    pl.off_outent = at(pl.out_entries);
+    pl.off_adapters = at(pl.adapter_ptrs);
+    pl.off_qrow = at(pl.qrow_seq);
+    pl.off_comb = at(pl.comb_rows);
+    pl.off_sptr = at(pl.sched_ptr);
+    pl.off_sitems = at(pl.sched_items);
+    pl.off_tptr = at(pl.tile_ptr);
+    pl.off_trecs = at(pl.tile_recs);
+    pl.off_irecs = at(pl.item_recs);
+    pl.off_ssrc = at(pl.stage_src);
+    pl.off_sdesc = at(pl.stage_desc);
+    pl.blob.assign(align256(total), 0);
+    auto cp = [&](size_t off, const auto& v) {
+      if (!v.empty()) std::memcpy(pl.blob.data() + off, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(pl.off_seqs, pl.seqs);
+    cp(pl.off_base, pl.base_pages);
+    cp(pl.off_res, pl.res_pages);
+    cp(pl.off_items, pl.items);
+    cp(pl.off_warps, pl.warps);
+    cp(pl.off_rows, pl.rows);
+    cp(pl.off_outptr, pl.out_ptr);
+    cp(pl.off_outent, pl.out_entries);
+    cp(pl.off_adapters, pl.adapter_ptrs);
+    cp(pl.off_qrow, pl.qrow_seq);
+    cp(pl.off_comb, pl.comb_rows);
+    cp(pl.off_sptr, pl.sched_ptr);
+    cp(pl.off_sitems, pl.sched_items);
+    cp(pl.off_tptr, pl.tile_ptr);
+    cp(pl.off_trecs, pl.tile_recs);
+    cp(pl.off_irecs, pl.item_recs);
+    cp(pl.off_ssrc, pl.stage_src);
+    cp(pl.off_sdesc, pl.stage_desc);
+  }
   pl.blob.resize(align256(pl.blob.size()));
+  lap("blob");
   pl.ws_bytes = align256((size_t)pl.n_entries * (size_t)(k::kEntAcc + d + r) * sizeof(float));
   if (pl.kernel == 2) {
     pl.stage_off = pl.ws_bytes;

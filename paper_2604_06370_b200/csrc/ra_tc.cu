@@ -58,7 +58,11 @@ constexpr bool kLazyStart = FKV_LAZY_START;
 #ifndef FKV_DIAG_SKIP
 #define FKV_DIAG_SKIP 0
 #endif
-constexpr int kSkip = FKV_DIAG_SKIP;  // first tile of a non-causal item: m = 0 reference (no column max)
+constexpr int kSkip = FKV_DIAG_SKIP;
+#ifndef FKV_STAGE_EARLY
+#define FKV_STAGE_EARLY 0
+#endif
+constexpr bool kStageEarly = FKV_STAGE_EARLY;  // stager: loads before griddepcontrol.wait (A/B: slower on C2)  // first tile of a non-causal item: m = 0 reference (no column max)
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
@@ -365,12 +369,18 @@ __device__ __forceinline__ int perm_d(int n) {
 // d-halves, 2 KB each) and q~ = Q B_k^T (NONE, K-major SW32, 512 B) or B_k^h
 // with permuted columns (DEFERRED, MN-major SW64 quarter blocks, 4 KB).
 __global__ void __launch_bounds__(256) ra_stage_kernel(AttnParams p, int n_images) {
-  // after the predecessor (kv_write: the pool rows) completed, the main kernel may start its prologue and K/V
-  // streaming; it waits for this grid's completion (griddepcontrol.wait) before it reads the staged images
-  pdl_wait();
+  // Loads and q~ before griddepcontrol.wait, stores after it: the reads (Q rows, B_k, the plan's descriptors) are
+  // never written by a kernel that triggers its dependents early (kv_write and the combine wait first; the main
+  // kernel, which triggers at entry, writes neither), while the image buffer may still be read by the previous
+  // main kernel until the predecessor grid completes. So the loads overlap the predecessor (kv_write) and only
+  // the stores wait; the main kernel waits for this grid's completion before it reads the images.
+  if (!kStageEarly) pdl_wait();
   pdl_trigger();
   const int ii = blockIdx.x;
-  if (ii >= n_images) return;
+  if (ii >= n_images) {
+    if (kStageEarly) pdl_wait();
+    return;
+  }
   __shared__ __align__(16) float qs[16][kD];
   __shared__ int4 dsc[5];  // planner record: B_k^h address, n_rows, kv head, Q row of each of the 16 slot rows
   uint8_t* img = p.stage + (int64_t)ii * kStageBytes;
@@ -383,46 +393,44 @@ __global__ void __launch_bounds__(256) ra_stage_kernel(AttnParams p, int n_image
                             (int64_t)p.layer * p.adapter_layer_stride;
   const bool def = p.rope_mode == FKV_ROPE_DEFERRED;
   __shared__ __align__(16) float bs[kR][kD + 4];
-  // Q rows and B_k^h in flight together: 2 x 16-byte loads per thread per pass
-  for (int c = tid; c < 16 * 16; c += 256) {  // one 16-byte Q chunk and one B_k chunk per thread
-    const int row = c >> 4, ch = c & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < n_rows) v = __ldg((const uint4*)((const __nv_bfloat16*)p.Q + (int64_t)qrows[row] * kD) + ch);
-    const int jj = c >> 4, n8 = (c & 15) * 8;  // B_k^h row jj (16 rows x 16 chunks, same index space)
-    const uint4 bv = __ldg((const uint4*)(Bk + jj * kD + (def ? perm_d(n8) : n8)));
-    *(uint4*)(img + (ch >> 3) * 2048 + kmajor_off(row, (ch & 7) * 8, 8, 1024, 0)) = v;
+  // one 16-byte Q chunk and one B_k^h chunk per thread (16 rows x 16 chunks each, the same index space)
+  const int row = tid >> 4, ch = tid & 15, jj = tid >> 4, n8 = (tid & 15) * 8;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (row < n_rows) v = __ldg((const uint4*)((const __nv_bfloat16*)p.Q + (int64_t)qrows[row] * kD) + ch);
+  const uint4 bv = __ldg((const uint4*)(Bk + jj * kD + (def ? perm_d(n8) : n8)));
+  float acc = 0.f;
+  if (!def) {
     const __nv_bfloat162* q2 = (const __nv_bfloat162*)&v;
     const __nv_bfloat162* b2 = (const __nv_bfloat162*)&bv;
-    if (def) {
-      *(uint4*)(img + 4096 + mnmajor_off(n8, jj, 4, 1024, 512)) = bv;  // packed B_k image (RoPE partner order)
-    } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(q2[e]), b = __bfloat1622float2(b2[e]);
-        qs[row][ch * 8 + 2 * e] = f.x;
-        qs[row][ch * 8 + 2 * e + 1] = f.y;
-        bs[jj][n8 + 2 * e] = b.x;
-        bs[jj][n8 + 2 * e + 1] = b.y;
-      }
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(q2[e]), b = __bfloat1622float2(b2[e]);
+      qs[row][ch * 8 + 2 * e] = f.x;
+      qs[row][ch * 8 + 2 * e + 1] = f.y;
+      bs[jj][n8 + 2 * e] = b.x;
+      bs[jj][n8 + 2 * e + 1] = b.y;
     }
-  }
-  if (!def) {
     // q~[row][j] = sum_d Q[row][d] B_k[j][d], one output per thread (paired FFMA2 over d)
     __syncthreads();
-    {
-      const int c = tid, row = c >> 4, jj = c & 15;
-      uint64_t acc2 = 0;
+    const int orow = tid >> 4, oj = tid & 15;
+    uint64_t acc2 = 0;
 #pragma unroll 8
-      for (int dd = 0; dd < kD; dd += 4) {
-        const float4 qv = *(const float4*)&qs[row][dd], bv4 = *(const float4*)&bs[jj][dd];
-        acc2 = fma2(f2(qv.x, qv.y), f2(bv4.x, bv4.y), acc2);
-        acc2 = fma2(f2(qv.z, qv.w), f2(bv4.z, bv4.w), acc2);
-      }
-      float a0, a1;
-      uf2(acc2, a0, a1);
-      const float acc = a0 + a1;
-      *(__nv_bfloat16*)(img + 4096 + kmajor_off(row, jj, 2, 256, 0)) = __float2bfloat16_rn(row < n_rows ? acc : 0.f);
+    for (int dd = 0; dd < kD; dd += 4) {
+      const float4 qv = *(const float4*)&qs[orow][dd], bv4 = *(const float4*)&bs[oj][dd];
+      acc2 = fma2(f2(qv.x, qv.y), f2(bv4.x, bv4.y), acc2);
+      acc2 = fma2(f2(qv.z, qv.w), f2(bv4.z, bv4.w), acc2);
     }
+    float a0, a1;
+    uf2(acc2, a0, a1);
+    acc = a0 + a1;
+  }
+  if (kStageEarly) pdl_wait();  // the previous main kernel is done with the image buffer
+  *(uint4*)(img + (ch >> 3) * 2048 + kmajor_off(row, (ch & 7) * 8, 8, 1024, 0)) = v;
+  if (def) {
+    *(uint4*)(img + 4096 + mnmajor_off(n8, jj, 4, 1024, 512)) = bv;  // packed B_k image (RoPE partner order)
+  } else {
+    const int orow = tid >> 4, oj = tid & 15;
+    *(__nv_bfloat16*)(img + 4096 + kmajor_off(orow, oj, 2, 256, 0)) = __float2bfloat16_rn(orow < n_rows ? acc : 0.f);
   }
 }
 
