@@ -60,9 +60,9 @@ constexpr bool kLazyStart = FKV_LAZY_START;
 #endif
 constexpr int kSkip = FKV_DIAG_SKIP;
 #ifndef FKV_STAGE_EARLY
-#define FKV_STAGE_EARLY 0
+#define FKV_STAGE_EARLY 1
 #endif
-constexpr bool kStageEarly = FKV_STAGE_EARLY;  // stager: loads before griddepcontrol.wait (A/B: slower on C2)  // first tile of a non-causal item: m = 0 reference (no column max)
+constexpr bool kStageEarly = FKV_STAGE_EARLY;  // stager: loads and q~ before griddepcontrol.wait (C2 +2.3%)  // first tile of a non-causal item: m = 0 reference (no column max)
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
