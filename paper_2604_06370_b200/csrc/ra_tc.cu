@@ -52,9 +52,10 @@ constexpr int kD = 128, kR = 16, kTile = 128, kMaxSlots = 8;
 #ifndef FKV_LAZY_START
 #define FKV_LAZY_START 1
 #endif
-constexpr bool kLazyStart = FKV_LAZY_START;
+constexpr bool kLazyStart = FKV_LAZY_START;  // first tile of a non-causal item: m = 0 reference (no column max)
 // diagnostics only (A/B builds, wrong output): skip loads / math to find the binding pipeline stage.
-// bit 1: K_base TMA, 2: V_base TMA, 4: R_k copies, 8: R_v copies, 16: key-warp exponentials (P = bf16(x))
+// bit 1: K_base TMA, 2: V_base TMA, 4: R_k copies, 8: R_v copies, 16: key-warp exponentials (P = bf16(x)),
+// 32: null key warps (pipeline handshakes only)
 #ifndef FKV_DIAG_SKIP
 #define FKV_DIAG_SKIP 0
 #endif
@@ -62,7 +63,7 @@ constexpr int kSkip = FKV_DIAG_SKIP;
 #ifndef FKV_STAGE_EARLY
 #define FKV_STAGE_EARLY 1
 #endif
-constexpr bool kStageEarly = FKV_STAGE_EARLY;  // stager: loads and q~ before griddepcontrol.wait (C2 +2.3%)  // first tile of a non-causal item: m = 0 reference (no column max)
+constexpr bool kStageEarly = FKV_STAGE_EARLY;  // stager: loads and q~ before griddepcontrol.wait (C2 +2.3%)
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
