@@ -64,6 +64,13 @@ constexpr int kSkip = FKV_DIAG_SKIP;
 #define FKV_STAGE_EARLY 1
 #endif
 constexpr bool kStageEarly = FKV_STAGE_EARLY;  // stager: loads and q~ before griddepcontrol.wait (C2 +2.3%)
+// lazy-rescale headroom (log2 units): p = 2^(x - m) may reach 2^kLazyHi before the running max moves. fp32
+// accumulators and bf16 P hold 2^16 x 32K keys easily; a larger headroom makes the first-tile slow path (m = 0
+// reference, ~8 K cycles cold) and later rescales rarer
+#ifndef FKV_LAZY_HI
+#define FKV_LAZY_HI 16
+#endif
+constexpr float kLazyHi = FKV_LAZY_HI;
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
@@ -1371,7 +1378,8 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           float mx = -INFINITY;
           // lazy start (NONE, 64 rows, items whose every query column sees every key): the first tile takes the
           // running max m = 0 as its reference instead of computing the column maxima; the slow path below still
-          // runs when a score leaves [-64, 8] of it (p then stays within [2^-64, 2^8]: no bf16 / fp32 underflow)
+          // runs when a score leaves [-64, kLazyHi] of it (p then stays within [2^-64, 2^kLazyHi]: no bf16 / fp32
+          // underflow or overflow)
           const bool lazy0 = C::PVROW && kLazyStart && j == 0 && causal_mask == 0;
           const bool lref = (lrefm >> ch) & 1u;
           {
@@ -1401,10 +1409,10 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               mx = max3(mx, a, b2);
             }
           }
-          // lazy rescaling: only when some score exceeds the running max by > 2^8
+          // lazy rescaling: only when some score exceeds the running max by > 2^kLazyHi
           float alpha_l = 1.f;  // this lane's column (cb + lane) rescale factor (row-sum partials)
           if (tid == 0) EV(20, T);
-          bool out = mx > 8.0f;
+          bool out = mx > kLazyHi;
           if (lazy0) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
