@@ -1172,10 +1172,12 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         float* ent = p.ws + (int64_t)(Re.entry_off[o < ns ? o : 0] + r) * p.entry_stride + kEntAcc;
         const uint32_t base = tm + C::tOX(ab) + 48 * q + lb;
         uint32_t x[48];
+        if (tid == 0) EV(14, ie);
         FKV_TMEM_LD16(base, x);
         FKV_TMEM_LD16(base + 16, (x + 16));
         FKV_TMEM_LD16(base + 32, (x + 32));
         tmem_ld_wait();
+        if (tid == 0) EV(15, ie);
         tc_fence_before();
         mbar_arrive(smem_u32(&ms.accfree[ab]));
         if (valid) {
@@ -1616,6 +1618,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
           lwb[wq * kRows + CPW * w + 32 * ch + lane] = v[0];
         }
+        if (tid == 0) EV(13, ii);
         named_bar_sync(bar_id, 128);
         if (kl < CPW) {
           const int c = CPW * w + kl, o = c >> 4, r = c & 15;

@@ -69,6 +69,10 @@ def main():
         row2 = [d[e, j] - t0 if d[e, j] else -1 for e in (0, 1, 7, 6)]
         print(f"{j:4d} " + " ".join(f"{x:9d}" for x in row) + f" | {j:3d} " + " ".join(f"{x:9d}" for x in row2))
     print("items: P:Qitem / S:Qfull", [(int(d[9, i] - t0), int(d[10, i] - t0)) for i in range(64) if d[9, i]])
+    print("items (NONE): key-warp start, end, reduced, | epilogue: start, TMEM loaded, done",
+          [(int(d[25, i] - t0), int(d[26, i] - t0), int(d[13, i] - t0) if d[13, i] else -1,
+            int(d[14, i] - t0) if d[14, i] else -1, int(d[15, i] - t0) if d[15, i] else -1,
+            int(d[27, i] - t0) if d[27, i] else -1) for i in range(64) if d[25, i]])
     print("key warps per item: start / end / epilogue done", [(int(d[25, i] - t0), int(d[26, i] - t0), int(d[27, i] - t0) if d[27, i] else -1) for i in range(64) if d[25, i]])
     if a.detail >= 0:
         print("key-warp phases per tile (cycles from W:sfull): S loaded, pre-bar_or, post-bar_or, pfree wait/ok, P stored, "
