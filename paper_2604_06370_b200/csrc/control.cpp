@@ -450,6 +450,8 @@ void write_kv(Ctx& c, int32_t layer, int32_t n, const int64_t* agents, const int
     const auto pv = pool_view(c);
     for (size_t o = 0; o < runs.size(); o += k::kMaxRuns) {
       const int32_t m = (int32_t)std::min<size_t>(k::kMaxRuns, runs.size() - o);
+      const bool no_write = getenv("FKV_DIAG_NOKVWRITE") != nullptr;  // diagnostics: timing only (read per call)
+      if (!no_write)
       check_cuda(k::launch_kv_write(pv, layer, runs.data() + o, m, kb, vb, rk, rv, mask, (cudaStream_t)stream),
                  "kv_write");
     }

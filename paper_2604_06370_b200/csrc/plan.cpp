@@ -722,7 +722,8 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
     e = p.kernel == 2   ? k::launch_attention_tc(a, c.tc_maps.data(), (cudaStream_t)stream)
         : p.kernel == 0 ? k::launch_attention_mma(a, (cudaStream_t)stream)
                         : k::launch_attention_simt(a, (cudaStream_t)stream);
-  if (e == cudaSuccess && (phases & FKV_PHASE_COMBINE)) e = k::launch_combine(a, (cudaStream_t)stream);
+  const bool no_combine = getenv("FKV_DIAG_NOCOMBINE") != nullptr;  // diagnostics: timing only (read per call)
+  if (e == cudaSuccess && (phases & FKV_PHASE_COMBINE) && !no_combine) e = k::launch_combine(a, (cudaStream_t)stream);
   if (e != cudaSuccess) throw Error(FKV_E_CUDA, std::string("attention: ") + cudaGetErrorString(e));
 }
 

@@ -71,6 +71,9 @@ constexpr bool kStageEarly = FKV_STAGE_EARLY;  // stager: loads and q~ before gr
 #define FKV_LAZY_HI 16
 #endif
 constexpr float kLazyHi = FKV_LAZY_HI;
+#ifndef FKV_MAX_TREE
+#define FKV_MAX_TREE 0
+#endif
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
@@ -1404,12 +1407,24 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
                 x2[q] = f2(a, b2);
               }
             }
+#if FKV_MAX_TREE
+            // four independent max3 chains, then a 4-way combine (the serial chain was 16 dependent max3)
+            float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              float a, b2;
+              uf2(x2[q], a, b2);
+              mq[q & 3] = max3(mq[q & 3], a, b2);
+            }
+            mx = max3(mq[0], mq[1], fmaxf(mq[2], mq[3]));
+#else
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
               float a, b2;
               uf2(x2[q], a, b2);
               mx = max3(mx, a, b2);
             }
+#endif
           }
           // lazy rescaling: only when some score exceeds the running max by > 2^kLazyHi
           float alpha_l = 1.f;  // this lane's column (cb + lane) rescale factor (row-sum partials)
