@@ -293,7 +293,12 @@ fkv_status fkv_plan_upload(fkv_ctx* ctx, fkv_plan* plan, void* dev, size_t bytes
  *   Q [n_rows_q][Hq_local][d], O same (rows = seqs in plan order, each its
  *   q_len rows), workspace >= info.workspace_bytes (fp32 partials),
  *   256-byte aligned (E_INVALID otherwise); O 16-byte aligned.
- * sm_scale <= 0 selects 1/sqrt(d) (C-4). Enqueued on `stream`. */
+ * sm_scale <= 0 selects 1/sqrt(d) (C-4). Enqueued on `stream`. The kernels
+ * use programmatic dependent launch: the first one may start, and read Q,
+ * the adapters and the uploaded plan, while the preceding kernel on `stream`
+ * finishes, so that kernel must not trigger its dependents
+ * (griddepcontrol.launch_dependents) before its writes to Q are done (plain
+ * launches, memcpys and this library's own kernels satisfy this). */
 fkv_status fkv_residual_attention(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
                                   float sm_scale, void* workspace, size_t ws_bytes, void* stream);
 /* The two kernels of fkv_residual_attention separately (for per-kernel
