@@ -301,12 +301,18 @@ fkv_status fkv_plan_upload(fkv_ctx* ctx, fkv_plan* plan, void* dev, size_t bytes
  * launches, memcpys and this library's own kernels satisfy this). */
 fkv_status fkv_residual_attention(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
                                   float sm_scale, void* workspace, size_t ws_bytes, void* stream);
-/* The two kernels of fkv_residual_attention separately (for per-kernel
- * timing): phases = FKV_PHASE_MAIN (split partials, Stages 1-2) and/or
- * FKV_PHASE_COMBINE (merge + late V fusion, Stage 3). MAIN must precede
- * COMBINE on the same stream with the same workspace. */
+/* The kernels of fkv_residual_attention separately (for per-kernel timing):
+ * phases = FKV_PHASE_MAIN (split partials, Stages 1-2: the tcgen05 kernel's
+ * operand stager + the main kernel) and/or FKV_PHASE_COMBINE (merge + late V
+ * fusion, Stage 3). FKV_PHASE_STAGE alone launches only the stager and
+ * FKV_PHASE_NOSTAGE | FKV_PHASE_MAIN only the main kernel, so the main kernel
+ * can be timed by itself; STAGE must then precede it (kernel 2; other kernels
+ * have no stager and ignore both bits). MAIN must precede COMBINE on the same
+ * stream with the same workspace. */
 #define FKV_PHASE_MAIN 1u
 #define FKV_PHASE_COMBINE 2u
+#define FKV_PHASE_STAGE 4u
+#define FKV_PHASE_NOSTAGE 8u
 fkv_status fkv_residual_attention_phases(fkv_ctx* ctx, const fkv_plan* plan, int32_t layer, const void* Q, void* O,
                                          float sm_scale, void* workspace, size_t ws_bytes, void* stream,
                                          uint32_t phases);

@@ -616,7 +616,9 @@ void upload_plan(Ctx& c, Plan& p, void* dev, size_t bytes, void* stream) {
 
 void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O, float scale, void* ws,
                    size_t ws_bytes, void* stream, uint32_t phases, float* lse) {
-  if (phases == 0 || (phases & ~3u)) throw Error(FKV_E_INVALID, "attention: bad phases");
+  if (phases == 0 || (phases & ~15u) || ((phases & FKV_PHASE_STAGE) && (phases & (FKV_PHASE_NOSTAGE | FKV_PHASE_MAIN))) ||
+      ((phases & FKV_PHASE_NOSTAGE) && !(phases & FKV_PHASE_MAIN)))
+    throw Error(FKV_E_INVALID, "attention: bad phases");
   if (!c.device) throw Error(FKV_E_INVALID, "attention: host-only ctx");
   if (p.generation != c.generation) throw Error(FKV_E_STALE, "attention: plan is stale");
   if (!p.dev) throw Error(FKV_E_INVALID, "attention: plan not uploaded");
@@ -716,7 +718,8 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   // stager's share of the step
   static const bool no_stage = getenv("FKV_DIAG_NOSTAGE") != nullptr;
   static int stage_calls = 0;  // the first calls stage real images (finite scores in the skipped ones)
-  if ((phases & FKV_PHASE_MAIN) && p.kernel == 2 && !(no_stage && ++stage_calls > 64))
+  if (((phases & FKV_PHASE_MAIN) && !(phases & FKV_PHASE_NOSTAGE) || (phases & FKV_PHASE_STAGE)) && p.kernel == 2 &&
+      !(no_stage && ++stage_calls > 64))
     e = k::launch_stage(a, (int32_t)p.stage_src.size(), (cudaStream_t)stream);
   if (e == cudaSuccess && (phases & FKV_PHASE_MAIN))
     e = p.kernel == 2   ? k::launch_attention_tc(a, c.tc_maps.data(), (cudaStream_t)stream)

@@ -177,6 +177,30 @@ def test_host_entry_point(mode):
     assert err <= TOL, err
 
 
+@pytest.mark.parametrize("mode", ["none", "deferred"])
+def test_split_phases_stage_then_main(mode):
+    """FKV_PHASE_STAGE then FKV_PHASE_MAIN | FKV_PHASE_NOSTAGE then FKV_PHASE_COMBINE (the bench's per-kernel
+    timing path) gives the oracle's result, bit-identical to the one-call path; bad phase masks are refused."""
+    scen = recipes.c1(prefix=900, private=50)
+    fkv = _ctx(scen, 32, 8, 128, mode)
+    driver.build(fkv, scen, seed=6)
+    batch = scen.batch()
+    pl = fkv.plan([(a, 1) for a in batch], flags=L.PLAN_CHECK_WRITTEN)
+    Q = driver.make_queries(fkv, scen, 6, 0)
+    O1 = fkv.residual_attention(pl, 0, Q)
+    O2 = torch.empty_like(Q)
+    fkv.residual_attention_phases(pl, 0, Q, O2, 4)
+    fkv.residual_attention_phases(pl, 0, Q, O2, 1 | 8)
+    fkv.residual_attention_phases(pl, 0, Q, O2, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(O1, O2)
+    err = _check(fkv, scen, 6, 0, mode, seqs=range(len(batch)), O=O2)
+    assert err <= TOL, err
+    for bad in (8, 4 | 1, 4 | 8, 16):
+        with pytest.raises(Exception):
+            fkv.residual_attention_phases(pl, 0, Q, O2, bad)
+
+
 # ---- (e) a multi-step decode loop -----------------------------------------------------------------------------
 
 @pytest.mark.parametrize("mode", ["none", "deferred"])
