@@ -472,6 +472,8 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
   };
   if (sbase & 1023) __trap();
   const long long t_start = clock64();
+  uint64_t g_start = 0;
+  if (p.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
   const int cta = blockIdx.x;
   const bool dbg_on = p.dbg != nullptr && cta == p.dbg_block;
   pdl_trigger();  // the combine kernel may be scheduled as CTAs drain (it waits for this grid's completion)
@@ -1666,6 +1668,10 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
   if (wid == 11) tmem_dealloc(tm, 512);
   if (tid == 0 && p.dbg && cta < 256) {  // diagnostics: per-CTA duration (cycles) and tile count
     p.dbg[30 * 256 + cta] = clock64() - t_start;
+    uint64_t g_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+    p.dbg[32 * 256 + cta] = (long long)g_start;  // diagnostics buffer of 34 x 256 (tools/timeline.py)
+    p.dbg[33 * 256 + cta] = (long long)g_end;
     p.dbg[31 * 256 + cta] = p.tile_ptr[cta + 1] - p.tile_ptr[cta];
   }
 }

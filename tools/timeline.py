@@ -51,15 +51,28 @@ def main():
         fkv.residual_attention_phases(pl, 0, Q, O, 1)
     e1.record()
     torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fkv.residual_attention_phases(pl, 0, Q, O, 4)
+    e2.record()
+    for _ in range(10):
+        fkv.residual_attention_phases(pl, 0, Q, O, 9)
+    e3.record()
+    torch.cuda.synchronize()
+    print(f"main kernel alone (10 back to back): {e2.elapsed_time(e3) / 10 * 1e3:.1f} us")
     print(f"items={pl.info.n_items} main kernel avg {e0.elapsed_time(e1) / 10 * 1e3:.1f} us; "
           f"alg bytes/layer {pl.info.alg_bytes / 1e6:.1f} MB")
-    dbg = torch.zeros(32 * 256, dtype=torch.int64, device="cuda")
+    dbg = torch.zeros(34 * 256, dtype=torch.int64, device="cuda")
     lib = L.load()
     lib.fkv_debug_timeline(fkv.ctx, ctypes.c_void_p(dbg.data_ptr()), a.block)
     fkv.residual_attention_phases(pl, 0, Q, O, 1)
     torch.cuda.synchronize()
     lib.fkv_debug_timeline(fkv.ctx, None, 0)
-    d = dbg.view(32, 256).cpu().numpy()
+    d = dbg.view(34, 256).cpu().numpy()
+    gs, ge = d[32, :148], d[33, :148]
+    if gs.any():
+        gs, ge = gs[gs > 0], ge[ge > 0]
+        print(f"CTA globaltimer: start spread {(gs.max() - gs.min()) / 1e3:.1f} us, first start -> last end "
+              f"{(ge.max() - gs.min()) / 1e3:.1f} us, first end {(ge.min() - gs.min()) / 1e3:.1f} us")
     t0 = d[:30][d[:30] > 0].min()
     print("per tile T (S/W/PV events) and per ring entry (K slab 3/tile, V entry 2/tile), cycles from first event")
     cols = [8, 2, 3, 4, 5]
