@@ -184,6 +184,7 @@ struct Plan {
   int64_t n_rows_q = 0;  // total query rows (sum q_len)
   int32_t kernel = 0;    // 0 mma grouped, 1 simt, 2 tcgen05 (keys on lanes, round 1), 3 tcgen05 rows on lanes
   int32_t tc_rows = 64;  // tcgen05: query rows per CTA
+  int32_t tc_pp = 0;     // tcgen05 NONE 64-row: ping-pong key warpgroups (entries per slot doubled)
   std::vector<DevSeq> seqs;
   std::vector<int32_t> base_pages, res_pages;
   std::vector<DevItem> items;

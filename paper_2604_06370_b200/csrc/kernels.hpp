@@ -95,6 +95,7 @@ struct AttnParams {
   const int4* tile_recs;
   const void* item_recs;  // per plan item: ItemRecT<tc_rows / 16>
   int32_t tc_rows;        // query rows per CTA of the tcgen05 kernel (64 | 128)
+  int32_t tc_pp;          // kernel 2, NONE, 64 rows: ping-pong key warpgroups (two partial entries per row and item)
   int32_t l2_evict_first; // base K / V tiles read by few row blocks: stream them through L2 evict-first
   const int32_t* stage_src;  // staged image i is built from warp slot stage_src[i]; DevItem::pad_[0] = first image
   const int4* stage_desc;    // per image, 5 x int4: {B_k^h address (layer 0) lo, hi, n_rows, kv head}, Q rows [16]

@@ -92,6 +92,8 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
     pl.tc_rows = renv ? atoi(renv) : 64;
     if (pl.tc_rows != 64 && pl.tc_rows != 128) pl.tc_rows = 64;
     if (c.cfg.rope_mode != FKV_ROPE_NONE) pl.tc_rows = 64;
+    const char* penv = getenv("FKV_TC_PINGPONG");
+    pl.tc_pp = (penv ? atoi(penv) : 0) != 0 && pl.tc_rows == 64 && c.cfg.rope_mode == FKV_ROPE_NONE;
   }
   const int kWarpsPerCta = pl.kernel == 2 ? pl.tc_rows / kRowsPerWarp : 8;
   const int kTileKeys = pl.kernel == 2 ? 128 : 64;
@@ -332,7 +334,8 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
         if (nr == 0) continue;
         w.n_rows = nr;
         w.entry_off = (int32_t)entries;
-        entries += kRowsPerWarp;  // entries are per warp slot (padded) for simple indexing
+        // entries are per warp slot (padded) for simple indexing; ping-pong: one block of 16 per key warpgroup
+        entries += (pl.tc_pp ? 2 : 1) * kRowsPerWarp;
         for (int j = 0; j < kRowsPerWarp; ++j) pl.rows.push_back(j < nr ? keep[j] : DevRow{-1, 0, 0, -1});
         pl.warps.push_back(w);
       }
@@ -483,10 +486,11 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
   // CSR: output row -> entries
   const int64_t n_out = pl.n_rows_q * c.hq_local;
   std::vector<int32_t> cnt(n_out + 1, 0);
+  const int n_halves = pl.tc_pp ? 2 : 1;  // ping-pong: each row has one partial entry per key warpgroup and item
   for (const DevWarp& w : pl.warps)
     for (int j = 0; j < w.n_rows; ++j) {
       const DevRow& rw = pl.rows[w.row_off + j];
-      cnt[(int64_t)(pl.seqs[rw.seq].q_row0 + rw.qi) * c.hq_local + rw.qh + 1]++;
+      cnt[(int64_t)(pl.seqs[rw.seq].q_row0 + rw.qi) * c.hq_local + rw.qh + 1] += n_halves;
     }
   for (int64_t i = 0; i < n_out; ++i) cnt[i + 1] += cnt[i];
   pl.out_ptr = cnt;
@@ -496,7 +500,7 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
     for (int j = 0; j < w.n_rows; ++j) {
       const DevRow& rw = pl.rows[w.row_off + j];
       const int64_t o = (int64_t)(pl.seqs[rw.seq].q_row0 + rw.qi) * c.hq_local + rw.qh;
-      pl.out_entries[fill[o]++] = w.entry_off + j;
+      for (int hv = 0; hv < n_halves; ++hv) pl.out_entries[fill[o]++] = w.entry_off + kRowsPerWarp * hv + j;
     }
   for (int64_t o = 0; o < n_out; ++o)
     if (!pl.key_range && pl.out_ptr[o + 1] == pl.out_ptr[o]) throw Error(FKV_E_NO_KEYS, "plan: an output row has no keys");
@@ -671,6 +675,7 @@ void run_attention(Ctx& c, const Plan& p, int32_t layer, const void* Q, void* O,
   a.tile_recs = (const int4*)(base + p.off_trecs);
   a.item_recs = base + p.off_irecs;
   a.tc_rows = p.tc_rows;
+  a.tc_pp = p.tc_pp;
   a.l2_evict_first = p.l2_evict_first ? 1 : 0;
   a.stage_src = (const int32_t*)(base + p.off_ssrc);
   a.stage_desc = (const int4*)(base + p.off_sdesc);

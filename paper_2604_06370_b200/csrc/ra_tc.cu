@@ -134,7 +134,8 @@ struct Cfg {
   static constexpr uint32_t OFF_P = OFF_Q + NQ * QB;
   static constexpr uint32_t OFF_X = OFF_P + NPH * PHB;  // [NQ][SLOTS][XB]
   static constexpr uint32_t OFF_MISC = OFF_X + NQ * SLOTS * XB;
-  static constexpr uint32_t MISCB = kRowsT == 128 ? 7168 : (PVROW ? 4096 : 2048);
+  // 64-row NONE: room for the ping-pong variant's per-warpgroup m_run / row-sum buffers (SMEM = 227 KB exactly)
+  static constexpr uint32_t MISCB = kRowsT == 128 ? 7168 : (PVROW ? 7168 : 2048);
   static constexpr uint32_t SMEM = OFF_MISC + MISCB;
   static_assert(SMEM <= 232448, "shared memory");
   static_assert(!(kDef && kRowsT != 64), "DEFERRED runs 64-row CTAs");
@@ -146,13 +147,14 @@ template <bool D, int R>
 struct kDefOf<Cfg<D, R>> {
   static constexpr bool value = D;
 };
-template <class C>
+template <class C, bool PP = false>
 struct MiscT {
   uint64_t kfull[C::KU], kempty[C::KU], rfull[1], rempty[1], vfull[C::VS], vempty[C::VS], rvfull[C::VS], qfull[2],
       qempty[2], sfull[2], sfree[2], pfull[C::NPH], pfree[C::NPH], accfree[2], recfull[C::NRC], recempty[C::NRC], kl[kDefOf<C>::value ? 4 * kKlBufs : 1];  // kl: DEFERRED klfull | klready
   // running column max (PVROW: two buffers by item parity, reset by the item's end, so items start barrier-free)
-  alignas(16) float m_run[(C::PVROW ? 2 : 1) * C::ROWS];
-  alignas(16) float lw[C::ONES ? 4 : (C::PVROW ? 2 : 1) * 4 * C::ROWS];  // row-sum partials per key warp [4][ROWS]
+  // (PP: [warpgroup][item parity])
+  alignas(16) float m_run[(PP ? 4 : C::PVROW ? 2 : 1) * C::ROWS];
+  alignas(16) float lw[C::ONES ? 4 : (PP ? 4 : C::PVROW ? 2 : 1) * 4 * C::ROWS];  // row-sum partials per key warp [4][ROWS]
   alignas(16) ItemRecT<C::SLOTS> rec[C::NRC];        // per-item header ring
   uint32_t tmem_base;
 };
@@ -446,12 +448,17 @@ __global__ void __launch_bounds__(256) ra_stage_kernel(AttnParams p, int n_image
 }
 
 // ---------------------------------------------------------------------------
-template <bool kDef, int kRowsT>
+template <bool kDef, int kRowsT, bool kPP>
 __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ TcMaps maps, AttnParams p) {
   using C = Cfg<kDef, kRowsT>;
+  // kPP (NONE, 64 rows): ping-pong key warpgroups. Warpgroup w takes the tiles T with T & 1 == w, all 64 query
+  // columns, its own running max, row sums, O_ext accumulator (TMEM set w) and partial entries (entry + 16 w), so
+  // the two softmax chains run on different tiles and overlap
+  static_assert(!kPP || (!kDef && kRowsT == 64), "ping-pong: NONE, 64 rows");
+  constexpr bool PP = kPP;
   constexpr int kRows = C::ROWS, kSlots = C::SLOTS;
   using ItemRec = ItemRecT<kSlots>;
-  using Misc = MiscT<C>;
+  using Misc = MiscT<C, kPP>;
   static_assert(sizeof(Misc) <= C::MISCB, "misc");
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -495,18 +502,18 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       mbar_init(smem_u32(&ms.qfull[i]), p.P == kTile ? 32 : 1);  // fast path: one cp.async arrive per lane
       mbar_init(smem_u32(&ms.qempty[i]), 1);  // S-side commit (the last MMA reading Q / X)
       mbar_init(smem_u32(&ms.sfull[i]), 1);
-      mbar_init(smem_u32(&ms.sfree[i]), 256);
+      mbar_init(smem_u32(&ms.sfree[i]), PP ? 128 : 256);
     }
     for (int i = 0; i < C::NPH; ++i) {
-      mbar_init(smem_u32(&ms.pfull[i]), 128);  // the key threads of one 64-key half (both warpgroups)
+      mbar_init(smem_u32(&ms.pfull[i]), PP ? 64 : 128);  // the key threads of one 64-key half (both warpgroups)
       mbar_init(smem_u32(&ms.pfree[i]), 1);
     }
     for (int i = 0; i < C::NRC; ++i) {
       mbar_init(smem_u32(&ms.recfull[i]), p.P == kTile ? 32 : 1);
       mbar_init(smem_u32(&ms.recempty[i]), 2);  // one arrive per key warpgroup after the item's epilogue
     }
-    mbar_init(smem_u32(&ms.accfree[0]), 256);
-    mbar_init(smem_u32(&ms.accfree[1]), 256);
+    mbar_init(smem_u32(&ms.accfree[0]), PP ? 128 : 256);
+    mbar_init(smem_u32(&ms.accfree[1]), PP ? 128 : 256);
     for (int w = 0; w < 2; ++w)
       for (int b = 0; b < kKlBufs; ++b) {
         if (kDef) {
@@ -519,7 +526,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
   if (wid == 11) tmem_alloc(smem_u32(&ms.tmem_base), 512);
   if (kSkip)  // diagnostics: skipped copies leave zeros (finite scores), not stale bytes
     for (uint32_t c = tid; c < C::OFF_MISC / 16; c += 384) *(uint4*)(smem + 16 * c) = make_uint4(0, 0, 0, 0);
-  for (int c = tid; c < (C::PVROW ? 2 : 1) * C::ROWS; c += 384) ms.m_run[c] = -INFINITY;
+  for (int c = tid; c < (PP ? 4 : C::PVROW ? 2 : 1) * C::ROWS; c += 384) ms.m_run[c] = -INFINITY;
   // the all-ones R_v slot (index 4) of every V-side entry: A^T lanes 64..79 accumulate the row sums l
   if (C::ONES)
     for (int c = tid; c < C::VS * 128; c += 384)
@@ -914,13 +921,21 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       const uint32_t id_pv = idesc_bf16(128, kRows, true, true);
       const uint32_t id_px = idesc_bf16(128, C::OXW, true, true);
       uint32_t nv = 0, T = 0;
+      uint32_t uses[2] = {0, 0};  // PP: items so far whose tiles used accumulator set w
       for (int ii = 0; ii < n_my; ++ii) {
         const int qb = ii % C::NQ;
         mbar_wait(smem_u32(&ms.recfull[ii % C::NRC]), (ii / C::NRC) & 1);
         const int n_tiles = ms.rec[ii % C::NRC].n_tiles & 0xffff;
         for (int j = 0; j < n_tiles; ++j, ++T) {
-          const int ab = ii % C::AB;
-          if (j == 0 && ii >= C::AB) mbar_wait(smem_u32(&ms.accfree[ab]), ((ii / C::AB) - 1) & 1);
+          const int ab = PP ? (int)(T & 1) : ii % C::AB;
+          if constexpr (PP) {
+            if (j < 2) {  // the warpgroup's first tile of the item: its previous item's epilogue freed the set
+              if (uses[ab] > 0) mbar_wait(smem_u32(&ms.accfree[ab]), (uses[ab] - 1) & 1);
+              ++uses[ab];
+            }
+          } else {
+            if (j == 0 && ii >= C::AB) mbar_wait(smem_u32(&ms.accfree[ab]), ((ii / C::AB) - 1) & 1);
+          }
           for (int kh = 0; kh < 2; ++kh, ++nv) {
             // P^T half kh of tile T = ring entry nv (the V-side entries run in the same order)
             const int ps = nv % C::NPH;
@@ -940,7 +955,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 #pragma unroll
               for (int s = 0; s < 4; ++s)
                 mma_ss_e(tm + C::tOX(ab), pa + (uint64_t)((s * 2048) >> 4), dv + (uint64_t)((s * 2048) >> 4), id_px,
-                         (j > 0 || kh > 0 || s > 0));
+                         (j >= (PP ? 2 : 1) || kh > 0 || s > 0));
               mma_commit_e(smem_u32(&ms.vempty[nv % C::VS]));
               mma_commit_e(smem_u32(&ms.pfree[ps]));
               continue;
@@ -1097,12 +1112,13 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
     // ================= key warps =================
     // thread = key of the tile = TMEM lane; key warpgroup w owns query columns [CPW w, CPW (w + 1)), processed in
     // chunks of 32 (one TMEM load of S^T each); DEFERRED (64-row CTAs): also the d-half w of the K_lora rotation
-    constexpr int CPW = kRows / 2, NCH = CPW / 32;
+    constexpr int CPW = PP ? kRows : kRows / 2, NCH = CPW / 32;
     const int w = wid >> 2;                         // key warpgroup 0/1
     const int kl = tid - 128 * w;                   // key within the tile == TMEM lane
     const int wq = wid & 3;                         // warp within the warpgroup (TMEM lane quarter)
     const uint32_t lb = (uint32_t)(32 * wq) << 16;
     const uint32_t bar_id = 1 + w;                  // named barrier of this warpgroup
+    const int WOFF = PP ? 0 : CPW * w;              // first query column of this warpgroup
     const uint64_t sc2 = f2(p.scale_log2, p.scale_log2);
     const float scl = p.scale_log2;
     uint32_t T = 0, U = 0;
@@ -1124,7 +1140,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
     // of its last tile Tl completed; then the accumulators and the header are free
     auto epilogue = [&](int ie, uint32_t Tl, int qbe) {
       const ItemRec& Re = ms.rec[qbe];
-      const int ab = ie % C::AB, ns = Re.meta & 15;
+      const int ab = PP ? w : ie % C::AB, ns = Re.meta & 15;
       for (uint32_t np = 2 * Tl; np < 2 * Tl + 2; ++np) mbar_wait(smem_u32(&ms.pfree[np % C::NPH]), (np / C::NPH) & 1);
       tc_fence_after();
       if constexpr (C::PVROW && kRows == 128) {
@@ -1172,29 +1188,36 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         // operand's second atom duplicates the rows); the lazy rescale keeps columns [0, 96) current in the first
         // copy and [96, 192) in the second, so all 8 key warps share the stores as: warp (w, wq) writes its rows'
         // columns [48 q, 48 q + 48), q = 2 (wq >> 1) + w: acc (16-byte stores) and the row owner's acc_r
-        const int c = 32 * (wq & 1) + lane, o = c >> 4, r = c & 15, q = 2 * (wq >> 1) + w;
+        // PP: one warpgroup holds the set, each of its warps writes 96 columns in two 48-column passes
+        const int c = 32 * (wq & 1) + lane, o = c >> 4, r = c & 15;
         const bool valid = o < ns && r < Re.n_rows[o];
-        float* ent = p.ws + (int64_t)(Re.entry_off[o < ns ? o : 0] + r) * p.entry_stride + kEntAcc;
-        const uint32_t base = tm + C::tOX(ab) + 48 * q + lb;
-        uint32_t x[48];
-        if (tid == 0) EV(14, ie);
-        FKV_TMEM_LD16(base, x);
-        FKV_TMEM_LD16(base + 16, (x + 16));
-        FKV_TMEM_LD16(base + 32, (x + 32));
-        tmem_ld_wait();
-        if (tid == 0) EV(15, ie);
-        tc_fence_before();
-        mbar_arrive(smem_u32(&ms.accfree[ab]));
-        if (valid) {
+        float* ent = p.ws + (int64_t)(Re.entry_off[o < ns ? o : 0] + r + (PP ? 16 * w : 0)) * p.entry_stride + kEntAcc;
+#pragma unroll 1
+        for (int pass = 0; pass < (PP ? 2 : 1); ++pass) {
+          const int q = 2 * (wq >> 1) + (PP ? pass : w);
+          const uint32_t base = tm + C::tOX(ab) + 48 * q + lb;
+          uint32_t x[48];
+          if (tid == 0) EV(14, ie);
+          FKV_TMEM_LD16(base, x);
+          FKV_TMEM_LD16(base + 16, (x + 16));
+          FKV_TMEM_LD16(base + 32, (x + 32));
+          tmem_ld_wait();
+          if (tid == 0) EV(15, ie);
+          if (pass == (PP ? 1 : 0)) {
+            tc_fence_before();
+            mbar_arrive(smem_u32(&ms.accfree[ab]));
+          }
+          if (valid) {
 #pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const int col = 48 * q + 16 * k;  // warp-uniform
-            if (col < kD) {
-              st_global_v8(ent + col, x + 16 * k);
-              st_global_v8(ent + col + 8, x + 16 * k + 8);
-            } else if ((col - kD) / 16 == o) {
-              st_global_v8(ent + kD, x + 16 * k);
-              st_global_v8(ent + kD + 8, x + 16 * k + 8);
+            for (int k = 0; k < 3; ++k) {
+              const int col = 48 * q + 16 * k;  // warp-uniform
+              if (col < kD) {
+                st_global_v8(ent + col, x + 16 * k);
+                st_global_v8(ent + col + 8, x + 16 * k + 8);
+              } else if ((col - kD) / 16 == o) {
+                st_global_v8(ent + kD, x + 16 * k);
+                st_global_v8(ent + kD + 8, x + 16 * k + 8);
+              }
             }
           }
         }
@@ -1205,7 +1228,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       }
 #pragma unroll 1
       for (int ch = 0; ch < NCH; ++ch) {
-        const int cb = CPW * w + 32 * ch;
+        const int cb = WOFF + 32 * ch;
         uint32_t o_[32], a_[32];
         FKV_TMEM_LD32(tm + C::tO(ab, 0) + cb + lb, o_);
         FKV_TMEM_LD32(tm + C::tA(ab, 0) + cb + lb, a_);
@@ -1247,8 +1270,10 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       I.n_tiles = R.n_tiles & 0xffff;
       I.n_slots = R.meta & 15;
       I.n_groups = (R.meta >> 4) & 15;
-      float* const mrun = ms.m_run + (C::PVROW ? (ii & 1) * kRows : 0);
-      float* const lwb = ms.lw + (C::PVROW ? (ii & 1) * 4 * kRows : 0);
+      // PVROW: m_run / row-sum partials double-buffered by item parity (PP: one buffer per warpgroup)
+      const int mbuf = PP ? 2 * w + (ii & 1) : (ii & 1);
+      float* const mrun = ms.m_run + (C::PVROW ? mbuf * kRows : 0);
+      float* const lwb = ms.lw + (C::PVROW ? mbuf * 4 * kRows : 0);
       if constexpr (!C::PVROW) {
         // per-item column state of this warpgroup; the previous item's epilogue is done with m_run / lw
         named_bar_sync(bar_id, 128);
@@ -1272,17 +1297,23 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 #pragma unroll
         for (int q = 0; q < (C::PVROW ? 16 : 1); ++q) lsum2[ch][q] = 0;
       // bit ch: chunk ch has a query column that does not see every key of the item (planner, n_tiles >> 16)
-      const uint32_t causal_mask = ((uint32_t)R.n_tiles >> (16 + NCH * w)) & ((1u << NCH) - 1);
+      const uint32_t causal_mask = ((uint32_t)R.n_tiles >> (16 + (WOFF >> 5))) & ((1u << NCH) - 1);
       // used query columns of each chunk (slot o < n_slots, row < n_rows[o]); unused ones are masked like invisible
       uint32_t colmask[NCH];
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
-        const int o0 = (CPW * w + 32 * ch) >> 4;
+        const int o0 = (WOFF + 32 * ch) >> 4;
         const int n0 = o0 < I.n_slots ? R.n_rows[o0] : 0, n1 = o0 + 1 < I.n_slots ? R.n_rows[o0 + 1] : 0;
         colmask[ch] = (n0 >= 16 ? 0xffffu : (1u << n0) - 1) | ((n1 >= 16 ? 0xffffu : (1u << n1) - 1) << 16);
       }
       if (tid == 0) EV(25, ii);
+      int jw = -1;          // PP: this warpgroup's tiles of the item so far - 1
+      uint32_t Tmine = 0;   // PP: this warpgroup's last tile
       for (int j = 0; j < I.n_tiles; ++j, ++T) {
+        if (PP && (int)(T & 1) != w) continue;  // the other warpgroup's tile
+        ++jw;
+        Tmine = T;
+        const int jm = PP ? jw : j;  // index of this tile among the warpgroup's tiles of the item
         const int t0 = I.k0 + j * kTile;
         const int t = t0 + kl;
         const bool tvalid = t < I.k1;
@@ -1342,10 +1373,11 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         // this thread's P^T half (keys 0..63 | 64..127) = ring entry 2T + half
         const uint32_t np = 2 * T + (kl >> 6), ps = np % C::NPH;
         uint8_t* pbuf = smem + C::OFF_P + ps * C::PHB;
-#pragma unroll 1
+        // PP: both chunks unrolled (lsum2[ch] / colmask[ch] stay in registers)
+#pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
           // ---- online softmax over the chunk's 32 query columns (Alg1.339-341) ----
-          const int cb = CPW * w + 32 * ch;
+          const int cb = WOFF + 32 * ch;
           const uint16_t* P1 = R.pos1 + cb;  // key t visible iff t - k0 < P1[c]
           uint32_t vm = tvalid ? colmask[ch] : 0u;
           if (((causal_mask >> ch) & 1) && tvalid) {
@@ -1387,7 +1419,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           // running max m = 0 as its reference instead of computing the column maxima; the slow path below still
           // runs when a score leaves [-64, kLazyHi] of it (p then stays within [2^-64, 2^kLazyHi]: no bf16 / fp32
           // underflow or overflow)
-          const bool lazy0 = C::PVROW && kLazyStart && j == 0 && causal_mask == 0;
+          const bool lazy0 = C::PVROW && kLazyStart && jm == 0 && causal_mask == 0;
           const bool lref = (lrefm >> ch) & 1u;
           {
             const float4* mp = (const float4*)&mrun[cb];
@@ -1445,7 +1477,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           if (slow_) {
             if (tid == 0) EV(21, T);
             // first tile of the item: every column is fresh (m = -inf), nothing to read back or rescale
-            const bool first = j == 0;
+            const bool first = jm == 0;
             float mo[32];
             if (!first) {
               const float4* mp = (const float4*)&mrun[cb];
@@ -1504,18 +1536,19 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
                 for (int q = 0; q < 16; ++q) lsum2[ch][q] = mul2(lsum2[ch][q], f2(al[2 * q], al[2 * q + 1]));
               }
             }
-            if (resc && j > 0) {
+            if (resc && jm > 0) {
               // rescale the chunk's columns of O^T and A^T by alpha (all PV up to tile T-1 complete)
-              for (uint32_t q2 = 2 * (T - 1); q2 < 2 * T; ++q2)
+              // all PV into this accumulator set up to the warpgroup's previous tile (PP: T - 2) complete
+              for (uint32_t q2 = 2 * (T - (PP ? 2 : 1)); q2 < 2 * (T - (PP ? 1 : 0)); ++q2)
                 mbar_wait(smem_u32(&ms.pfree[q2 % C::NPH]), (q2 / C::NPH) & 1);
               tc_fence_after();
               if constexpr (C::PVROW) {
                 // rows on lanes, times alpha_l of this lane's row cb + lane. 64 rows: quarters w (columns [0, 96)) and
                 // w + 2 (the duplicate rows, columns [96, 192)); 128 rows: quarter 2 w + ch, all 256 columns
-                const bool mine = kRows == 64 ? (wq & 1) == w : wq == 2 * w + ch;
+                const bool mine = PP ? (wq & 1) == ch : kRows == 64 ? (wq & 1) == w : wq == 2 * w + ch;
                 if (mine) {
                   constexpr int NPART = kRows == 64 ? 3 : C::OXW / 32;
-                  const uint32_t base = tm + C::tOX(ii % C::AB) + (kRows == 64 ? 96 * (wq >> 1) : 0) + lb;
+                  const uint32_t base = tm + C::tOX(PP ? w : ii % C::AB) + (kRows == 64 ? 96 * (wq >> 1) : 0) + lb;
 #pragma unroll 1
                   for (int part = 0; part < NPART; ++part) {
                     uint32_t r[32];
@@ -1606,7 +1639,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
         if (!kDef && tid == 0) EV(12, T);
         mbar_arrive(smem_u32(&ms.pfull[ps]));
         if (tid == 0) EV(4, T);
-        if (C::AB > 1 && j == 0 && pend_ii >= 0) {
+        if (C::AB > 1 && jm == 0 && pend_ii >= 0) {
           epilogue(pend_ii, pend_Tl, pend_qb);
           pend_ii = -1;
         }
@@ -1633,14 +1666,15 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
               v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
             }
           }
-          lwb[wq * kRows + CPW * w + 32 * ch + lane] = v[0];
+          lwb[wq * kRows + WOFF + 32 * ch + lane] = v[0];
         }
         if (tid == 0) EV(13, ii);
         named_bar_sync(bar_id, 128);
         if (kl < CPW) {
-          const int c = CPW * w + kl, o = c >> 4, r = c & 15;
+          // PP: a warpgroup without a tile in the item writes l = 0 (the combine skips the entry)
+          const int c = WOFF + kl, o = c >> 4, r = c & 15;
           if (o < I.n_slots && r < R.n_rows[o]) {
-            float* ent = p.ws + (int64_t)(R.entry_off[o] + r) * p.entry_stride;
+            float* ent = p.ws + (int64_t)(R.entry_off[o] + r + (PP ? 16 * w : 0)) * p.entry_stride;
             ent[0] = ((lrefm >> (kl >> 5)) & 1u) ? 0.f : mrun[c];  // column c = CPW w + kl is in chunk kl / 32
             ent[1] = lwb[c] + lwb[kRows + c] + lwb[2 * kRows + c] + lwb[3 * kRows + c];
           }
@@ -1655,9 +1689,14 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
       }
       if (C::AB == 1) {
         epilogue(ii, T - 1, qb);
+      } else if (PP && jw < 0) {
+        // PP: no tile of this item for this warpgroup: no accumulator to write; release the header now (an earlier
+        // item's epilogue may still be pending)
+        named_bar_sync(bar_id, 128);
+        if (kl == 0) mbar_arrive(smem_u32(&ms.recempty[qb]));
       } else {
         pend_ii = ii;
-        pend_Tl = T - 1;
+        pend_Tl = PP ? Tmine : T - 1;
         pend_qb = qb;
       }
     }
@@ -1678,13 +1717,13 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 
 }  // namespace
 
-template <bool kDef, int kRowsT>
+template <bool kDef, int kRowsT, bool kPP = false>
 cudaError_t launch_tc_variant(const AttnParams& p, const void* maps, cudaStream_t s) {
   static bool attr[64] = {};  // the max-dynamic-shared-memory opt-in is per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr[dev]) {
-    const cudaError_t e = cudaFuncSetAttribute(ra_tc_kernel<kDef, kRowsT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const cudaError_t e = cudaFuncSetAttribute(ra_tc_kernel<kDef, kRowsT, kPP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                Cfg<kDef, kRowsT>::SMEM);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr[dev] = true;
@@ -1701,7 +1740,7 @@ cudaError_t launch_tc_variant(const AttnParams& p, const void* maps, cudaStream_
   la[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = la;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, ra_tc_kernel<kDef, kRowsT>, *(const TcMaps*)maps, p);
+  return cudaLaunchKernelEx(&cfg, ra_tc_kernel<kDef, kRowsT, kPP>, *(const TcMaps*)maps, p);
 }
 
 cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStream_t s) {
@@ -1712,7 +1751,8 @@ cudaError_t launch_attention_tc(const AttnParams& p, const void* maps, cudaStrea
     if (p.tc_rows != 64) return cudaErrorInvalidValue;
     return launch_tc_variant<true, 64>(p, maps, s);
   }
-  return p.tc_rows == 128 ? launch_tc_variant<false, 128>(p, maps, s) : launch_tc_variant<false, 64>(p, maps, s);
+  if (p.tc_rows == 128) return launch_tc_variant<false, 128>(p, maps, s);
+  return p.tc_pp ? launch_tc_variant<false, 64, true>(p, maps, s) : launch_tc_variant<false, 64>(p, maps, s);
 }
 
 cudaError_t launch_stage(const AttnParams& p, int32_t n_images, cudaStream_t s) {
