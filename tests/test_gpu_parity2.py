@@ -268,3 +268,18 @@ def test_sequence_split_range_plans_merge(mode, G):
         Om = merge_lse(torch.stack(Os), torch.stack(ls))
         err = _check(fkv, scen, 31, 0, mode, seqs=range(len(batch)), O=Om)
         assert err <= TOL, (C, err)
+
+
+# ---- opt-in ping-pong key warpgroups (FKV_TC_PINGPONG): same parity bar -----------------------
+
+@pytest.mark.parametrize("pieces", [False, True])
+def test_pingpong_variant_needle(pieces, monkeypatch):
+    """The ping-pong variant (two partial entries per row and item, per-warpgroup running max) on the peaked /
+    needle inputs, with one-tile pieces (1-tile items: one warpgroup has no tile and writes l = 0)."""
+    monkeypatch.setenv("FKV_TC_PINGPONG", "1")
+    test_needle_and_peaked_queries("none", pieces, monkeypatch)
+
+
+def test_pingpong_variant_decode_loop(monkeypatch):
+    monkeypatch.setenv("FKV_TC_PINGPONG", "1")
+    test_decode_loop_three_steps("none")
