@@ -151,19 +151,24 @@ class Workload:
         self.batch = self.scen.batch()
         self.C = self.scen.q_len
 
-    def flops_per_layer(self, hkv_local, group):
-        """Algorithmic FLOPs of one layer (minimal form): QK^T and PV over the
-        visible keys of every query row, the rank-r rebuild per (owner, kv head,
-        key), q.K_lora, P.R_v and the late fusion per row."""
+    def flops_per_layer(self, hkv_local, group, mode="none"):
+        """Algorithmic FLOPs of one layer (minimal form): QK^T and PV over the visible keys of every query row,
+        the rank-r terms per (row, key) (NONE: q~.R_k and P.R_v; DEFERRED: q.K_lora and P.R_v), q~ and the late
+        fusion per row, and for DEFERRED the rank-r rebuild K_lora = R_k B_k per (residual owner, kv head, key)."""
         d, r = self.d, self.r
         tot = 0
         owners = {}
         for a in self.batch:
             L = self.scen.seqlen(a)
             vis = sum(L - self.C + i + 1 for i in range(self.C))  # causal visible keys over the chunk
-            tot += hkv_local * group * vis * (2 * d + 2 * d + 2 * r) + hkv_local * group * self.C * 2 * r * d
-            owners[a] = L
-        tot += sum(owners.values()) * hkv_local * 2 * r * d  # rebuild K_lora (DEFERRED form)
+            rank_term = 2 * r + (2 * d if mode == "deferred" else 2 * r)
+            tot += hkv_local * group * vis * (2 * d + 2 * d + rank_term) + hkv_local * group * self.C * 4 * r * d
+            # a same-agent branch shares its parent's residual pages over the prefix (one owner there)
+            s = self.scen.spec(a)
+            key = s.parent if (s.share_res and s.parent is not None) else a
+            owners[key] = max(owners.get(key, 0), L)
+        if mode == "deferred":
+            tot += sum(owners.values()) * hkv_local * 2 * r * d  # rebuild K_lora = R_k B_k
         return tot
 
 
@@ -561,7 +566,7 @@ def _roofline(run, wl, ms, hbm, tc_sus, src, config_name, mode):
     kname = KERNEL_NAMES.get(run.info.kernel, "?")
     window = "main kernel only (kernel 2: its stager launched before the window)"
     if run.prefill:
-        flops = wl.flops_per_layer(run.fkv.hkv, run.fkv.group)
+        flops = wl.flops_per_layer(run.fkv.hkv, run.fkv.group, mode)
         achieved = flops / (avg_main / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": tc_sus, "unit": "TFLOP/s", "frac": achieved / tc_sus,
                 "traffic": traffic, "peak_source": f"{src} (sustained bf16)", "alg_flops_per_launch": flops}
@@ -573,6 +578,11 @@ def _roofline(run, wl, ms, hbm, tc_sus, src, config_name, mode):
                 "traffic": traffic, "peak_source": src, "alg_bytes_per_launch": alg,
                 "frac_whole_layer": alg / (layer_ms / 1e3) / 1e9 / hbm,
                 "frac_vs_8tbs_spec": achieved / 8000.0}
+        # the other roof (decode lines against both): algorithmic FLOPs of the layer (QK^T, PV, the
+        # rank-r terms; the workload's sequence lengths) over the same launch time vs sustained bf16
+        flops = wl.flops_per_layer(run.fkv.hkv, run.fkv.group, mode)
+        roof["tensor_achieved_tflops"] = flops / (avg_main / 1e3) / 1e12
+        roof["tensor_frac"] = roof["tensor_achieved_tflops"] / tc_sus
     roof.update({"kernel": f"ResidualAttention {kname} (one launch per layer)", "event_window": window,
                  "avg_launch_ms": avg_main, "share_of_step": sum(main_ms) / len(run.alg_bytes or [1]) / ms})
     return roof
