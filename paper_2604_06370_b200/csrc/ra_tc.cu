@@ -74,6 +74,9 @@ constexpr float kLazyHi = FKV_LAZY_HI;
 #ifndef FKV_MAX_TREE
 #define FKV_MAX_TREE 0
 #endif
+#ifndef FKV_SFULL_SPIN
+#define FKV_SFULL_SPIN 0
+#endif
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
@@ -1395,7 +1398,13 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             }
           }
           if (ch == 0) {
+#if FKV_SFULL_SPIN
+            // diagnostics A/B: the key warps poll sfull with test_wait (no suspend) instead of the suspend-hint wait
+            while (!mbar_test(smem_u32(&ms.sfull[sb]), (T >> 1) & 1)) {
+            }
+#else
             mbar_wait(smem_u32(&ms.sfull[sb]), (T >> 1) & 1);
+#endif
             if (tid == 0) EV(3, T);
             tc_fence_after();
           }
