@@ -77,6 +77,10 @@ constexpr float kLazyHi = FKV_LAZY_HI;
 #ifndef FKV_SFULL_SPIN
 #define FKV_SFULL_SPIN 0
 #endif
+#ifndef FKV_SKIP_EMPTY
+#define FKV_SKIP_EMPTY 1
+#endif
+constexpr bool kSkipEmpty = FKV_SKIP_EMPTY;  // key warps skip the softmax of a chunk with no used query column
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
@@ -1380,6 +1384,21 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
           // ---- online softmax over the chunk's 32 query columns (Alg1.339-341) ----
+          if (kSkipEmpty && colmask[ch] == 0u) {
+            // no query row of the item in this chunk (a 1-slot private item leaves the second warpgroup idle):
+            // only the handshakes (the P^T columns are never read for a used row), the SMSP's MUFU and issue
+            // slots go to the other warpgroup's chain
+            if (ch == 0) {
+              mbar_wait(smem_u32(&ms.sfull[sb]), (T >> 1) & 1);
+              tc_fence_after();
+            }
+            if (ch == NCH - 1) {
+              tc_fence_before();
+              mbar_arrive(smem_u32(&ms.sfree[sb]));
+            }
+            if (ch == 0 && np >= (uint32_t)C::NPH) mbar_wait(smem_u32(&ms.pfree[ps]), ((np / C::NPH) - 1) & 1);
+            continue;
+          }
           const int cb = WOFF + 32 * ch;
           const uint16_t* P1 = R.pos1 + cb;  // key t visible iff t - k0 < P1[c]
           uint32_t vm = tvalid ? colmask[ch] : 0u;
