@@ -80,11 +80,11 @@ constexpr float kLazyHi = FKV_LAZY_HI;
 #ifndef FKV_SKIP_EMPTY
 #define FKV_SKIP_EMPTY 1
 #endif
-constexpr bool kSkipEmpty = FKV_SKIP_EMPTY;
+constexpr bool kSkipEmpty = FKV_SKIP_EMPTY;  // key warps skip the softmax of a chunk with no used query column
 #ifndef FKV_NARROW
 #define FKV_NARROW 0
 #endif
-constexpr bool kNarrow = FKV_NARROW;  // 8-column fast path for chunks whose used columns are the first 8 (A/B: -2.4%, off)  // key warps skip the softmax of a chunk with no used query column
+constexpr bool kNarrow = FKV_NARROW;  // 8-column fast path for chunks whose used columns are the first 8 (A/B: -2.4%, off)
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
