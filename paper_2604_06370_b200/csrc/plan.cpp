@@ -54,8 +54,8 @@ Plan* make_plan(Ctx& c, int32_t n, const fkv_seq* seqs, uint32_t flags, int64_t 
   const int32_t d_ = c.cfg.head_dim, r_ = c.cfg.rank;
   // diagnostics: FKV_PLAN_TIMING prints the planner's section times; FKV_PLAN_ASSUME_TC plans for kernel 2 on a
   // host-only ctx (planner profiling without a GPU; such a plan cannot run)
-  static const bool timing = getenv("FKV_PLAN_TIMING") != nullptr;
-  static const bool assume_tc = getenv("FKV_PLAN_ASSUME_TC") != nullptr;
+  const bool timing = getenv("FKV_PLAN_TIMING") != nullptr;
+  const bool assume_tc = getenv("FKV_PLAN_ASSUME_TC") != nullptr;
   auto tic = std::chrono::steady_clock::now();
   auto lap = [&](const char* what) {
     if (!timing) return;

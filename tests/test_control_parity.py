@@ -260,3 +260,42 @@ def test_eviction_partial_hit_bit_exact(seed):
         assert m.take_copy_log() == o.copies, step
         o.copies.clear()
         o.check_invariants()
+
+
+@pytest.mark.parametrize("pingpong", [False, True])
+def test_kernel2_plan_structure_c2(pingpong, monkeypatch):
+    """The tcgen05 (kernel 2) planner on the C2 tree, on a host ctx (FKV_PLAN_ASSUME_TC: plan only, no GPU):
+    the shared 32K segment of every kv head is split into 8 pieces of 32 tiles for each of its 4 row blocks
+    (16 agents x 4 branches x 4 q heads = 256 rows per kv head, 64 per CTA), each sequence's 129-key tail is
+    one 2-tile item, every slot gets 16 partial entries (32 with the ping-pong key warpgroups), and planning
+    is deterministic."""
+    from workloads import recipes
+    monkeypatch.setenv("FKV_PLAN_ASSUME_TC", "1")
+    if pingpong:
+        monkeypatch.setenv("FKV_TC_PINGPONG", "1")
+    scen = recipes.c2()
+    nb, nr = scen.pages_needed(128)
+    m = ForkKV(n_layers=1, n_q_heads=32, n_kv_heads=8, head_dim=128, rank=16, page_size=128, n_base_pages=nb + 8,
+               n_res_pages=nr + 8, dtype="bf16", rope_mode="none", device=None)
+    for ad in sorted({s.adapter for s in scen.agents}):
+        m.register_adapter(ad)
+    for s in scen.agents:
+        if s.parent is None:
+            m.create_root(s.id, s.adapter)
+        else:
+            m.fork(s.parent, s.fork_len, s.id, s.adapter, L.FORK_SHARE_RESIDUAL if s.share_res else 0)
+        if s.n_private:
+            m.append([s.id], [s.n_private], [1] * s.n_private)
+    batch = scen.batch()
+    pl = m.plan([(a, 1) for a in batch], upload=False)
+    info = pl.info
+    assert info.kernel == 2
+    assert info.n_segments == 1 + 64                      # one shared prefix segment + 64 private tails
+    hkv, shared_tiles, blocks, pieces = 8, 256, 4, 8
+    assert info.n_items == hkv * (blocks * pieces + 64)    # 768
+    assert info.key_tiles == hkv * (blocks * shared_tiles + 64 * 2)
+    per_slot = 32 if pingpong else 16
+    assert info.n_entries == hkv * (blocks * pieces * 4 + 64) * per_slot
+    pl2 = m.plan([(a, 1) for a in batch], upload=False)
+    for f in ("n_items", "n_entries", "key_tiles", "device_bytes", "workspace_bytes", "alg_bytes", "n_ctas"):
+        assert getattr(pl2.info, f) == getattr(info, f), f
