@@ -437,21 +437,27 @@ cudaError_t launch_synth_fill(void* dst, int32_t dtype, uint64_t seed, int32_t k
 // registers: all 2048-row C2 warps resident in one wave
 template <typename T>
 __global__ void __launch_bounds__(256, 2) combine128_kernel(AttnParams p) {
-  pdl_wait();
-  pdl_trigger();
+  // the plan's records (row -> entry range, entry ids, B_v address) are read before griddepcontrol.wait: the
+  // main kernel does not write them, so two of the dependent load round trips overlap its tail; the partial
+  // entries are read after the wait
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= p.n_out_rows) return;
-  const longlong2 cr = p.comb_rows[warp];
+  const bool live = warp < p.n_out_rows;
+  longlong2 cr = make_longlong2(0, 0);
+  if (live) cr = p.comb_rows[warp];
   const int e0 = (int)(cr.x & 0xffffffffll), e1 = (int)(cr.x >> 32);
+  const int my_e0 = live && lane < e1 - e0 ? p.out_entries[e0 + lane] : 0;
   // B_v^h rows (16 x 128) for the late fusion: prefetched into L1 now (one 128-byte line per lane), read at the end
   const T* bv = (const T*)cr.y + (int64_t)p.layer * p.adapter_layer_stride;
-  asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)bv + 128 * lane * (int)sizeof(T) / 2));
+  if (live) asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)bv + 128 * lane * (int)sizeof(T) / 2));
+  pdl_wait();
+  pdl_trigger();
+  if (!live) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   float accr = 0.f, l = 0.f, Mrun = -INFINITY;
   for (int eb = e0; eb < e1; eb += 32) {
     const int ne = min(32, e1 - eb);
-    const int my_e = lane < ne ? p.out_entries[eb + lane] : 0;
+    const int my_e = eb == e0 ? my_e0 : (lane < ne ? p.out_entries[eb + lane] : 0);
     const float* my = p.ws + (int64_t)my_e * p.entry_stride;
     const float2 ml = lane < ne ? *(const float2*)my : make_float2(-INFINITY, 0.f);
     for (int i0 = 0; i0 < ne; i0 += 16) {
