@@ -398,11 +398,18 @@ __global__ void __launch_bounds__(256) ra_stage_kernel(AttnParams p, int n_image
   // kernel, which triggers at entry, writes neither), while the image buffer may still be read by the previous
   // main kernel until the predecessor grid completes. So the loads overlap the predecessor (kv_write) and only
   // the stores wait; the main kernel waits for this grid's completion before it reads the images.
-  if (!kStageEarly) pdl_wait();
-  pdl_trigger();
+  // The dependents (the main kernel) launch only once every stager CTA has passed griddepcontrol.wait: the
+  // main kernel streams K/V pool rows before its own wait, and the predecessor (kv_write) writes the newest ones
+  if (!kStageEarly) {
+    pdl_wait();
+    pdl_trigger();
+  }
   const int ii = blockIdx.x;
   if (ii >= n_images) {
-    if (kStageEarly) pdl_wait();
+    if (kStageEarly) {
+      pdl_wait();
+      pdl_trigger();
+    }
     return;
   }
   __shared__ __align__(16) float qs[16][kD];
@@ -448,7 +455,10 @@ __global__ void __launch_bounds__(256) ra_stage_kernel(AttnParams p, int n_image
     uf2(acc2, a0, a1);
     acc = a0 + a1;
   }
-  if (kStageEarly) pdl_wait();  // the previous main kernel is done with the image buffer
+  if (kStageEarly) {
+    pdl_wait();     // the predecessor's pool rows are written; the previous main kernel is done with the images
+    pdl_trigger();  // only now may the main kernel launch (see above)
+  }
   *(uint4*)(img + (ch >> 3) * 2048 + kmajor_off(row, (ch & 7) * 8, 8, 1024, 0)) = v;
   if (def) {
     *(uint4*)(img + 4096 + mnmajor_off(n8, jj, 4, 1024, 512)) = bv;  // packed B_k image (RoPE partner order)
