@@ -283,3 +283,29 @@ def test_pingpong_variant_needle(pieces, monkeypatch):
 def test_pingpong_variant_decode_loop(monkeypatch):
     monkeypatch.setenv("FKV_TC_PINGPONG", "1")
     test_decode_loop_three_steps("none")
+
+
+@pytest.mark.parametrize("mode", ["none", "deferred"])
+def test_newest_rows_visible_in_bench_order(mode):
+    """bench.py's launch order: plan + upload first, then per step the new rows' write_kv and the attention back
+    to back on one stream (kv_write -> stager -> main kernel chained by programmatic dependent launch). With a
+    one-tile context the main kernel's first K / V loads read the page kv_write has just written: the stager
+    must not let the main kernel launch before kv_write completed (a race fixed in session 3)."""
+    scen = recipes.c1(prefix=96, private=4)
+    fkv = _ctx(scen, 32, 8, 128, mode, extra_pos=24)
+    driver.build(fkv, scen, seed=21)
+    batch = scen.batch()
+    stage = {}
+    for step in range(1, 13):
+        pos = [scen.seqlen(a) for a in batch]
+        fkv.append(batch, [1] * len(batch), synth.tokens(21, 0, step, len(batch)).tolist())
+        for a in batch:
+            scen.spec(a).n_private += 1
+        pl = fkv.plan([(a, 1) for a in batch])               # uploaded before the rows are written
+        Q = driver.make_queries(fkv, scen, 21, 0, step=step)
+        torch.cuda.synchronize()
+        for a, p in zip(batch, pos):
+            driver.write_rows(fkv, 21, a, a, p, 1, L.WRITE_ALL, 0, stage=stage)
+        O = fkv.residual_attention(pl, 0, Q)
+        err = _check(fkv, scen, 21, 0, mode, seqs=range(len(batch)), O=O, step=step)
+        assert err <= TOL, (step, err)
