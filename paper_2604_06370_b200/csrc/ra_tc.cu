@@ -372,12 +372,25 @@ __device__ __forceinline__ void st_global_v8(float* dst, const uint32_t* x) {
 
 // diagnostics: clock64 stamp of pipeline event e for index j (< 256) of CTA dbg_block (fkv_debug_timeline)
 // (EV: the kernel-uniform dbg_on test first, so the stamps cost one predicated branch when off)
+// The stamps are compiled out of the product build: their per-site tests cost issue slots in the key warps' loop
+// (A/B: C2 main kernel 90.8 -> 88.6 us). tools/timeline.py needs a -DFKV_TIMELINE=1 build
+// (bash tools/variants.sh tl -DFKV_TIMELINE=1; FKV_LIB_PATH=paper_2604_06370_b200/variants/libforkkv_tl.so)
+#ifndef FKV_TIMELINE
+#define FKV_TIMELINE 0
+#endif
+#if FKV_TIMELINE
 #define EV(e, j)                 \
   do {                           \
     if (dbg_on) ev(p, e, j);     \
   } while (0)
+#else
+#define EV(e, j) \
+  do {           \
+  } while (0)
+#endif
+// dbg_on (dbg != null and this CTA is dbg_block) is tested by EV once per site; only the index bound here
 __device__ __forceinline__ void ev(const AttnParams& p, int e, uint32_t j) {
-  if (p.dbg && (int)blockIdx.x == p.dbg_block && j < 256) p.dbg[e * 256 + j] = clock64();
+  if (j < 256) p.dbg[e * 256 + j] = clock64();
 }
 
 // permuted B_k column n' -> d, in 32-column quarter blocks b = 2w + q (w = d-half of key warpgroup w,

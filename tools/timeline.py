@@ -68,6 +68,14 @@ def main():
     torch.cuda.synchronize()
     lib.fkv_debug_timeline(fkv.ctx, None, 0)
     d = dbg.view(34, 256).cpu().numpy()
+    if not d[:30].any():
+        print("no pipeline stamps: the product build compiles them out; build a timeline variant with\n"
+              "  bash tools/variants.sh tl -DFKV_TIMELINE=1\nand run with "
+              "FKV_LIB_PATH=paper_2604_06370_b200/variants/libforkkv_tl.so")
+        dur = d[30, :148]
+        if dur.any():
+            print(f"CTA cycles: min {dur.min()} median {int(np.median(dur))} max {dur.max()}")
+        return
     gs, ge = d[32, :148], d[33, :148]
     if gs.any():
         gs, ge = gs[gs > 0], ge[ge > 0]
