@@ -71,20 +71,10 @@ constexpr bool kStageEarly = FKV_STAGE_EARLY;  // stager: loads and q~ before gr
 #define FKV_LAZY_HI 16
 #endif
 constexpr float kLazyHi = FKV_LAZY_HI;
-#ifndef FKV_MAX_TREE
-#define FKV_MAX_TREE 0
-#endif
-#ifndef FKV_SFULL_SPIN
-#define FKV_SFULL_SPIN 0
-#endif
 #ifndef FKV_SKIP_EMPTY
 #define FKV_SKIP_EMPTY 1
 #endif
 constexpr bool kSkipEmpty = FKV_SKIP_EMPTY;  // key warps skip the softmax of a chunk with no used query column
-#ifndef FKV_NARROW
-#define FKV_NARROW 0
-#endif
-constexpr bool kNarrow = FKV_NARROW;  // 8-column fast path for chunks whose used columns are the first 8 (A/B: -2.4%, off)
 constexpr int kKlBufs = 4;
 // TMEM columns (Cfg::tS / tO / tA): S^T[2 buffers] 0..127 | O^T, A^T of accumulator set 0 at 128, 192 |
 // NONE: set 1 at 256, 320 (double-buffered across items) | DEFERRED: K_lora [wg][4 bufs] x 32 at 256..511.
@@ -1444,13 +1434,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             }
           }
           if (ch == 0) {
-#if FKV_SFULL_SPIN
-            // diagnostics A/B: the key warps poll sfull with test_wait (no suspend) instead of the suspend-hint wait
-            while (!mbar_test(smem_u32(&ms.sfull[sb]), (T >> 1) & 1)) {
-            }
-#else
             mbar_wait(smem_u32(&ms.sfull[sb]), (T >> 1) & 1);
-#endif
             if (tid == 0) EV(3, T);
             tc_fence_after();
           }
@@ -1476,14 +1460,10 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           // underflow or overflow)
           const bool lazy0 = C::PVROW && kLazyStart && jm == 0 && causal_mask == 0;
           const bool lref = (lrefm >> ch) & 1u;
-          // narrow chunk: every used query column of the chunk lies in its first 8 (a private item's 4 rows): the
-          // fast path computes those 8 columns only, the other P^T columns are 0 (warp-uniform, per item)
-          const bool narrow = kNarrow && C::PVROW && (colmask[ch] >> 8) == 0u && !((causal_mask >> ch) & 1u);
           {
             const float4* mp = (const float4*)&mrun[cb];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              if (narrow && q >= 2) continue;
               const float4 m4 = (lazy0 || lref) ? make_float4(0.f, 0.f, 0.f, 0.f) : mp[q];
               const uint64_t s01 = f2(__uint_as_float(sr[4 * q]), __uint_as_float(sr[4 * q + 1]));
               const uint64_t s23 = f2(__uint_as_float(sr[4 * q + 2]), __uint_as_float(sr[4 * q + 3]));
@@ -1493,7 +1473,6 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
             if (vm != 0xffffffffu) {
 #pragma unroll
               for (int q = 0; q < 16; ++q) {
-                if (narrow && q >= 4) continue;
                 float a, b2;
                 uf2(x2[q], a, b2);
                 a = (vm >> (2 * q)) & 1u ? a : -INFINITY;
@@ -1501,25 +1480,12 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
                 x2[q] = f2(a, b2);
               }
             }
-#if FKV_MAX_TREE
-            // four independent max3 chains, then a 4-way combine (the serial chain was 16 dependent max3)
-            float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-              float a, b2;
-              uf2(x2[q], a, b2);
-              mq[q & 3] = max3(mq[q & 3], a, b2);
-            }
-            mx = max3(mq[0], mq[1], fmaxf(mq[2], mq[3]));
-#else
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              if (narrow && q >= 4) continue;
               float a, b2;
               uf2(x2[q], a, b2);
               mx = max3(mx, a, b2);
             }
-#endif
           }
           // lazy rescaling: only when some score exceeds the running max by > 2^kLazyHi
           float alpha_l = 1.f;  // this lane's column (cb + lane) rescale factor (row-sum partials)
@@ -1528,7 +1494,6 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           if (lazy0) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-              if (narrow && q >= 4) continue;
               float a, b2;
               uf2(x2[q], a, b2);
               out |= (a < -64.f && a > -INFINITY) || (b2 < -64.f && b2 > -INFINITY);
@@ -1657,10 +1622,6 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            if (narrow && q >= 4) {
-              pk[q] = 0u;
-              continue;
-            }
             float a, b2;
             uf2(x2[q], a, b2);
             const float ea = (kSkip & 16) ? a : ex2(a), eb = (kSkip & 16) ? b2 : ex2(b2);
