@@ -63,7 +63,10 @@ constexpr int kSkip = FKV_DIAG_SKIP;
 #ifndef FKV_STAGE_EARLY
 #define FKV_STAGE_EARLY 1
 #endif
-constexpr bool kStageEarly = FKV_STAGE_EARLY;  // stager: loads and q~ before griddepcontrol.wait (C2 +2.3%)
+constexpr bool kStageEarly = FKV_STAGE_EARLY;
+#ifndef FKV_PROD_SLEEP
+#define FKV_PROD_SLEEP 0  // ns the polling producer sleeps after a pass without progress (A/B: 0 > 20..200 >> 800)
+#endif  // stager: loads and q~ before griddepcontrol.wait (C2 +2.3%)
 // lazy-rescale headroom (log2 units): p = 2^(x - m) may reach 2^kLazyHi before the running max moves. fp32
 // accumulators and bf16 P hold 2^16 x 32K keys easily; a larger headroom makes the first-tile slow path (m = 0
 // reference, ~8 K cycles cold) and later rescales rarer
@@ -694,7 +697,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
         }
         if (!busy) break;
-        if (!progress) __nanosleep(200);  // polling warps have issue priority: yield the SMSP to the key warps
+        if (!progress) __nanosleep(FKV_PROD_SLEEP);  // polling warps have issue priority: yield the SMSP to the key warps
       }
       asm volatile("cp.async.wait_all;\n" ::: "memory");
     } else if (wid == 8 && lane == 0) {
@@ -821,7 +824,7 @@ __global__ void __launch_bounds__(384, 1) ra_tc_kernel(const __grid_constant__ T
           }
         }
         if (!busy) break;
-        if (!progress) __nanosleep(200);  // polling warps have issue priority: yield the SMSP to the key warps
+        if (!progress) __nanosleep(FKV_PROD_SLEEP);  // polling warps have issue priority: yield the SMSP to the key warps
       }
     } else if (wid == 9) {
       // ================= S-side MMA issuer (whole warp: uniform operands, one elected lane issues) =================
